@@ -1,0 +1,325 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path on BASELINE.json's metric.
+
+Workload (config.workload): cfg1 of BASELINE.json — batched pairwise
+Levenshtein, 10^6 DNA pairs per GPU, L ~ U[500,1500], b = a mutated at 5%
+substitutions + 1% indels (seeded synthetic stand-in).
+A step = one pass of the distance engine over the whole pair batch.
+
+  value  GCUPS (cells = sum |a|*|b|, untrimmed) with the sequences and pair
+         lists already resident in HBM; device time (CUDA events on the
+         launching stream), max over ranks, aggregated over all ranks.
+  e2e    same metric through the C ABI with HOST buffers: every step uploads
+         the step's sequences from pinned host memory (dm_seqset_create),
+         runs dm_lev_pairs (pair lists H2D, distances D2H) and frees them.
+
+--impl reference times the compiled reference (oracle/_ref, the unmodified
+divmsa C++ sources) on the box's host cores: divmsa::parallel_for +
+divmsa::levenshtein over a bounded sample of the same pairs per step.
+
+Multi-GPU (torchrun): pairs are independent, so each rank owns its own batch
+(weak scaling, no data-path collective); barrier + max-over-ranks timing.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+C_LEV = 10.0 / 32.0  # canonical INT32 ops per Levenshtein cell
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+def cpu_baseline(data, offs, n_pairs, budget_s=12.0, threads=None):
+    """Reference (oracle/_ref) on a bounded sample of the workload's pairs."""
+    import oracle
+    ref = oracle.reference()
+    threads = threads or os.cpu_count() or 1
+    seqs = [data[int(offs[i]):int(offs[i + 1])] for i in range(len(offs) - 1)]
+    lens = np.diff(offs).astype(np.float64)
+    # size the sample for ~budget_s at ~0.35 GCUPS/thread
+    cells_per_pair = float(np.mean(lens[0::2] * lens[1::2]))
+    k = int(max(64, min(n_pairs, budget_s * 0.35e9 * threads / cells_per_pair)))
+    ia = np.arange(k, dtype=np.uint32) * 2
+    ib = ia + 1
+    cells = float(np.sum(lens[ia] * lens[ib]))
+    t0 = time.perf_counter()
+    ref.lev_pairs(seqs, ia, ib, threads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": cells / dt / 1e9, "unit": "GCUPS", "cores": threads, "kind": "reference",
+            "sample": f"first {k} of the {n_pairs} cfg1 pairs ({cells:.3e} cells, {dt:.1f} s), "
+                      f"divmsa::parallel_for(grain 64)+levenshtein on {threads} host threads"}
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    import paper_2601_15458_b200 as dm  # only for the synthetic generator (host code)
+    data, offs = dm.synth(1, scale=args.scale)
+    import oracle
+    ref = oracle.reference()
+    threads = os.cpu_count() or 1
+    seqs = [data[int(offs[i]):int(offs[i + 1])] for i in range(len(offs) - 1)]
+    n_pairs = len(seqs) // 2
+    lens = np.diff(offs).astype(np.float64)
+    cells_per_pair = float(np.mean(lens[0::2] * lens[1::2]))
+    k = int(max(64, min(n_pairs, args.ref_step_s * 0.35e9 * threads / cells_per_pair)))
+    ia = np.arange(k, dtype=np.uint32) * 2
+    ib = ia + 1
+    cells = float(np.sum(lens[ia] * lens[ib]))
+    for _ in range(args.warmup):
+        ref.lev_pairs(seqs, ia[:max(1, k // 8)], ib[:max(1, k // 8)], threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ref.lev_pairs(seqs, ia, ib, threads=threads)
+    dt = time.perf_counter() - t0
+    v = cells * args.steps / dt / 1e9
+    line = {"metric": "levenshtein_gcups", "value": v, "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "cfg1: 1e6 DNA pairs, L~U[500,1500], 5% sub + 1% indel (batched Levenshtein)",
+                       "pairs_per_step": k, "scale": args.scale},
+            "cpu_baseline": {"value": v, "unit": "GCUPS", "cores": threads, "kind": "reference",
+                             "sample": f"first {k} cfg1 pairs per step ({cells:.3e} cells)"},
+            "e2e": {"value": v, "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scale", type=float, default=1.0, help="fraction of cfg1's 10^6 pairs per GPU")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    ap.add_argument("--ref-step-s", type=float, default=8.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        return run_reference(args)
+
+    rank, world, local = dist_env()
+    import torch
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2601_15458_b200 as dm
+    from paper_2601_15458_b200._lib import check, lib
+    import ctypes as C
+
+    ctx = dm.Context(local)
+    stream = torch.cuda.current_stream()
+    check(lib().dm_ctx_set_stream(ctx.handle, C.c_void_p(stream.cuda_stream)))
+
+    data, offs = dm.synth(1, scale=args.scale, seed=2601154581 + 1000003 * rank)
+    n_pairs = (len(offs) - 1) // 2
+    lens = np.diff(offs).astype(np.int64)
+    cells_step = int(np.sum(lens[0::2] * lens[1::2]))
+
+    # ---- device-resident run (value) ------------------------------------
+    ss = dm.SeqSet(data=data, offsets=offs, ctx=ctx)
+    ia = torch.arange(n_pairs, dtype=torch.int32, device="cuda") * 2
+    ib = ia + 1
+    out = torch.empty(n_pairs, dtype=torch.int32, device="cuda")
+    st = dm.dm_stats()
+
+    def step():
+        check(lib().dm_lev_pairs_device(ctx.handle, ss.handle, C.c_void_p(ia.data_ptr()),
+                                        C.c_void_p(ib.data_ptr()), n_pairs, C.c_void_p(out.data_ptr()),
+                                        C.byref(st)))
+        return st.kernel_ms, st.launches
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    kern_ms, launches = 0.0, 0
+    for _ in range(args.steps):
+        k, l = step()
+        kern_ms += k
+        launches += l
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms, kern_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms, kern_ms = float(t[0]), float(t[1])
+    ms_per_step = ms / args.steps
+    value = cells_step * world / (ms_per_step * 1e-3) / 1e9
+    kernel_gcups = cells_step / (kern_ms / args.steps * 1e-3) / 1e9
+
+    # parity spot-check of the timed output against the C restatement
+    import oracle
+    orc = oracle.restatement()
+    got = out.cpu().numpy().astype(np.uint32)
+    rs = np.random.default_rng(rank)
+    for i in rs.choice(n_pairs, 16, replace=False):
+        a = data[int(offs[2 * i]):int(offs[2 * i + 1])]
+        b = data[int(offs[2 * i + 1]):int(offs[2 * i + 2])]
+        if got[i] != orc.levenshtein(a, b):
+            raise SystemExit(f"bench: distance mismatch at pair {i}")
+    del ss
+
+    # ---- end-to-end through the C ABI with host buffers (e2e) ----------
+    pinned = torch.empty(len(data), dtype=torch.uint8, pin_memory=True)
+    pinned.numpy()[:] = np.frombuffer(data, dtype=np.uint8)
+    ia_h = (np.arange(n_pairs, dtype=np.uint32) * 2)
+    ib_h = ia_h + 1
+    out_h = np.empty(n_pairs, dtype=np.uint32)
+    offs_c = np.ascontiguousarray(offs, dtype=np.uint64)
+    u32p = C.POINTER(C.c_uint32)
+
+    def e2e_step():
+        h = C.c_void_p()
+        check(lib().dm_seqset_create(ctx.handle, C.cast(C.c_void_p(pinned.data_ptr()), C.c_char_p),
+                                     offs_c.ctypes.data_as(C.POINTER(C.c_uint64)), len(offs) - 1, C.byref(h)))
+        check(lib().dm_lev_pairs(ctx.handle, h, ia_h.ctypes.data_as(u32p), ib_h.ctypes.data_as(u32p), n_pairs,
+                                 out_h.ctypes.data_as(u32p), None))
+        lib().dm_seqset_destroy(h)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t[0])
+    if not np.array_equal(out_h, got):
+        raise SystemExit("bench: e2e distances differ from the device-resident run")
+    e2e = {"value": cells_step * world / e2e_s / 1e9, "unit": "GCUPS",
+           "h2d_bytes_per_step": int(len(data) + offs_c.nbytes + 8 * n_pairs),
+           "d2h_bytes_per_step": int(4 * n_pairs)}
+
+    # ---- roofline: INT32 lane-op peak measured on this box --------------
+    peaks = []
+    for mode in (0, 1, 2):
+        v = C.c_double()
+        check(lib().dm_int32_peak(ctx.handle, mode, C.byref(v)))
+        peaks.append(v.value)
+    p_int32 = max(peaks)
+    roof_gcups = p_int32 / C_LEV / 1e9
+    roofline = {"bound": "int32", "achieved": kernel_gcups, "peak": roof_gcups, "unit": "GCUPS",
+                "frac": kernel_gcups / roof_gcups, "traffic": None,
+                "peak_source": (f"measured INT32 lane-op/s {p_int32:.3e} (max of LOP3 {peaks[0]:.3e}, "
+                                f"IADD3 {peaks[1]:.3e}, LOP3+IMAD {peaks[2]:.3e}) / c_lev=10/32 ops per cell"),
+                "kernel": "lev_kernel<NP=2,R> (all buckets)",
+                "cells_executed_per_step": int(st.cells_executed)}
+
+    line = {"metric": "levenshtein_gcups", "value": value, "unit": "GCUPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": "cfg1: 1e6 DNA pairs/GPU, L~U[500,1500], 5% sub + 1% indel "
+                                   "(batched Levenshtein, BASELINE.json configs[1])",
+                       "pairs_per_gpu": n_pairs, "cells_per_step_per_gpu": cells_step,
+                       "l2": "inputs (%.1f GB/GPU) larger than L2" % (len(data) / 1e9),
+                       "parallelism": f"dp{world} (independent pair batches)"},
+            "gpu_launches": int(launches), "clocks": clk, "e2e": e2e, "roofline": roofline}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(data, offs, n_pairs, args.cpu_budget_s)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

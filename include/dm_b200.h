@@ -1,0 +1,158 @@
+/* dm_b200.h — C ABI of the B200-native MuSAlS hot path (libdmb200.so).
+ *
+ * Plain pointers and sizes only; no exceptions and no C++/torch types cross
+ * this boundary. Every call returns a status (DM_OK = 0); on failure
+ * dm_last_error() returns a thread-local message whose text matches the
+ * reference exception it replaces (e.g. "...not de-duplicated",
+ * "...exceeds alignment width ..."), and the status says which exception
+ * type the reference throws: DM_EINVAL <-> std::invalid_argument,
+ * DM_ERUNTIME <-> std::runtime_error.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/proj):
+ *   dm_levenshtein / dm_lev_pairs   divmsa::levenshtein          include/divmsa/distance.hpp:11
+ *   dm_lev_one_to_many              distance_scan                src/cluster_tree.cpp:31-41
+ *   dm_geometric_median             divmsa::geometric_median     include/divmsa/cluster_tree.hpp:56-59
+ *   dm_build_tree                   divmsa::build_tree           include/divmsa/cluster_tree.hpp:66-67
+ *   dm_nw_align / dm_nw_batch       divmsa::nw_align             include/divmsa/pairwise.hpp:89-90
+ *   dm_insert_gap_columns           divmsa::insert_gap_columns   include/divmsa/msa_merge.hpp:34-35
+ *   dm_align_all                    divmsa::align_all            include/divmsa/msa_merge.hpp:47-49
+ *   dm_msa                          build_tree + align_all       src/pipeline.cpp:113-128
+ * Python FFI that binds these today: python/py_module.cpp:77-155.
+ */
+#ifndef DM_B200_H
+#define DM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DM_OK 0
+#define DM_EINVAL 1   /* std::invalid_argument in the reference */
+#define DM_ERUNTIME 2 /* std::runtime_error in the reference */
+#define DM_ECUDA 3    /* CUDA failure (no device, launch error, ...) */
+#define DM_ENOMEM 4
+
+typedef struct dm_ctx dm_ctx;       /* one CUDA device + stream + scratch */
+typedef struct dm_seqset dm_seqset; /* device-resident residues + bit-plane profiles */
+typedef struct dm_pw dm_pw;         /* one PairwiseResult */
+typedef struct dm_msa_out dm_msa_out;
+
+/* Mirrors divmsa::ClusterNode (cluster_tree.hpp:20-34), 40 bytes. */
+typedef struct {
+    uint32_t begin, end, center, radius, pole_l, pole_r;
+    int32_t left, right, parent;
+    uint32_t depth;
+} dm_node;
+
+/* Per-call device timing and work counters (filled when non-NULL). */
+typedef struct {
+    double kernel_ms;        /* device time of the hot kernels (CUDA events) */
+    double total_ms;         /* device time of the whole call incl. copies */
+    uint64_t cells;          /* oracle-equivalent cells: sum |a|*|b| (untrimmed) */
+    uint64_t cells_executed; /* cells the kernels actually computed (padding incl.) */
+    uint64_t launches;       /* kernels launched */
+    double tree_ms, align_ms;
+    uint64_t lev_calls, nw_calls;
+} dm_stats;
+
+const char* dm_last_error(void);
+int dm_abi_version(void);
+
+/* ---- context ---------------------------------------------------------- */
+int dm_ctx_create(int device, dm_ctx** out);
+int dm_ctx_destroy(dm_ctx* ctx);
+int dm_ctx_sync(dm_ctx* ctx);
+/* Issue all further work of ctx on `stream` (a cudaStream_t), e.g. a torch
+ * stream, so callers can time with events on their own stream. */
+int dm_ctx_set_stream(dm_ctx* ctx, void* stream);
+/* INT32 lane-op peak of this device (mode 0 LOP3, 1 IADD3, 2 LOP3+IMAD). */
+int dm_int32_peak(dm_ctx* ctx, int mode, double* lane_ops_per_s);
+/* Multi-GPU: this rank's share of sharded work (rank, world). The shards
+ * exchange results with dm_ctx's NCCL communicator when one is attached. */
+int dm_ctx_set_shard(dm_ctx* ctx, int rank, int world);
+
+/* ---- sequences -------------------------------------------------------- */
+/* Residues of n sequences, concatenated in `data`; sequence i is
+ * data[offsets[i], offsets[i+1]). Raw bytes are compared. */
+int dm_seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint32_t n,
+                     dm_seqset** out);
+int dm_seqset_destroy(dm_seqset* s);
+uint32_t dm_seqset_count(const dm_seqset* s);
+int dm_seqset_planes(const dm_seqset* s); /* bit-planes used by the distance engine */
+
+/* ---- distance engine (Levenshtein) ------------------------------------ */
+uint32_t dm_levenshtein(dm_ctx* ctx, const char* a, uint64_t na, const char* b, uint64_t nb,
+                        int* status);
+/* out[i] = levenshtein(seq ia[i], seq ib[i]); host arrays. */
+int dm_lev_pairs(dm_ctx* ctx, const dm_seqset* s, const uint32_t* ia, const uint32_t* ib,
+                 uint64_t n, uint32_t* out, dm_stats* st);
+/* Same with DEVICE arrays (ia, ib, out resident in HBM); no host copies. */
+int dm_lev_pairs_device(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia,
+                        const uint32_t* d_ib, uint64_t n, uint32_t* d_out, dm_stats* st);
+/* distance_scan: out[i] = levenshtein(seq from, seq members[i]). */
+int dm_lev_one_to_many(dm_ctx* ctx, const dm_seqset* s, uint32_t from, const uint32_t* members,
+                       uint64_t n, uint32_t* out, dm_stats* st);
+int dm_geometric_median(dm_ctx* ctx, const dm_seqset* s, const uint32_t* members, uint64_t n,
+                        uint64_t seed, uint64_t exact_cap, uint32_t* out);
+
+/* ---- guide tree ------------------------------------------------------- */
+/* nodes: capacity 2n-1; order: n. Errors: DM_ERUNTIME "cannot build a cluster
+ * tree from zero sequences" / "...input was not de-duplicated". */
+int dm_build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_cap,
+                  dm_node* nodes, uint64_t* nnodes, uint32_t* order, dm_stats* st);
+
+/* ---- pairwise aligner (Gotoh NW) -------------------------------------- */
+/* table: 128x128 int16 indexed by char (ScoringScheme::score, pairwise.hpp:30);
+ * has_symbol: 128 flags (ScoringScheme::has_symbol); open_surcharge: gap_open
+ * in affine mode, 0 in flat mode (pairwise.hpp:36-38). */
+int dm_nw_align(dm_ctx* ctx, const char* a, uint64_t na, const char* b, uint64_t nb,
+                const int16_t* table, const uint8_t* has_symbol, int open_surcharge,
+                int gap_extend, dm_pw** out);
+/* Batched: job k aligns a_k = A[a_off[k], a_off[k+1]) against b_k likewise. */
+int dm_nw_batch(dm_ctx* ctx, const char* A, const uint64_t* a_off, const char* B,
+                const uint64_t* b_off, uint32_t njobs, const int16_t* table,
+                const uint8_t* has_symbol, int open_surcharge, int gap_extend, dm_pw** out,
+                dm_stats* st);
+int64_t dm_pw_score(const dm_pw* p, uint32_t k);
+uint64_t dm_pw_len(const dm_pw* p, uint32_t k);
+int dm_pw_aligned(const dm_pw* p, uint32_t k, char* a_out, char* b_out);
+uint64_t dm_pw_ngaps_a(const dm_pw* p, uint32_t k);
+uint64_t dm_pw_ngaps_b(const dm_pw* p, uint32_t k);
+int dm_pw_gaps(const dm_pw* p, uint32_t k, uint32_t* gaps_a, uint32_t* gaps_b);
+void dm_pw_free(dm_pw* p);
+
+/* ---- MSA builder ------------------------------------------------------ */
+/* rows: nrows x width; out: nrows x (width + npos). Errors as msa_merge.cpp:37-44. */
+int dm_insert_gap_columns(dm_ctx* ctx, const char* rows, uint64_t nrows, uint64_t width,
+                          const uint32_t* pos, uint64_t npos, char* out);
+/* align_all over a tree from dm_build_tree (or the reference). */
+int dm_align_all(dm_ctx* ctx, const dm_seqset* s, const dm_node* nodes, uint64_t nnodes,
+                 const uint32_t* order, const int16_t* table, const uint8_t* has_symbol,
+                 int open_surcharge, int gap_extend, dm_msa_out** out, dm_stats* st);
+/* build_tree + align_all, device-resident between the two. */
+int dm_msa(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_cap,
+           const int16_t* table, const uint8_t* has_symbol, int open_surcharge,
+           int gap_extend, dm_msa_out** out, dm_stats* st);
+uint64_t dm_msa_width(const dm_msa_out* m);
+uint64_t dm_msa_rows(const dm_msa_out* m);
+/* rows in tree order (row r carries sequence order[r]); buf: rows x width. */
+int dm_msa_copy_rows(const dm_msa_out* m, char* buf);
+int dm_msa_copy_row_seq(const dm_msa_out* m, uint32_t* row_to_sequence);
+uint64_t dm_msa_nnodes(const dm_msa_out* m);
+int dm_msa_copy_tree(const dm_msa_out* m, dm_node* nodes, uint32_t* order);
+void dm_msa_free(dm_msa_out* m);
+
+/* ---- synthetic inputs --------------------------- */
+/* cfg 0..4 at `scale` (1.0 = full size). Returns concatenated residues +
+ * offsets (free with dm_free). For cfg 1, sequence 2i / 2i+1 form pair i. */
+int dm_synth(int cfg, double scale, uint64_t seed, char** data, uint64_t** offsets,
+             uint64_t* n);
+void dm_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

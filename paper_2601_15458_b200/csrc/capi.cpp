@@ -1,0 +1,237 @@
+// extern "C" boundary of libdmb200.so (include/dm_b200.h). Maps internal
+// exceptions onto status codes + a thread-local message, so no C++ exception
+// ever crosses the ABI.
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "dm_internal.h"
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return DM_OK;
+    } catch (const dm::invalid_argument& e) {
+        g_err = e.what();
+        return DM_EINVAL;
+    } catch (const dm::cuda_error& e) {
+        g_err = e.what();
+        return DM_ECUDA;
+    } catch (const dm::runtime_error& e) {
+        g_err = e.what();
+        return DM_ERUNTIME;
+    } catch (const std::bad_alloc& e) {
+        g_err = "out of memory";
+        return DM_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return DM_ERUNTIME;
+    }
+}
+
+void require(bool ok, const char* msg) {
+    if (!ok) throw dm::invalid_argument(msg);
+}
+}  // namespace
+
+extern "C" {
+
+const char* dm_last_error(void) { return g_err.c_str(); }
+int dm_abi_version(void) { return 1; }
+
+int dm_ctx_create(int device, dm_ctx** out) {
+    return guard([&] {
+        require(out != nullptr, "null output pointer");
+        int count = 0;
+        DM_CUDA(cudaGetDeviceCount(&count));
+        if (device < 0 || device >= count) throw dm::cuda_error("CUDA device " + std::to_string(device) + " not present");
+        DM_CUDA(cudaSetDevice(device));
+        auto* c = new dm_ctx;
+        c->device = device;
+        cudaDeviceProp prop;
+        DM_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10) {
+            delete c;
+            throw dm::cuda_error(std::string("libdmb200 is built for sm_100a; device is ") + prop.name);
+        }
+        c->sm_count = prop.multiProcessorCount;
+        DM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = c->stream;
+        DM_CUDA(cudaEventCreate(&c->ev0));
+        DM_CUDA(cudaEventCreate(&c->ev1));
+        *out = c;
+    });
+}
+
+int dm_ctx_destroy(dm_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        cudaEventDestroy(ctx->ev0);
+        cudaEventDestroy(ctx->ev1);
+        if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+        delete ctx;
+    });
+}
+
+int dm_ctx_sync(dm_ctx* ctx) {
+    return guard([&] { DM_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+int dm_ctx_set_stream(dm_ctx* ctx, void* stream) {
+    return guard([&] {
+        require(ctx != nullptr, "null context");
+        DM_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (ctx->own_stream) {
+            DM_CUDA(cudaStreamDestroy(ctx->own_stream));
+            ctx->own_stream = nullptr;
+        }
+        ctx->stream = static_cast<cudaStream_t>(stream);
+    });
+}
+
+int dm_int32_peak(dm_ctx* ctx, int mode, double* lane_ops_per_s) {
+    return guard([&] {
+        require(ctx && lane_ops_per_s, "null argument");
+        require(mode >= 0 && mode <= 2, "mode must be 0, 1 or 2");
+        *lane_ops_per_s = dm::int32_peak(ctx, mode);
+    });
+}
+
+int dm_ctx_set_shard(dm_ctx* ctx, int rank, int world) {
+    return guard([&] {
+        require(world >= 1 && rank >= 0 && rank < world, "invalid shard (rank, world)");
+        ctx->rank = rank;
+        ctx->world = world;
+    });
+}
+
+int dm_seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint32_t n,
+                     dm_seqset** out) {
+    return guard([&] {
+        require(ctx && out && offsets, "null argument");
+        DM_CUDA(cudaSetDevice(ctx->device));
+        *out = dm::seqset_create(ctx, data, offsets, n);
+    });
+}
+
+int dm_seqset_destroy(dm_seqset* s) {
+    return guard([&] { delete s; });
+}
+
+uint32_t dm_seqset_count(const dm_seqset* s) { return s ? s->n : 0; }
+int dm_seqset_planes(const dm_seqset* s) { return s ? s->planes : 0; }
+
+static void fill_stats(dm_stats* st, const dm::LevTotals& t, float total_ms) {
+    if (!st) return;
+    std::memset(st, 0, sizeof(*st));
+    st->kernel_ms = t.kernel_ms;
+    st->total_ms = total_ms;
+    st->cells = t.cells;
+    st->cells_executed = t.cells_exec;
+    st->launches = t.launches;
+}
+
+uint32_t dm_levenshtein(dm_ctx* ctx, const char* a, uint64_t na, const char* b, uint64_t nb,
+                        int* status) {
+    uint32_t d = 0;
+    int rc = guard([&] {
+        require(ctx != nullptr, "null context");
+        std::string buf;
+        buf.append(a, na);
+        buf.append(b, nb);
+        uint64_t off[3] = {0, na, na + nb};
+        dm_seqset* s = dm::seqset_create(ctx, buf.data(), off, 2);
+        std::vector<dm::LevItem> items{{0, 1, 0}};
+        uint32_t* d_out = ctx->out.as<uint32_t>(1);
+        try {
+            dm::lev_run_host_items(ctx, s, items, d_out, nullptr, false);
+            DM_CUDA(cudaMemcpyAsync(&d, d_out, 4, cudaMemcpyDeviceToHost, ctx->stream));
+            DM_CUDA(cudaStreamSynchronize(ctx->stream));
+        } catch (...) {
+            delete s;
+            throw;
+        }
+        delete s;
+    });
+    if (status) *status = rc;
+    return d;
+}
+
+int dm_lev_pairs(dm_ctx* ctx, const dm_seqset* s, const uint32_t* ia, const uint32_t* ib,
+                 uint64_t n, uint32_t* out, dm_stats* st) {
+    return guard([&] {
+        require(ctx && s, "null argument");
+        for (uint64_t i = 0; i < n; ++i)
+            require(ia[i] < s->n && ib[i] < s->n, "sequence index out of range");
+        cudaStream_t stream = ctx->stream;
+        cudaEvent_t t0, t1;
+        DM_CUDA(cudaEventCreate(&t0));
+        DM_CUDA(cudaEventCreate(&t1));
+        DM_CUDA(cudaEventRecord(t0, stream));
+        uint32_t* d_ab = ctx->aux3.as<uint32_t>(2 * n + 1);
+        uint32_t* d_out = ctx->out.as<uint32_t>(n + 1);
+        if (n) {
+            DM_CUDA(cudaMemcpyAsync(d_ab, ia, n * 4, cudaMemcpyHostToDevice, stream));
+            DM_CUDA(cudaMemcpyAsync(d_ab + n, ib, n * 4, cudaMemcpyHostToDevice, stream));
+        }
+        dm::LevTotals tot;
+        dm::lev_run_device_pairs(ctx, s, d_ab, d_ab + n, n, d_out, &tot, st != nullptr);
+        if (n) DM_CUDA(cudaMemcpyAsync(out, d_out, n * 4, cudaMemcpyDeviceToHost, stream));
+        DM_CUDA(cudaEventRecord(t1, stream));
+        DM_CUDA(cudaEventSynchronize(t1));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, t0, t1);
+        cudaEventDestroy(t0);
+        cudaEventDestroy(t1);
+        fill_stats(st, tot, ms);
+    });
+}
+
+int dm_lev_pairs_device(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia,
+                        const uint32_t* d_ib, uint64_t n, uint32_t* d_out, dm_stats* st) {
+    return guard([&] {
+        require(ctx && s, "null argument");
+        cudaEvent_t t0, t1;
+        DM_CUDA(cudaEventCreate(&t0));
+        DM_CUDA(cudaEventCreate(&t1));
+        DM_CUDA(cudaEventRecord(t0, ctx->stream));
+        dm::LevTotals tot;
+        dm::lev_run_device_pairs(ctx, s, d_ia, d_ib, n, d_out, &tot, st != nullptr);
+        DM_CUDA(cudaEventRecord(t1, ctx->stream));
+        DM_CUDA(cudaEventSynchronize(t1));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, t0, t1);
+        cudaEventDestroy(t0);
+        cudaEventDestroy(t1);
+        fill_stats(st, tot, ms);
+    });
+}
+
+int dm_lev_one_to_many(dm_ctx* ctx, const dm_seqset* s, uint32_t from, const uint32_t* members,
+                       uint64_t n, uint32_t* out, dm_stats* st) {
+    return guard([&] {
+        require(ctx && s, "null argument");
+        require(from < s->n, "sequence index out of range");
+        std::vector<dm::LevItem> items(n);
+        for (uint64_t i = 0; i < n; ++i) {
+            require(members[i] < s->n, "sequence index out of range");
+            items[i] = dm::LevItem{from, members[i], (uint32_t)i};
+        }
+        uint32_t* d_out = ctx->out.as<uint32_t>(n + 1);
+        dm::LevTotals tot;
+        dm::lev_run_host_items(ctx, s, items, d_out, &tot, st != nullptr);
+        if (n) DM_CUDA(cudaMemcpyAsync(out, d_out, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        DM_CUDA(cudaStreamSynchronize(ctx->stream));
+        fill_stats(st, tot, 0.f);
+    });
+}
+
+void dm_free(void* p) { std::free(p); }
+
+}  // extern "C"

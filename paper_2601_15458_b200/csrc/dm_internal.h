@@ -1,0 +1,147 @@
+// Internal declarations shared by the CUDA translation units of libdmb200.so.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dm_b200.h"
+
+namespace dm {
+
+// Internal errors are exceptions; capi.cpp maps them onto DM_* status codes.
+struct invalid_argument : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct runtime_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct cuda_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define DM_CUDA(call)                                                                   \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            throw ::dm::cuda_error(std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+// Growable device scratch buffer (never shrinks; reused across calls).
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* get(size_t bytes) {
+        if (bytes > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            size_t c = bytes + bytes / 4 + 256;
+            DM_CUDA(cudaMalloc(&p, c));
+            cap = c;
+        }
+        return p;
+    }
+    template <class T>
+    T* as(size_t count) { return static_cast<T*>(get(count * sizeof(T))); }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* get(size_t bytes) {
+        if (bytes > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            size_t c = bytes + bytes / 4 + 256;
+            DM_CUDA(cudaMallocHost(&p, c));
+            cap = c;
+        }
+        return p;
+    }
+    template <class T>
+    T* as(size_t count) { return static_cast<T*>(get(count * sizeof(T))); }
+    ~PinnedBuf() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+}  // namespace dm
+
+struct dm_ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;      // stream every call is issued on
+    cudaStream_t own_stream = nullptr;  // created by dm_ctx_create (null once replaced)
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int rank = 0, world = 1;
+    // scratch for the distance engine
+    dm::DevBuf items, out, counter, aux, aux2, aux3;
+    dm::PinnedBuf pin_items, pin_out;
+    // scratch for the aligner / merge scheduler
+    dm::DevBuf nw_in, nw_jobs, nw_trace, nw_res, nw_gaps, rows_a, rows_b, colmap, tree_buf;
+    uint64_t launches = 0;
+};
+
+// Device-resident sequence store.
+struct dm_seqset {
+    dm_ctx* ctx = nullptr;
+    uint32_t n = 0;
+    int planes = 2;    // bit-planes per residue code: 2 (<=4 symbols), 5 (<=32), 8
+    int nsym = 0;      // distinct residue bytes
+    uint8_t code_of[256] = {};
+    // host mirrors
+    std::vector<uint32_t> len;     // residues per sequence
+    std::vector<uint64_t> off;     // byte offset of sequence i in d_codes (16-B aligned)
+    std::vector<uint64_t> blk_off; // first 64-row block of sequence i in d_planes
+    std::vector<uint64_t> raw_off; // offset of sequence i in d_raw (as given by the caller)
+    // device
+    uint8_t* d_raw = nullptr;      // raw residue bytes (what NW scores and the MSA prints)
+    uint64_t* d_raw_off = nullptr;
+    uint8_t* d_codes = nullptr;    // dense codes 0..nsym-1, 16-B aligned per sequence
+    uint64_t* d_off = nullptr;
+    uint32_t* d_len = nullptr;
+    uint64_t* d_blk = nullptr;
+    uint64_t* d_planes = nullptr; // [block][plane] 64-bit words
+    uint64_t total_blocks = 0;
+    ~dm_seqset();
+};
+
+namespace dm {
+
+// One Levenshtein job: distance(seq pat, seq txt) -> out[slot].
+struct LevItem {
+    uint32_t pat;
+    uint32_t txt;
+    uint32_t slot;
+};
+
+struct LevTotals {
+    uint64_t cells = 0, cells_exec = 0, launches = 0;
+    float kernel_ms = 0.f;
+};
+
+// Run a batch of device-resident items (already oriented, bucket-sorted
+// by the planner). d_out is indexed by item.slot.
+void lev_run_host_items(dm_ctx* ctx, const dm_seqset* s, std::vector<LevItem>& items,
+                        uint32_t* d_out, LevTotals* tot, bool time_kernels);
+// Pairs given as device arrays (bench path): builds items on the device.
+void lev_run_device_pairs(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia,
+                          const uint32_t* d_ib, uint64_t n, uint32_t* d_out, LevTotals* tot,
+                          bool time_kernels);
+
+dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint32_t n);
+
+// Guide tree (tree.cu / tree_host.cpp).
+void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_cap,
+                std::vector<dm_node>& nodes, std::vector<uint32_t>& order, dm_stats* st);
+double int32_peak(dm_ctx* ctx, int mode);
+uint32_t geometric_median(dm_ctx* ctx, const dm_seqset* s, const uint32_t* members, uint64_t n,
+                          uint64_t seed, uint64_t exact_cap);
+
+}  // namespace dm

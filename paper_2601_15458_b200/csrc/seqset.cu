@@ -1,0 +1,190 @@
+// Device-resident sequence store: raw residues, a dense
+// re-coding of the residues for the distance engine, and per-sequence
+// bit-plane profiles.
+//
+// Levenshtein compares raw bytes (distance.cpp:40 `ai != b[j]`),
+// so the code map is a bijection over the bytes that actually occur: S
+// distinct bytes get codes 0..S-1 and the distance engine works on
+// NP = 2 (S <= 4, e.g. ACGT), 5 (S <= 32, proteins) or 8 bit-planes.
+//
+// Plane layout: sequence i owns blocks [blk_off[i], blk_off[i] + ceil(len/64));
+// block b holds NP 64-bit words, word k bit t = bit k of code(residue 64b+t).
+// Residues past the end of the sequence are zero (their rows are never read
+// by the final count; see lev.cu).
+#include <algorithm>
+#include <cstring>
+
+#include "dm_internal.h"
+
+namespace dm {
+namespace {
+
+__global__ void census_kernel(const uint8_t* __restrict__ raw, uint64_t nbytes,
+                              unsigned int* __restrict__ present) {
+    __shared__ unsigned int sm[8];
+    if (threadIdx.x < 8) sm[threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nbytes; i += stride) {
+        const unsigned c = raw[i];
+        atomicOr(&sm[c >> 5], 1u << (c & 31));
+    }
+    __syncthreads();
+    if (threadIdx.x < 8 && sm[threadIdx.x]) atomicOr(&present[threadIdx.x], sm[threadIdx.x]);
+}
+
+// One warp per sequence: recode raw bytes into the 16-B aligned code buffer.
+__global__ void recode_kernel(const uint8_t* __restrict__ raw, const uint64_t* __restrict__ raw_off,
+                              const uint64_t* __restrict__ off, uint32_t n,
+                              const uint8_t* __restrict__ lut, uint8_t* __restrict__ codes) {
+    __shared__ uint8_t slut[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) slut[i] = lut[i];
+    __syncthreads();
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t s = warp; s < n; s += nw) {
+        const uint64_t a = raw_off[s], e = raw_off[s + 1], o = off[s];
+        for (uint64_t i = a + lane; i < e; i += 32) codes[o + (i - a)] = slut[raw[i]];
+    }
+}
+
+template <int NP>
+__global__ void planes_kernel(const uint8_t* __restrict__ codes, const uint64_t* __restrict__ off,
+                              const uint32_t* __restrict__ len, const uint64_t* __restrict__ blk,
+                              uint32_t n, uint64_t* __restrict__ planes) {
+    // one thread per sequence block; sequences located by binary search on blk
+    const uint64_t total = blk[n];
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < total; b += stride) {
+        uint32_t lo = 0, hi = n;  // largest s with blk[s] <= b
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (blk[mid] <= b) lo = mid; else hi = mid;
+        }
+        // skip empty sequences sharing the same start
+        while (lo + 1 < n && blk[lo + 1] <= b) ++lo;
+        const uint32_t s = lo;
+        const uint64_t local = b - blk[s];
+        const uint32_t L = len[s];
+        const uint8_t* p = codes + off[s] + local * 64;
+        const uint64_t rem = (uint64_t)L - local * 64;
+        const int cnt = rem < 64 ? (int)rem : 64;
+        uint64_t w[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) w[k] = 0;
+        for (int t = 0; t < cnt; ++t) {
+            const unsigned c = p[t];
+#pragma unroll
+            for (int k = 0; k < NP; ++k) w[k] |= (uint64_t)((c >> k) & 1u) << t;
+        }
+#pragma unroll
+        for (int k = 0; k < NP; ++k) planes[b * NP + k] = w[k];
+    }
+}
+
+}  // namespace
+
+dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint32_t n) {
+    auto* s = new dm_seqset;
+    s->ctx = ctx;
+    s->n = n;
+    try {
+        s->len.resize(n);
+        s->off.resize(n + 1);
+        s->blk_off.resize(n + 1);
+        uint64_t o = 0, b = 0;
+        for (uint32_t i = 0; i < n; ++i) {
+            if (offsets[i + 1] < offsets[i]) throw invalid_argument("sequence offsets must be non-decreasing");
+            const uint64_t L = offsets[i + 1] - offsets[i];
+            if (L > 0xffffffffull) throw invalid_argument("sequence longer than 2^32-1 residues");
+            s->len[i] = (uint32_t)L;
+            s->off[i] = o;
+            s->blk_off[i] = b;
+            o += (L + 16) & ~uint64_t(15);  // >= 1 pad byte, 16-B aligned starts
+            b += (L + 63) / 64;
+        }
+        s->off[n] = o;
+        s->blk_off[n] = b;
+        s->total_blocks = b;
+        s->raw_off.assign(offsets, offsets + n + 1);
+        const uint64_t base = offsets[0];
+        const uint64_t nbytes = offsets[n] - base;
+        cudaStream_t st = ctx->stream;
+
+        uint8_t* d_raw = nullptr;
+        uint64_t* d_raw_off = nullptr;
+        DM_CUDA(cudaMalloc(&d_raw, nbytes + 16));
+        DM_CUDA(cudaMalloc(&d_raw_off, (n + 1) * sizeof(uint64_t)));
+        s->d_raw = d_raw;
+        s->d_raw_off = d_raw_off;
+        std::vector<uint64_t> rel(n + 1);
+        for (uint32_t i = 0; i <= n; ++i) rel[i] = offsets[i] - base;
+        if (nbytes) DM_CUDA(cudaMemcpyAsync(d_raw, data + base, nbytes, cudaMemcpyHostToDevice, st));
+        DM_CUDA(cudaMemcpyAsync(d_raw_off, rel.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st));
+        s->raw_off = rel;
+
+        unsigned int* d_present = ctx->aux.as<unsigned int>(8);
+        DM_CUDA(cudaMemsetAsync(d_present, 0, 32, st));
+        if (nbytes) {
+            const int grid = (int)std::min<uint64_t>((nbytes + 4095) / 4096, (uint64_t)ctx->sm_count * 8);
+            census_kernel<<<std::max(grid, 1), 256, 0, st>>>(d_raw, nbytes, d_present);
+            DM_CUDA(cudaGetLastError());
+        }
+        unsigned int present[8];
+        DM_CUDA(cudaMemcpyAsync(present, d_present, 32, cudaMemcpyDeviceToHost, st));
+        DM_CUDA(cudaStreamSynchronize(st));
+        uint8_t lut[256] = {};
+        int nsym = 0;
+        for (int c = 0; c < 256; ++c)
+            if (present[c >> 5] & (1u << (c & 31))) lut[c] = (uint8_t)nsym++;
+        std::memcpy(s->code_of, lut, 256);
+        s->nsym = nsym;
+        s->planes = nsym <= 4 ? 2 : (nsym <= 32 ? 5 : 8);
+
+        DM_CUDA(cudaMalloc(&s->d_codes, o + 16));
+        DM_CUDA(cudaMalloc(&s->d_off, (n + 1) * sizeof(uint64_t)));
+        DM_CUDA(cudaMalloc(&s->d_len, std::max<size_t>(n, 1) * sizeof(uint32_t)));
+        DM_CUDA(cudaMalloc(&s->d_blk, (n + 1) * sizeof(uint64_t)));
+        DM_CUDA(cudaMalloc(&s->d_planes, std::max<uint64_t>(b, 1) * s->planes * sizeof(uint64_t)));
+        DM_CUDA(cudaMemsetAsync(s->d_codes, 0, o + 16, st));
+        DM_CUDA(cudaMemcpyAsync(s->d_off, s->off.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st));
+        if (n) DM_CUDA(cudaMemcpyAsync(s->d_len, s->len.data(), n * 4, cudaMemcpyHostToDevice, st));
+        DM_CUDA(cudaMemcpyAsync(s->d_blk, s->blk_off.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st));
+        uint8_t* d_lut = (uint8_t*)ctx->aux2.get(256);
+        DM_CUDA(cudaMemcpyAsync(d_lut, lut, 256, cudaMemcpyHostToDevice, st));
+        if (n) {
+            const int grid = (int)std::min<uint64_t>((n + 7) / 8, (uint64_t)ctx->sm_count * 16);
+            recode_kernel<<<grid, 256, 0, st>>>(d_raw, d_raw_off, s->d_off, n, d_lut, s->d_codes);
+            DM_CUDA(cudaGetLastError());
+        }
+        if (b) {
+            const int grid = (int)std::min<uint64_t>((b + 255) / 256, (uint64_t)ctx->sm_count * 16);
+            if (s->planes == 2)
+                planes_kernel<2><<<grid, 256, 0, st>>>(s->d_codes, s->d_off, s->d_len, s->d_blk, n, s->d_planes);
+            else if (s->planes == 5)
+                planes_kernel<5><<<grid, 256, 0, st>>>(s->d_codes, s->d_off, s->d_len, s->d_blk, n, s->d_planes);
+            else
+                planes_kernel<8><<<grid, 256, 0, st>>>(s->d_codes, s->d_off, s->d_len, s->d_blk, n, s->d_planes);
+            DM_CUDA(cudaGetLastError());
+        }
+        ctx->launches += 3;
+        DM_CUDA(cudaStreamSynchronize(st));
+    } catch (...) {
+        delete s;
+        throw;
+    }
+    return s;
+}
+
+}  // namespace dm
+
+dm_seqset::~dm_seqset() {
+    if (d_raw) cudaFree(d_raw);
+    if (d_raw_off) cudaFree(d_raw_off);
+    if (d_codes) cudaFree(d_codes);
+    if (d_off) cudaFree(d_off);
+    if (d_len) cudaFree(d_len);
+    if (d_blk) cudaFree(d_blk);
+    if (d_planes) cudaFree(d_planes);
+}

@@ -1,0 +1,133 @@
+"""Parity of the GPU distance engine (K1) with the CPU oracle.
+
+Pins restate /root/reference/proj/tests/test_distance.cpp:11-28 and
+acceptance.cpp:163-189; random sweeps compare every distance bit-exactly with
+the C restatement and the compiled reference."""
+import random
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def rand_str(rng, n, alphabet="ACGT"):
+    return "".join(rng.choice(alphabet) for _ in range(n))
+
+
+@pytest.mark.parametrize("a,b,d", [
+    ("KITTEN", "SITTING", 3), ("", "", 0), ("A", "", 1), ("", "ACGT", 4), ("ACGT", "ACGT", 0),
+    ("A", "C", 1), ("AC", "CA", 2),
+    # trims must never change the value (test_distance.cpp:21-28)
+    ("ABCXDEF", "ABCYDEF", 1), ("AAAA", "AAA", 1), ("XXXABC", "ABC", 3), ("ABC", "ABCXXX", 3),
+    ("AAAA", "AAAA", 0),
+])
+def test_known_pairs(dm, ctx, a, b, d):
+    assert dm.levenshtein(a, b, ctx) == d
+
+
+def test_recursive_definition_small(dm, ctx, orc):
+    # test_distance.cpp:30-42 / acceptance #3: short random pairs, both orders
+    rng = random.Random(1003)
+    seqs, ia, ib = [], [], []
+    for _ in range(500):
+        a, b = rand_str(rng, rng.randrange(13)), rand_str(rng, rng.randrange(13))
+        ia.append(len(seqs)); seqs.append(a)
+        ib.append(len(seqs)); seqs.append(b)
+    ss = dm.SeqSet(seqs, ctx)
+    fwd = dm.lev_pairs(ss, ia, ib)
+    rev = dm.lev_pairs(ss, ib, ia)
+    want = [orc.levenshtein(seqs[x], seqs[y]) for x, y in zip(ia, ib)]
+    assert list(fwd) == want
+    assert list(rev) == want
+
+
+@pytest.mark.parametrize("alphabet", ["ACGT", "ACGTURYSWKMBDHVN", "ARNDCQEGHILKMFPSTWYV",
+                                      "".join(chr(c) for c in range(33, 127))])
+def test_block_boundaries(dm, ctx, orc, alphabet):
+    """Lengths straddling 32/64/128/.../4096 rows exercise every (G, R) bucket."""
+    rng = random.Random(len(alphabet))
+    edges = [1, 2, 31, 32, 33, 63, 64, 65, 127, 128, 129, 191, 192, 255, 256, 257, 511, 512, 513,
+             700, 1023, 1024, 1025, 1500, 2047, 2048, 2049, 3000, 4095, 4096, 4097]
+    seqs, ia, ib = [], [], []
+    for la in edges:
+        for _ in range(3):
+            lb = max(0, la + rng.randint(-40, 40))
+            a = rand_str(rng, la, alphabet)
+            # related pair: mutate a
+            b = list(a[:lb]) + [rng.choice(alphabet) for _ in range(max(0, lb - la))]
+            for k in range(max(1, lb // 20)):
+                if b:
+                    b[rng.randrange(len(b))] = rng.choice(alphabet)
+            ia.append(len(seqs)); seqs.append(a)
+            ib.append(len(seqs)); seqs.append("".join(b))
+    ss = dm.SeqSet(seqs, ctx)
+    got = dm.lev_pairs(ss, ia, ib)
+    want = [orc.levenshtein(seqs[x], seqs[y]) for x, y in zip(ia, ib)]
+    assert list(got) == want
+
+
+def test_unrelated_long(dm, ctx, ref):
+    rng = random.Random(5)
+    seqs = [rand_str(rng, rng.randint(1, 2600)) for _ in range(120)]
+    ia = list(range(0, 120, 2))
+    ib = list(range(1, 120, 2))
+    ss = dm.SeqSet(seqs, ctx)
+    assert np.array_equal(dm.lev_pairs(ss, ia, ib), ref.lev_pairs(seqs, ia, ib))
+
+
+def test_cfg1_sample_vs_reference(dm, ctx, ref):
+    """cfg1-shaped pairs (L in [500,1500], 5% sub + 1% indel) vs the compiled reference."""
+    data, offs = dm.synth(1, scale=0.003)  # 3000 pairs
+    seqs = dm.split(data, offs)
+    ss = dm.SeqSet(data=data, offsets=offs, ctx=ctx)
+    n = len(seqs) // 2
+    ia = np.arange(n) * 2
+    ib = ia + 1
+    got, st = dm.lev_pairs(ss, ia, ib, stats=True)
+    want = ref.lev_pairs(seqs, ia, ib)
+    assert np.array_equal(got, want)
+    assert st["cells"] == sum(len(seqs[a]) * len(seqs[b]) for a, b in zip(ia, ib))
+
+
+def test_one_to_many(dm, ctx, ref):
+    data, offs = dm.synth(0, scale=0.3)
+    seqs = dm.split(data, offs)
+    ss = dm.SeqSet(data=data, offsets=offs, ctx=ctx)
+    members = np.arange(len(seqs))
+    got = dm.lev_one_to_many(ss, 7, members)
+    want = ref.lev_pairs(seqs, np.full(len(seqs), 7), members)
+    assert np.array_equal(got, want)
+    assert got[7] == 0
+
+
+def test_batch_sizes_and_grouping(dm, ctx, orc):
+    """Tiny batches use wide groups (G up to 32); results must not depend on it."""
+    rng = random.Random(9)
+    seqs = [rand_str(rng, rng.randint(900, 1700)) for _ in range(6)]
+    ss = dm.SeqSet(seqs, ctx)
+    want = {(x, y): orc.levenshtein(seqs[x], seqs[y]) for x in range(6) for y in range(6)}
+    for k in (1, 2, 5, 36):
+        pairs = list(want)[:k]
+        got = dm.lev_pairs(ss, [p[0] for p in pairs], [p[1] for p in pairs])
+        assert list(got) == [want[p] for p in pairs]
+
+
+def test_cfg1_full_properties(dm, ctx, orc):
+    """Full cfg1 batch (10^6 pairs): size-independent checks plus a sampled oracle."""
+    data, offs = dm.synth(1, scale=1.0)
+    ss = dm.SeqSet(data=data, offsets=offs, ctx=ctx)
+    n = (len(offs) - 1) // 2
+    ia = np.arange(n, dtype=np.uint32) * 2
+    ib = ia + 1
+    d = dm.lev_pairs(ss, ia, ib)
+    d2 = dm.lev_pairs(ss, ib, ia)
+    assert np.array_equal(d, d2)  # symmetry through a different orientation path
+    lens = np.diff(offs).astype(np.int64)
+    la, lb = lens[ia], lens[ib]
+    assert (d >= np.abs(la - lb)).all() and (d <= np.maximum(la, lb)).all()
+    rng = np.random.default_rng(3)
+    for i in rng.choice(n, 200, replace=False):
+        a = data[offs[2 * i]:offs[2 * i + 1]]
+        b = data[offs[2 * i + 1]:offs[2 * i + 2]]
+        assert d[i] == orc.levenshtein(a, b)
