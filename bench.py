@@ -299,7 +299,7 @@ def main():
     roofline = {"bound": "int32", "achieved": kernel_gcups, "peak": roof_gcups, "unit": "GCUPS",
                 "frac": kernel_gcups / roof_gcups, "traffic": None,
                 "peak_source": (f"measured INT32 lane-op/s {p_int32:.3e} (max of LOP3 {peaks[0]:.3e}, "
-                                f"IADD3 {peaks[1]:.3e}, LOP3+IMAD {peaks[2]:.3e}) / c_lev=10/32 ops per cell"),
+                                f"IMAD {peaks[1]:.3e}, LOP3+IMAD {peaks[2]:.3e}) / c_lev=10/32 ops per cell"),
                 "kernel": "lev_kernel<NP=2,R> (all buckets)",
                 "cells_executed_per_step": int(st.cells_executed)}
 

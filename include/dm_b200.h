@@ -68,7 +68,7 @@ int dm_ctx_sync(dm_ctx* ctx);
 /* Issue all further work of ctx on `stream` (a cudaStream_t), e.g. a torch
  * stream, so callers can time with events on their own stream. */
 int dm_ctx_set_stream(dm_ctx* ctx, void* stream);
-/* INT32 lane-op peak of this device (mode 0 LOP3, 1 IADD3, 2 LOP3+IMAD). */
+/* INT32 lane-op peak of this device (mode 0 LOP3 (ALU), 1 IMAD (FMA), 2 LOP3+IMAD). */
 int dm_int32_peak(dm_ctx* ctx, int mode, double* lane_ops_per_s);
 /* Multi-GPU: this rank's share of sharded work (rank, world). The shards
  * exchange results with dm_ctx's NCCL communicator when one is attached. */

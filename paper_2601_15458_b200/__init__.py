@@ -152,6 +152,47 @@ def lev_one_to_many(seqset: SeqSet, origin: int, members, stats: bool = False):
     return (out, s.as_dict()) if stats else out
 
 
+NODE_FIELDS = ("begin", "end", "center", "radius", "pole_l", "pole_r", "left", "right", "parent", "depth")
+NO_SEQUENCE = 0xFFFFFFFF  # cluster_tree.hpp:15 kNoSequence
+
+
+def nodes_to_array(nodes, count: int) -> np.ndarray:
+    return np.array([[getattr(nodes[i], f) for f in NODE_FIELDS] for i in range(count)], dtype=np.int64)
+
+
+def array_to_nodes(arr: np.ndarray):
+    out = (dm_node * len(arr))()
+    for i, row in enumerate(np.asarray(arr, dtype=np.int64)):
+        for f, v in zip(NODE_FIELDS, row):
+            setattr(out[i], f, int(v))
+    return out
+
+
+def build_tree(seqset: SeqSet, seed: int = 42, exact_cap: int = 100, stats: bool = False):
+    """divmsa::build_tree (cluster_tree.hpp:66-67) on the GPU.
+
+    Returns (nodes, order): nodes is an int64 array [2n-1, 10] with columns
+    NODE_FIELDS in the reference's BFS numbering; order the uint32 permutation."""
+    n = seqset.n
+    nodes = (dm_node * max(2 * n - 1, 1))()
+    order = np.zeros(max(n, 1), dtype=np.uint32)
+    nn = C.c_uint64()
+    s = dm_stats()
+    check(lib().dm_build_tree(seqset.ctx.handle, seqset.handle, int(seed), int(exact_cap), nodes, C.byref(nn),
+                              _ptr(order), C.byref(s)))
+    res = (nodes_to_array(nodes, nn.value), order[:n].copy())
+    return res + (s.as_dict(),) if stats else res
+
+
+def geometric_median(seqset: SeqSet, members, seed: int, exact_cap: int = 100) -> int:
+    """divmsa::geometric_median (cluster_tree.hpp:56-59) on the GPU."""
+    members = _u32(members)
+    out = C.c_uint32()
+    check(lib().dm_geometric_median(seqset.ctx.handle, seqset.handle, _ptr(members), len(members), int(seed),
+                                    int(exact_cap), C.byref(out)))
+    return int(out.value)
+
+
 def synth(cfg: int, scale: float = 1.0, seed: int = 0):
     """Seeded synthetic inputs of BASELINE config `cfg`.
 

@@ -232,6 +232,42 @@ int dm_lev_one_to_many(dm_ctx* ctx, const dm_seqset* s, uint32_t from, const uin
     });
 }
 
+int dm_geometric_median(dm_ctx* ctx, const dm_seqset* s, const uint32_t* members, uint64_t n,
+                        uint64_t seed, uint64_t exact_cap, uint32_t* out) {
+    return guard([&] {
+        require(ctx && s && out, "null argument");
+        *out = dm::geometric_median(ctx, s, members, n, seed, exact_cap);
+    });
+}
+
+int dm_build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_cap,
+                  dm_node* nodes, uint64_t* nnodes, uint32_t* order, dm_stats* st) {
+    return guard([&] {
+        require(ctx && s && nodes && nnodes && order, "null argument");
+        std::vector<dm_node> nv;
+        std::vector<uint32_t> ov;
+        if (st) std::memset(st, 0, sizeof(*st));
+        cudaEvent_t t0, t1;
+        DM_CUDA(cudaEventCreate(&t0));
+        DM_CUDA(cudaEventCreate(&t1));
+        DM_CUDA(cudaEventRecord(t0, ctx->stream));
+        dm::build_tree(ctx, s, seed, exact_cap, nv, ov, st);
+        DM_CUDA(cudaEventRecord(t1, ctx->stream));
+        DM_CUDA(cudaEventSynchronize(t1));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, t0, t1);
+        cudaEventDestroy(t0);
+        cudaEventDestroy(t1);
+        if (st) {
+            st->tree_ms = ms;
+            st->total_ms = ms;
+        }
+        std::memcpy(nodes, nv.data(), nv.size() * sizeof(dm_node));
+        std::memcpy(order, ov.data(), ov.size() * sizeof(uint32_t));
+        *nnodes = nv.size();
+    });
+}
+
 void dm_free(void* p) { std::free(p); }
 
 }  // extern "C"

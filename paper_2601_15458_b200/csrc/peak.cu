@@ -3,11 +3,10 @@
 // bf16, so the integer peak is measured on the box, at the clocks of the run.
 //
 // mode 0: independent LOP3 chains            (ALU pipe only)
-// mode 1: independent IADD3 chains           (ALU pipe only)
+// mode 1: independent IMAD chains            (FMA pipe only)
 // mode 2: LOP3 chains interleaved with IMAD  (ALU + FMA pipes, dual issue)
-// Each chain step is exactly one SASS instruction (inline PTX lop3 / mad.lo;
-// IADD3 from a 3-operand add the compiler fuses); 8 chains per thread give
-// ILP well past the 4-cycle latency.
+// Each chain step is exactly one SASS instruction (inline PTX lop3 / mad.lo);
+// 8 chains per thread give ILP well past the 4-cycle latency.
 #include "dm_internal.h"
 
 namespace dm {
@@ -25,8 +24,6 @@ __global__ void __launch_bounds__(256) int_peak_kernel(uint32_t* out, int iters,
             for (int k = 0; k < 8; ++k) {
                 if (MODE == 0 || (MODE == 2 && (k & 1) == 0)) {
                     asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[k]) : "r"(b), "r"(c));
-                } else if (MODE == 1) {
-                    a[k] = a[k] + b + c;
                 } else {
                     asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[k]) : "r"(b | 1u), "r"(c));
                 }
@@ -61,7 +58,7 @@ double int32_peak(dm_ctx* ctx, int mode) {
     DM_CUDA(cudaEventSynchronize(ctx->ev1));
     float ms = 0;
     DM_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-    // lane-ops: threads * iters * 16 unroll * 8 chains (mode 1: IADD3 = 1 op)
+    // lane-ops: threads * iters * 16 unroll * 8 chains, one instruction each
     const double ops = (double)blocks * 256 * iters * 16.0 * 8.0 * reps;
     return ops / (ms * 1e-3);
 }

@@ -1,0 +1,653 @@
+// Guide tree (SURVEY.md §2.2 K3/K4 + the level scheduler): divisive
+// clustering of cluster_tree.cpp:168-235 with every distance on the GPU.
+//
+// Per level of the reference's BFS frontier the work is four dependent
+// batches: median all-pairs -> center sweep -> pole_l sweep -> pole_r sweep
+// (cluster_tree.cpp:76-109). Here:
+//   * "big" nodes (more members than the small-subtree threshold T) are run
+//     level by level; each phase is ONE distance-engine batch over all big
+//     nodes of the level, followed by a reduction kernel (median argmin, sweep
+//     argmax, stable partition) that keeps the decision on the device;
+//   * a node with 2 <= |C| <= T (T = min(exact_cap, 128)) has every distance
+//     its whole subtree will ever ask for inside its own |C|x|C| matrix: the
+//     median of a node this small uses all members as candidates
+//     (cluster_tree.cpp:128-129) and every descendant works on a subset. So
+//     the matrix is computed once (one batch over all such roots) and
+//     subtree_kernel resolves the whole subtree in shared memory, one CTA
+//     per root. This is exact: no distance is approximated or skipped, only
+//     recomputation of identical pairs is avoided.
+// Seeds stay on the host, bit-identical: FNV-1a over the current member
+// slice (:18-27) -> combine_seed -> mt19937_64 -> Floyd's sample_distinct,
+// sorted (rng.hpp:14-59). Ties: argmin/argmax go to the lowest SEQUENCE index
+// (:48-50, :159-163); the partition is stable (:98-109); children are numbered
+// left then right in frontier order (:212-231) by a final BFS renumbering.
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <random>
+#include <unordered_set>
+
+#include "dm_internal.h"
+
+namespace dm {
+namespace {
+
+constexpr uint32_t kNo = 0xffffffffu;
+constexpr int kSubMax = 128;  // largest subtree resolved in shared memory
+
+// ---------------------------------------------------------------- host rng
+uint64_t mix_seed(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+uint64_t combine_seed(uint64_t seed, uint64_t salt) { return mix_seed(seed ^ mix_seed(salt)); }
+uint64_t bounded_draw(std::mt19937_64& g, uint64_t bound) {
+    const uint64_t limit = UINT64_MAX - UINT64_MAX % bound;
+    uint64_t v;
+    do v = g(); while (v >= limit);
+    return v % bound;
+}
+std::vector<uint64_t> sample_distinct(std::mt19937_64& g, uint64_t n, uint64_t k) {
+    std::vector<uint64_t> out;
+    if (k >= n) {
+        out.resize(n);
+        std::iota(out.begin(), out.end(), 0);
+        return out;
+    }
+    std::unordered_set<uint64_t> picked;
+    picked.reserve(k * 2);
+    for (uint64_t j = n - k; j < n; ++j) {
+        const uint64_t t = bounded_draw(g, j + 1);
+        picked.insert(picked.count(t) ? j : t);
+    }
+    out.assign(picked.begin(), picked.end());
+    std::sort(out.begin(), out.end());
+    return out;
+}
+uint64_t hash_members(const uint32_t* m, size_t n) {
+    uint64_t h = 14695981039346656037ULL;
+    for (size_t i = 0; i < n; ++i) {
+        h ^= m[i];
+        h *= 1099511628211ULL;
+    }
+    return h;
+}
+
+// ------------------------------------------------------------ reductions
+// lexicographic (primary, id) keys; argmin prefers smaller, argmax larger
+// primary, both prefer the LOWER id on ties.
+struct Key {
+    uint64_t v;
+    uint32_t id;
+    uint32_t idx;
+};
+__device__ __forceinline__ bool better_min(const Key& a, const Key& b) {
+    return a.v < b.v || (a.v == b.v && a.id < b.id);
+}
+__device__ __forceinline__ bool better_max(const Key& a, const Key& b) {
+    return a.v > b.v || (a.v == b.v && a.id < b.id);
+}
+template <bool MIN>
+__device__ Key block_reduce(Key k, Key* sh) {
+    for (int o = 16; o > 0; o >>= 1) {
+        Key t;
+        t.v = __shfl_down_sync(0xffffffffu, k.v, o);
+        t.id = __shfl_down_sync(0xffffffffu, k.id, o);
+        t.idx = __shfl_down_sync(0xffffffffu, k.idx, o);
+        if (MIN ? better_min(t, k) : better_max(t, k)) k = t;
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = k;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i)
+            if (MIN ? better_min(sh[i], k) : better_max(sh[i], k)) k = sh[i];
+        sh[0] = k;
+    }
+    __syncthreads();
+    return sh[0];
+}
+
+// K3: median of each big node from its k x k candidate matrix (upper triangle
+// filled at slot i*k+j, i<j): argmin of uint64 row sums (cluster_tree.cpp:152-165).
+__global__ void median_argmin_kernel(const uint32_t* __restrict__ mat, const uint64_t* __restrict__ mat_off,
+                                     const uint32_t* __restrict__ kk, const uint32_t* __restrict__ cand,
+                                     const uint64_t* __restrict__ cand_off, uint32_t* __restrict__ center) {
+    __shared__ Key sh[32];
+    const uint32_t v = blockIdx.x;
+    const uint32_t k = kk[v];
+    const uint32_t* M = mat + mat_off[v];
+    const uint32_t* C = cand + cand_off[v];
+    Key best{~0ull, kNo, 0};
+    for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
+        uint64_t s = 0;
+        for (uint32_t j = 0; j < k; ++j) {
+            if (j == i) continue;
+            s += i < j ? M[(uint64_t)i * k + j] : M[(uint64_t)j * k + i];
+        }
+        Key c{s, C[i], i};
+        if (better_min(c, best)) best = c;
+    }
+    best = block_reduce<true>(best, sh);
+    if (threadIdx.x == 0) center[v] = best.id;
+}
+
+// K4: radius = max distance, argmax with ties to the lowest sequence index
+// (cluster_tree.cpp:44-54, :83-84) over each node's slice of a sweep.
+__global__ void sweep_argmax_kernel(const uint32_t* __restrict__ dist, const uint32_t* __restrict__ order,
+                                    const uint32_t* __restrict__ nb, const uint32_t* __restrict__ ne,
+                                    uint32_t* __restrict__ maxv, uint32_t* __restrict__ argid) {
+    __shared__ Key sh[32];
+    const uint32_t v = blockIdx.x;
+    Key best{0, kNo, 0};
+    bool any = false;
+    for (uint32_t p = nb[v] + threadIdx.x; p < ne[v]; p += blockDim.x) {
+        Key c{dist[p], order[p], p};
+        if (!any || better_max(c, best)) best = c;
+        any = true;
+    }
+    if (!any) best = Key{0, kNo, 0};
+    best = block_reduce<false>(best, sh);
+    if (threadIdx.x == 0) {
+        maxv[v] = (uint32_t)best.v;
+        argid[v] = best.id;
+    }
+}
+
+// Stable partition of each node slice: d_l <= d_r to the left
+// (cluster_tree.cpp:98-109). One CTA per node; ballot-scan over warps.
+__global__ void partition_kernel(uint32_t* __restrict__ order, uint32_t* __restrict__ tmp,
+                                 const uint32_t* __restrict__ dl, const uint32_t* __restrict__ dr,
+                                 const uint32_t* __restrict__ nb, const uint32_t* __restrict__ ne,
+                                 uint32_t* __restrict__ mid) {
+    __shared__ uint32_t wcnt[32];
+    __shared__ uint32_t base_l, base_r, total_l;
+    const uint32_t v = blockIdx.x;
+    const uint32_t b = nb[v], e = ne[v];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    // pass 1: count lefts
+    uint32_t cnt = 0;
+    for (uint32_t p = b + threadIdx.x; p < e; p += blockDim.x) cnt += dl[p] <= dr[p];
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, o);
+    if (l == 0) wcnt[w] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int i = 0; i < nw; ++i) t += wcnt[i];
+        total_l = t;
+        base_l = 0;
+        base_r = 0;
+    }
+    __syncthreads();
+    const uint32_t L = total_l;
+    // pass 2: chunked stable scatter (chunk = blockDim)
+    for (uint32_t c0 = b; c0 < e; c0 += blockDim.x) {
+        const uint32_t p = c0 + threadIdx.x;
+        const bool in = p < e;
+        const bool left = in && dl[p] <= dr[p];
+        const unsigned ml = __ballot_sync(0xffffffffu, left);
+        const unsigned mr = __ballot_sync(0xffffffffu, in && !left);
+        __syncthreads();
+        if (l == 0) wcnt[w] = __popc(ml) | (__popc(mr) << 16);
+        __syncthreads();
+        uint32_t pl = 0, pr = 0;
+        for (int i = 0; i < w; ++i) {
+            pl += wcnt[i] & 0xffff;
+            pr += wcnt[i] >> 16;
+        }
+        const unsigned lt = (1u << l) - 1u;
+        if (left) tmp[b + base_l + pl + __popc(ml & lt)] = order[p];
+        else if (in) tmp[b + L + base_r + pr + __popc(mr & lt)] = order[p];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t sl = 0, sr = 0;
+            for (int i = 0; i < nw; ++i) {
+                sl += wcnt[i] & 0xffff;
+                sr += wcnt[i] >> 16;
+            }
+            base_l += sl;
+            base_r += sr;
+        }
+        __syncthreads();
+    }
+    for (uint32_t p = b + threadIdx.x; p < e; p += blockDim.x) order[p] = tmp[p];
+    if (threadIdx.x == 0) mid[v] = L;
+}
+
+// Record of one node of a small subtree; links are local ids.
+struct SubRec {
+    uint32_t b, e, center, radius, pole_l, pole_r;
+    int32_t left, right, parent;
+    uint32_t depth;
+};
+
+// Resolves a whole subtree of <= kSubMax members from its distance matrix.
+__global__ void __launch_bounds__(128) subtree_kernel(
+    uint32_t* __restrict__ order, const uint32_t* __restrict__ root_begin, const uint32_t* __restrict__ root_k,
+    const uint64_t* __restrict__ mat_off, const uint32_t* __restrict__ mats, const uint64_t* __restrict__ rec_off,
+    SubRec* __restrict__ recs, int* __restrict__ err) {
+    extern __shared__ uint32_t smem[];
+    __shared__ Key sh[32];
+    __shared__ uint32_t qb[2 * kSubMax], qe[2 * kSubMax], qd[2 * kSubMax];
+    __shared__ int32_t qp[2 * kSubMax];
+    __shared__ uint32_t ids[kSubMax], ord[kSubMax], tmp[kSubMax];
+    __shared__ uint32_t s_tail, s_bad, s_L;
+    const uint32_t r = blockIdx.x;
+    const uint32_t k = root_k[r];
+    const uint32_t kp = k | 1u;  // odd stride: conflict-free column walks
+    uint32_t* D = smem;          // kp * k
+    const uint32_t* M = mats + mat_off[r];
+    const uint32_t base = root_begin[r];
+    SubRec* out = recs + rec_off[r];
+    for (uint32_t t = threadIdx.x; t < k; t += blockDim.x) {
+        ids[t] = order[base + t];
+        ord[t] = t;
+    }
+    for (uint32_t x = threadIdx.x; x < k * k; x += blockDim.x) {
+        const uint32_t i = x / k, j = x % k;
+        D[i * kp + j] = i < j ? M[(uint64_t)i * k + j] : (i > j ? M[(uint64_t)j * k + i] : 0u);
+    }
+    if (threadIdx.x == 0) {
+        qb[0] = 0;
+        qe[0] = k;
+        qp[0] = -1;
+        qd[0] = 0;
+        s_tail = 1;
+        s_bad = 0;
+    }
+    __syncthreads();
+    for (uint32_t h = 0; h < s_tail; ++h) {
+        const uint32_t b = qb[h], e = qe[h], m = e - b;
+        if (m == 1) {
+            if (threadIdx.x == 0)
+                out[h] = SubRec{b, e, ids[ord[b]], 0, kNo, kNo, -1, -1, qp[h], qd[h]};
+            __syncthreads();
+            continue;
+        }
+        // median: all members are candidates (m <= exact_cap)
+        Key best{~0ull, kNo, 0};
+        for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+            const uint32_t* row = D + ord[b + i] * kp;
+            uint64_t s = 0;
+            for (uint32_t j = 0; j < m; ++j) s += row[ord[b + j]];
+            Key c{s, ids[ord[b + i]], ord[b + i]};
+            if (better_min(c, best)) best = c;
+        }
+        const Key cen = block_reduce<true>(best, sh);
+        // radius + pole_l
+        Key far{0, kNo, 0};
+        bool any = false;
+        for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+            const uint32_t x = ord[b + i];
+            Key c{D[cen.idx * kp + x], ids[x], x};
+            if (!any || better_max(c, far)) far = c;
+            any = true;
+        }
+        if (!any) far = Key{0, kNo, 0};
+        const Key pl = block_reduce<false>(far, sh);
+        Key far2{0, kNo, 0};
+        any = false;
+        for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+            const uint32_t x = ord[b + i];
+            Key c{D[pl.idx * kp + x], ids[x], x};
+            if (!any || better_max(c, far2)) far2 = c;
+            any = true;
+        }
+        if (!any) far2 = Key{0, kNo, 0};
+        const Key pr = block_reduce<false>(far2, sh);
+        if (pr.id == pl.id) {
+            if (threadIdx.x == 0) s_bad = 1;
+            __syncthreads();
+            break;
+        }
+        // stable partition on warp 0
+        if (threadIdx.x < 32) {
+            const int l = threadIdx.x;
+            const unsigned lt = (1u << l) - 1u;
+            uint32_t nl = 0;
+            for (uint32_t c0 = 0; c0 < m; c0 += 32) {
+                const uint32_t i = c0 + l;
+                const uint32_t x = i < m ? ord[b + i] : 0;
+                const bool f = i < m && D[pl.idx * kp + x] <= D[pr.idx * kp + x];
+                const unsigned msk = __ballot_sync(0xffffffffu, f);
+                if (f) tmp[nl + __popc(msk & lt)] = x;
+                nl += __popc(msk);
+            }
+            uint32_t nr = nl;
+            for (uint32_t c0 = 0; c0 < m; c0 += 32) {
+                const uint32_t i = c0 + l;
+                const uint32_t x = i < m ? ord[b + i] : 0;
+                const bool f = i < m && !(D[pl.idx * kp + x] <= D[pr.idx * kp + x]);
+                const unsigned msk = __ballot_sync(0xffffffffu, f);
+                if (f) tmp[nr + __popc(msk & lt)] = x;
+                nr += __popc(msk);
+            }
+            if (l == 0) s_L = nl;
+        }
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) ord[b + i] = tmp[i];
+        if (threadIdx.x == 0) {
+            const uint32_t L = s_L, t = s_tail;
+            uint32_t radius = D[cen.idx * kp + pl.idx];
+            out[h] = SubRec{b, e, cen.id, radius, pl.id, pr.id, (int32_t)t, (int32_t)t + 1, qp[h], qd[h]};
+            qb[t] = b; qe[t] = b + L; qp[t] = (int32_t)h; qd[t] = qd[h] + 1;
+            qb[t + 1] = b + L; qe[t + 1] = e; qp[t + 1] = (int32_t)h; qd[t + 1] = qd[h] + 1;
+            s_tail = t + 2;
+        }
+        __syncthreads();
+    }
+    if (s_bad) {
+        if (threadIdx.x == 0) atomicExch(err, 1);
+        return;
+    }
+    for (uint32_t t = threadIdx.x; t < k; t += blockDim.x) order[base + t] = ids[ord[t]];
+}
+
+// ------------------------------------------------------------ host side
+struct PNode {
+    uint32_t begin = 0, end = 0, center = kNo, radius = 0, pole_l = kNo, pole_r = kNo;
+    int32_t left = -1, right = -1, parent = -1;
+    uint32_t depth = 0;
+};
+
+template <class T>
+T* upload(dm_ctx* ctx, DevBuf& buf, const std::vector<T>& v) {
+    T* d = buf.as<T>(std::max<size_t>(v.size(), 1));
+    if (!v.empty()) DM_CUDA(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+    return d;
+}
+template <class T>
+void download(dm_ctx* ctx, std::vector<T>& v, const T* d, size_t n) {
+    v.resize(n);
+    if (n) DM_CUDA(cudaMemcpyAsync(v.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+}
+
+struct TreeScratch {
+    DevBuf order, tmp, dc, dl, dr, mat, matoff, kk, cand, candoff, nb, ne, res1, res2, res3, sub_begin, sub_k,
+        sub_mat, sub_matoff, sub_recoff, sub_recs, err;
+};
+
+const char* kDedupMsg = "cluster contains identical sequences; input was not de-duplicated";
+
+}  // namespace
+
+void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_cap_in,
+                std::vector<dm_node>& nodes_out, std::vector<uint32_t>& order, dm_stats* st) {
+    const uint32_t n = s->n;
+    if (n == 0) throw runtime_error("cannot build a cluster tree from zero sequences");
+    const uint64_t exact_cap = std::max<uint64_t>(2, exact_cap_in);
+    const uint32_t T = (uint32_t)std::min<uint64_t>(exact_cap, kSubMax);
+    cudaStream_t stream = ctx->stream;
+    TreeScratch sc;
+    LevTotals tot;
+    const bool timing = st != nullptr;
+
+    order.resize(n);
+    std::iota(order.begin(), order.end(), 0u);
+    std::vector<PNode> pool(1);
+    pool[0].begin = 0;
+    pool[0].end = n;
+    std::vector<uint32_t> big, small;
+    if (n == 1) pool[0].center = 0;
+    else if (n <= T) small.push_back(0);
+    else big.push_back(0);
+
+    uint32_t* d_order = upload(ctx, sc.order, order);
+    uint32_t* d_tmp = sc.tmp.as<uint32_t>(n);
+    uint32_t* d_dc = sc.dc.as<uint32_t>(n);
+    uint32_t* d_dl = sc.dl.as<uint32_t>(n);
+    uint32_t* d_dr = sc.dr.as<uint32_t>(n);
+    std::vector<LevItem> items;
+
+    while (!big.empty()) {
+        const size_t B = big.size();
+        // ---- phase 1: median candidates (host seeds) + all-pairs batch
+        std::vector<uint64_t> mat_off(B), cand_off(B);
+        std::vector<uint32_t> kk(B), cand, nb(B), ne(B);
+        uint64_t mtot = 0;
+        items.clear();
+        for (size_t v = 0; v < B; ++v) {
+            const PNode& nd = pool[big[v]];
+            const uint32_t m = nd.end - nd.begin;
+            nb[v] = nd.begin;
+            ne[v] = nd.end;
+            cand_off[v] = cand.size();
+            const uint32_t* mem = order.data() + nd.begin;
+            if (m <= exact_cap) {
+                cand.insert(cand.end(), mem, mem + m);
+            } else {
+                const uint64_t node_seed = combine_seed(seed, hash_members(mem, m));
+                std::mt19937_64 g(node_seed);
+                for (uint64_t p : sample_distinct(g, m, exact_cap)) cand.push_back(mem[p]);
+            }
+            const uint32_t k = (uint32_t)(cand.size() - cand_off[v]);
+            kk[v] = k;
+            mat_off[v] = mtot;
+            const uint32_t* c = cand.data() + cand_off[v];
+            for (uint32_t i = 0; i < k; ++i)
+                for (uint32_t j = i + 1; j < k; ++j)
+                    items.push_back(LevItem{c[i], c[j], (uint32_t)(mtot + (uint64_t)i * k + j)});
+            mtot += (uint64_t)k * k;
+        }
+        uint32_t* d_mat = sc.mat.as<uint32_t>(mtot);
+        lev_run_host_items(ctx, s, items, d_mat, &tot, timing);
+        uint32_t* d_center = sc.res1.as<uint32_t>(B);
+        median_argmin_kernel<<<(unsigned)B, 128, 0, stream>>>(
+            d_mat, upload(ctx, sc.matoff, mat_off), upload(ctx, sc.kk, kk), upload(ctx, sc.cand, cand),
+            upload(ctx, sc.candoff, cand_off), d_center);
+        DM_CUDA(cudaGetLastError());
+        std::vector<uint32_t> center, radius, pole_l, pole_r, mids;
+        download(ctx, center, d_center, B);
+        DM_CUDA(cudaStreamSynchronize(stream));
+        uint32_t* d_nb = upload(ctx, sc.nb, nb);
+        uint32_t* d_ne = upload(ctx, sc.ne, ne);
+
+        // ---- phases 2-4: sweeps from center, pole_l, pole_r
+        auto sweep = [&](const std::vector<uint32_t>& from, uint32_t* d_dist) {
+            items.clear();
+            for (size_t v = 0; v < B; ++v)
+                for (uint32_t p = nb[v]; p < ne[v]; ++p) items.push_back(LevItem{from[v], order[p], p});
+            lev_run_host_items(ctx, s, items, d_dist, &tot, timing);
+        };
+        uint32_t* d_max = sc.res2.as<uint32_t>(B);
+        uint32_t* d_arg = sc.res3.as<uint32_t>(B);
+        sweep(center, d_dc);
+        sweep_argmax_kernel<<<(unsigned)B, 256, 0, stream>>>(d_dc, d_order, d_nb, d_ne, d_max, d_arg);
+        DM_CUDA(cudaGetLastError());
+        download(ctx, radius, d_max, B);
+        download(ctx, pole_l, d_arg, B);
+        DM_CUDA(cudaStreamSynchronize(stream));
+        sweep(pole_l, d_dl);
+        sweep_argmax_kernel<<<(unsigned)B, 256, 0, stream>>>(d_dl, d_order, d_nb, d_ne, d_max, d_arg);
+        DM_CUDA(cudaGetLastError());
+        download(ctx, pole_r, d_arg, B);
+        DM_CUDA(cudaStreamSynchronize(stream));
+        for (size_t v = 0; v < B; ++v)
+            if (pole_r[v] == pole_l[v]) throw runtime_error(kDedupMsg);
+        sweep(pole_r, d_dr);
+        uint32_t* d_mid = sc.res1.as<uint32_t>(B);
+        partition_kernel<<<(unsigned)B, 256, 0, stream>>>(d_order, d_tmp, d_dl, d_dr, d_nb, d_ne, d_mid);
+        DM_CUDA(cudaGetLastError());
+        download(ctx, mids, d_mid, B);
+        DM_CUDA(cudaMemcpyAsync(order.data(), d_order, (size_t)n * 4, cudaMemcpyDeviceToHost, stream));
+        DM_CUDA(cudaStreamSynchronize(stream));
+        ctx->launches += 4;
+        tot.launches += 4;
+
+        // ---- children (cluster_tree.cpp:201-231)
+        std::vector<uint32_t> next;
+        for (size_t v = 0; v < B; ++v) {
+            const uint32_t id = big[v];
+            pool[id].center = center[v];
+            pool[id].radius = radius[v];
+            pool[id].pole_l = pole_l[v];
+            pool[id].pole_r = pole_r[v];
+            const uint32_t b = pool[id].begin, e = pool[id].end, mid = b + mids[v];
+            const uint32_t depth = pool[id].depth + 1;
+            for (int side = 0; side < 2; ++side) {
+                PNode c;
+                c.begin = side ? mid : b;
+                c.end = side ? e : mid;
+                c.parent = (int32_t)id;
+                c.depth = depth;
+                const uint32_t cid = (uint32_t)pool.size();
+                (side ? pool[id].right : pool[id].left) = (int32_t)cid;
+                const uint32_t m = c.end - c.begin;
+                if (m == 1) c.center = order[c.begin];
+                pool.push_back(c);
+                if (m >= 2) (m <= T ? small : next).push_back(cid);
+            }
+        }
+        big.swap(next);
+    }
+
+    // ---- small subtrees: one all-pairs matrix each, resolved on the device
+    if (!small.empty()) {
+        const size_t S = small.size();
+        std::vector<uint32_t> sb(S), sk(S);
+        std::vector<uint64_t> moff(S), roff(S);
+        uint64_t mtot = 0, rtot = 0;
+        items.clear();
+        for (size_t r = 0; r < S; ++r) {
+            const PNode& nd = pool[small[r]];
+            const uint32_t k = nd.end - nd.begin;
+            sb[r] = nd.begin;
+            sk[r] = k;
+            moff[r] = mtot;
+            roff[r] = rtot;
+            const uint32_t* mem = order.data() + nd.begin;
+            for (uint32_t i = 0; i < k; ++i)
+                for (uint32_t j = i + 1; j < k; ++j)
+                    items.push_back(LevItem{mem[i], mem[j], (uint32_t)(mtot + (uint64_t)i * k + j)});
+            mtot += (uint64_t)k * k;
+            rtot += 2ull * k - 1;
+        }
+        uint32_t* d_mat = sc.sub_mat.as<uint32_t>(mtot);
+        lev_run_host_items(ctx, s, items, d_mat, &tot, timing);
+        SubRec* d_recs = sc.sub_recs.as<SubRec>(rtot);
+        int* d_err = sc.err.as<int>(1);
+        DM_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), stream));
+        const size_t smem = (size_t)(T | 1u) * T * 4;
+        DM_CUDA(cudaFuncSetAttribute(subtree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        subtree_kernel<<<(unsigned)S, 128, smem, stream>>>(d_order, upload(ctx, sc.sub_begin, sb),
+                                                           upload(ctx, sc.sub_k, sk), upload(ctx, sc.sub_matoff, moff),
+                                                           d_mat, upload(ctx, sc.sub_recoff, roff), d_recs, d_err);
+        DM_CUDA(cudaGetLastError());
+        ctx->launches += 1;
+        tot.launches += 1;
+        std::vector<SubRec> recs;
+        download(ctx, recs, d_recs, rtot);
+        int err = 0;
+        DM_CUDA(cudaMemcpyAsync(&err, d_err, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        DM_CUDA(cudaMemcpyAsync(order.data(), d_order, (size_t)n * 4, cudaMemcpyDeviceToHost, stream));
+        DM_CUDA(cudaStreamSynchronize(stream));
+        if (err) throw runtime_error(kDedupMsg);
+        for (size_t r = 0; r < S; ++r) {
+            const uint32_t root = small[r];
+            const uint32_t k = sk[r];
+            const SubRec* R = recs.data() + roff[r];
+            const uint32_t nloc = 2 * k - 1;
+            std::vector<uint32_t> gid(nloc);
+            gid[0] = root;
+            for (uint32_t h = 1; h < nloc; ++h) {
+                gid[h] = (uint32_t)pool.size();
+                pool.emplace_back();
+            }
+            const uint32_t b0 = pool[root].begin, d0 = pool[root].depth;
+            const int32_t par0 = pool[root].parent;
+            for (uint32_t h = 0; h < nloc; ++h) {
+                PNode& p = pool[gid[h]];
+                p.begin = b0 + R[h].b;
+                p.end = b0 + R[h].e;
+                p.center = R[h].center;
+                p.radius = R[h].radius;
+                p.pole_l = R[h].pole_l;
+                p.pole_r = R[h].pole_r;
+                p.left = R[h].left < 0 ? -1 : (int32_t)gid[R[h].left];
+                p.right = R[h].right < 0 ? -1 : (int32_t)gid[R[h].right];
+                p.parent = h == 0 ? par0 : (int32_t)gid[R[h].parent];
+                p.depth = d0 + R[h].depth;
+            }
+        }
+    }
+
+    // ---- BFS renumbering = the reference's level-synchronous numbering
+    nodes_out.clear();
+    nodes_out.reserve(pool.size());
+    std::vector<uint32_t> q{0};
+    std::vector<int32_t> newid(pool.size(), -1);
+    newid[0] = 0;
+    for (size_t h = 0; h < q.size(); ++h) {
+        const PNode& p = pool[q[h]];
+        if (p.left >= 0) {
+            newid[p.left] = (int32_t)q.size();
+            q.push_back((uint32_t)p.left);
+            newid[p.right] = (int32_t)q.size();
+            q.push_back((uint32_t)p.right);
+        }
+    }
+    for (uint32_t id : q) {
+        const PNode& p = pool[id];
+        dm_node d;
+        d.begin = p.begin;
+        d.end = p.end;
+        d.center = p.center;
+        d.radius = p.radius;
+        d.pole_l = p.pole_l;
+        d.pole_r = p.pole_r;
+        d.left = p.left < 0 ? -1 : newid[p.left];
+        d.right = p.right < 0 ? -1 : newid[p.right];
+        d.parent = p.parent < 0 ? -1 : newid[p.parent];
+        d.depth = p.depth;
+        nodes_out.push_back(d);
+    }
+    if (st) {
+        st->cells += tot.cells;
+        st->cells_executed += tot.cells_exec;
+        st->launches += tot.launches;
+        st->kernel_ms += tot.kernel_ms;
+    }
+}
+
+uint32_t geometric_median(dm_ctx* ctx, const dm_seqset* s, const uint32_t* members, uint64_t n,
+                          uint64_t seed, uint64_t exact_cap) {
+    // cluster_tree.cpp:115-166
+    if (n == 0) throw invalid_argument("geometric_median of an empty member set");
+    for (uint64_t i = 0; i < n; ++i)
+        if (members[i] >= s->n) throw invalid_argument("sequence index out of range");
+    if (n == 1) return members[0];
+    exact_cap = std::max<uint64_t>(2, exact_cap);
+    std::vector<uint32_t> cand;
+    if (n <= exact_cap) {
+        cand.assign(members, members + n);
+    } else {
+        std::mt19937_64 g(seed);
+        for (uint64_t p : sample_distinct(g, n, exact_cap)) cand.push_back(members[p]);
+    }
+    const uint32_t k = (uint32_t)cand.size();
+    std::vector<LevItem> items;
+    for (uint32_t i = 0; i < k; ++i)
+        for (uint32_t j = i + 1; j < k; ++j) items.push_back(LevItem{cand[i], cand[j], i * k + j});
+    uint32_t* d = ctx->out.as<uint32_t>((size_t)k * k);
+    lev_run_host_items(ctx, s, items, d, nullptr, false);
+    std::vector<uint32_t> mat((size_t)k * k);
+    DM_CUDA(cudaMemcpyAsync(mat.data(), d, mat.size() * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    DM_CUDA(cudaStreamSynchronize(ctx->stream));
+    size_t best = 0;
+    uint64_t best_sum = UINT64_MAX;
+    for (uint32_t i = 0; i < k; ++i) {
+        uint64_t sum = 0;
+        for (uint32_t j = 0; j < k; ++j)
+            if (i != j) sum += i < j ? mat[(size_t)i * k + j] : mat[(size_t)j * k + i];
+        if (sum < best_sum || (sum == best_sum && cand[i] < cand[best])) {
+            best_sum = sum;
+            best = i;
+        }
+    }
+    return cand[best];
+}
+
+}  // namespace dm
