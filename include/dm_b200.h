@@ -145,6 +145,39 @@ uint64_t dm_msa_nnodes(const dm_msa_out* m);
 int dm_msa_copy_tree(const dm_msa_out* m, dm_node* nodes, uint32_t* order);
 void dm_msa_free(dm_msa_out* m);
 
+/* ---- scoring schemes (pairwise.cpp:59-142) ----------------------------- */
+/* kind 0: default_nucleotide_scheme (IUPAC), 1: default_protein_scheme
+ * (BLOSUM62). Outputs the 128x128 table, the has_symbol flags and the open
+ * surcharge (gap_open, or 0 when flat). Validation errors as the reference. */
+int dm_scheme_default(int kind, int gap_open, int gap_extend, int flat, int16_t* table,
+                      uint8_t* has_symbol, int* open_surcharge);
+/* ScoringScheme(symbols, matrix, gap_open, gap_extend, mode); gap_scores
+ * (nsym entries, or NULL) overrides score('-', symbol) as a matrix file's
+ * gap column does (pairwise.cpp:243-250), gap_gap overrides score('-','-'). */
+int dm_scheme_custom(const char* symbols, uint32_t nsym, const int* matrix, int gap_open,
+                     int gap_extend, int flat, const int* gap_scores, int gap_gap, int16_t* table,
+                     uint8_t* has_symbol, int* open_surcharge);
+
+/* ---- pipeline (align_sequences, pipeline.cpp:78-159) -------------------- */
+typedef struct {
+    uint64_t input_count, unique_count, duplicate_count;
+    uint32_t tree_depth;
+    uint64_t width;
+    int alphabet; /* 0 nucleotide, 1 protein */
+    double elapsed_s;
+} dm_align_summary;
+/* alphabet: 0 auto, 1 nucleotide, 2 protein. custom_table/custom_has: a
+ * scheme from dm_scheme_custom (NULL: built-in for the alphabet; residue
+ * validation is skipped for custom schemes, as with --matrix). Record ids in
+ * error messages are "seq<i>" (py_module.cpp:134-138). input_order: 1 rows
+ * parallel to the input (RowOrder::Input), 0 tree order. rows_out: n x width,
+ * free with dm_free. */
+int dm_align_sequences(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint32_t n,
+                       int alphabet, int gap_open, int gap_extend, int flat,
+                       const int16_t* custom_table, const uint8_t* custom_has, uint64_t seed,
+                       int input_order, char** rows_out, uint64_t* width_out,
+                       dm_align_summary* summary, dm_stats* st);
+
 /* ---- synthetic inputs --------------------------- */
 /* cfg 0..4 at `scale` (1.0 = full size). Returns concatenated residues +
  * offsets (free with dm_free). For cfg 1, sequence 2i / 2i+1 form pair i. */

@@ -193,6 +193,253 @@ def geometric_median(seqset: SeqSet, members, seed: int, exact_cap: int = 100) -
     return int(out.value)
 
 
+class ScoringScheme:
+    """divmsa::ScoringScheme (pairwise.hpp:22-52): 128x128 int16 table over
+    chars, the gap symbol a first-class row, affine or flat gap mode."""
+
+    def __init__(self, table: np.ndarray, has_symbol: np.ndarray, gap_open: int, gap_extend: int, mode: str,
+                 symbols: str):
+        self.table = np.ascontiguousarray(table, dtype=np.int16)
+        self.has_symbol = np.ascontiguousarray(has_symbol, dtype=np.uint8)
+        self._gap_open, self._gap_extend, self.mode, self.symbols = gap_open, gap_extend, mode, symbols
+
+    @classmethod
+    def nucleotide(cls, gap_open: int = -10, gap_extend: int = -1, mode: str = "affine"):
+        """default_nucleotide_scheme (pairwise.cpp:122-137)."""
+        return cls._default(0, gap_open, gap_extend, mode, "ACGTURYSWKMBDHVN")
+
+    @classmethod
+    def protein(cls, gap_open: int = -10, gap_extend: int = -1, mode: str = "affine"):
+        """default_protein_scheme, BLOSUM62 (pairwise.cpp:139-142)."""
+        return cls._default(1, gap_open, gap_extend, mode, "ARNDCQEGHILKMFPSTWYVBZX*")
+
+    @classmethod
+    def _default(cls, kind, gap_open, gap_extend, mode, symbols):
+        t = np.zeros(128 * 128, dtype=np.int16)
+        h = np.zeros(128, dtype=np.uint8)
+        o = C.c_int()
+        check(lib().dm_scheme_default(kind, gap_open, gap_extend, int(_flat(mode)), _ptr(t, C.c_int16),
+                                      _ptr(h, C.c_uint8), C.byref(o)))
+        return cls(t, h, gap_open, gap_extend, mode, symbols)
+
+    @classmethod
+    def custom(cls, symbols: str, matrix, gap_open: int, gap_extend: int, mode: str = "affine",
+               gap_scores=None, gap_gap: int = 0):
+        """ScoringScheme(symbols, matrix, gap_open, gap_extend, mode) (pairwise.cpp:59-108)."""
+        m = np.ascontiguousarray(np.asarray(matrix, dtype=np.int32).ravel())
+        gs = None if gap_scores is None else np.ascontiguousarray(gap_scores, dtype=np.int32)
+        t = np.zeros(128 * 128, dtype=np.int16)
+        h = np.zeros(128, dtype=np.uint8)
+        o = C.c_int()
+        check(lib().dm_scheme_custom(symbols.encode(), len(symbols), _ptr(m, C.c_int) if m.size else None,
+                                     gap_open, gap_extend, int(_flat(mode)), None if gs is None else _ptr(gs, C.c_int),
+                                     gap_gap, _ptr(t, C.c_int16), _ptr(h, C.c_uint8), C.byref(o)))
+        return cls(t, h, gap_open, gap_extend, mode, symbols)
+
+    def score(self, x: str, y: str) -> int:
+        return int(self.table[ord(x) * 128 + ord(y)])
+
+    def has(self, c: str) -> bool:
+        return bool(self.has_symbol[ord(c)]) if ord(c) < 128 else False
+
+    def gap_open(self) -> int:
+        return self._gap_open
+
+    def gap_extend(self) -> int:
+        return self._gap_extend
+
+    def open_surcharge(self) -> int:
+        """gap_open in affine mode, 0 in flat mode (pairwise.hpp:36-38)."""
+        return self._gap_open if self.mode == "affine" else 0
+
+
+def _flat(mode: str) -> bool:
+    if mode not in ("affine", "flat"):
+        raise ValueError(f"unknown gap mode '{mode}' (expected affine or flat)")
+    return mode == "flat"
+
+
+def _scheme_for(alphabet: str, gap_open: int, gap_extend: int, gap_mode: str) -> ScoringScheme:
+    """py_module.cpp scheme_for: alphabet 'nt' | 'aa'."""
+    if alphabet == "nt":
+        return ScoringScheme.nucleotide(gap_open, gap_extend, gap_mode)
+    if alphabet == "aa":
+        return ScoringScheme.protein(gap_open, gap_extend, gap_mode)
+    raise ValueError(f"unknown alphabet '{alphabet}' (expected nt or aa)")
+
+
+@dataclass
+class PairwiseResult:
+    """divmsa::PairwiseResult (pairwise.hpp:78-84)."""
+    aligned_a: str
+    aligned_b: str
+    score: int
+    gaps_into_a: List[int] = field(default_factory=list)
+    gaps_into_b: List[int] = field(default_factory=list)
+
+    def __repr__(self):
+        return f"PairwiseResult(aligned_a='{self.aligned_a}', aligned_b='{self.aligned_b}', score={self.score})"
+
+
+def _pw_results(h, count: int) -> List[PairwiseResult]:
+    L = lib()
+    out = []
+    for k in range(count):
+        n = L.dm_pw_len(h, k)
+        a = C.create_string_buffer(n + 1)
+        b = C.create_string_buffer(n + 1)
+        L.dm_pw_aligned(h, k, a, b)
+        ga = np.zeros(max(L.dm_pw_ngaps_a(h, k), 1), dtype=np.uint32)
+        gb = np.zeros(max(L.dm_pw_ngaps_b(h, k), 1), dtype=np.uint32)
+        L.dm_pw_gaps(h, k, _ptr(ga), _ptr(gb))
+        out.append(PairwiseResult(a.raw[:n].decode("latin-1"), b.raw[:n].decode("latin-1"), int(L.dm_pw_score(h, k)),
+                                  [int(x) for x in ga[:L.dm_pw_ngaps_a(h, k)]],
+                                  [int(x) for x in gb[:L.dm_pw_ngaps_b(h, k)]]))
+    return out
+
+
+def nw_align(a, b, alphabet="nt", gap_open: int = -10, gap_extend: int = -1, gap_mode: str = "affine",
+             scheme: ScoringScheme | None = None, ctx: Context | None = None) -> PairwiseResult:
+    """divmsa.nw_align (py_module.cpp:105-118 -> pairwise.cpp:301) on the GPU."""
+    ctx = ctx or default_context()
+    sc = scheme or _scheme_for(alphabet, gap_open, gap_extend, gap_mode)
+    a = a.encode() if isinstance(a, str) else bytes(a)
+    b = b.encode() if isinstance(b, str) else bytes(b)
+    h = C.c_void_p()
+    check(lib().dm_nw_align(ctx.handle, a, len(a), b, len(b), _ptr(sc.table, C.c_int16),
+                            _ptr(sc.has_symbol, C.c_uint8), sc.open_surcharge(), sc.gap_extend(), C.byref(h)))
+    try:
+        return _pw_results(h, 1)[0]
+    finally:
+        lib().dm_pw_free(h)
+
+
+def nw_batch(pairs, scheme: ScoringScheme, ctx: Context | None = None, stats: bool = False):
+    """Batched nw_align over [(a, b), ...] (one device launch pair)."""
+    ctx = ctx or default_context()
+    A, ao = _pack([p[0] for p in pairs])
+    B, bo = _pack([p[1] for p in pairs])
+    h = C.c_void_p()
+    s = dm_stats()
+    check(lib().dm_nw_batch(ctx.handle, A, _ptr(ao, C.c_uint64), B, _ptr(bo, C.c_uint64), len(pairs),
+                            _ptr(scheme.table, C.c_int16), _ptr(scheme.has_symbol, C.c_uint8), scheme.open_surcharge(),
+                            scheme.gap_extend(), C.byref(h), C.byref(s)))
+    try:
+        res = _pw_results(h, len(pairs))
+    finally:
+        lib().dm_pw_free(h)
+    return (res, s.as_dict()) if stats else res
+
+
+def insert_gap_columns(rows: List[str], positions, ctx: Context | None = None) -> List[str]:
+    """divmsa::insert_gap_columns (msa_merge.hpp:34-35) on the GPU."""
+    ctx = ctx or default_context()
+    width = len(rows[0]) if rows else 0
+    pos = _u32(positions)
+    nw = width + len(pos)
+    out = C.create_string_buffer(max(len(rows) * nw, 1))
+    check(lib().dm_insert_gap_columns(ctx.handle, "".join(rows).encode(), len(rows), width, _ptr(pos), len(pos), out))
+    return [out.raw[r * nw:(r + 1) * nw].decode("latin-1") for r in range(len(rows))]
+
+
+@dataclass
+class Msa:
+    """divmsa::Msa (msa_merge.hpp:18-26): rows in tree order."""
+    rows: List[str]
+    row_to_sequence: np.ndarray
+    width: int
+    nodes: np.ndarray = None
+    order: np.ndarray = None
+    stats: dict = None
+
+    def row_of(self, sequence: int) -> int:
+        hit = np.nonzero(self.row_to_sequence == sequence)[0]
+        if len(hit) == 0:
+            raise ValueError(f"center row for sequence {sequence} not found in alignment")
+        return int(hit[0])
+
+
+def _msa_from(h) -> Msa:
+    L = lib()
+    W, R = L.dm_msa_width(h), L.dm_msa_rows(h)
+    buf = C.create_string_buffer(max(W * R, 1))
+    L.dm_msa_copy_rows(h, buf)
+    rs = np.zeros(max(R, 1), dtype=np.uint32)
+    L.dm_msa_copy_row_seq(h, _ptr(rs))
+    nn = L.dm_msa_nnodes(h)
+    nodes = (dm_node * max(nn, 1))()
+    order = np.zeros(max(R, 1), dtype=np.uint32)
+    L.dm_msa_copy_tree(h, nodes, _ptr(order))
+    raw = buf.raw
+    return Msa([raw[r * W:(r + 1) * W].decode("latin-1") for r in range(R)], rs[:R].copy(), int(W),
+               nodes_to_array(nodes, nn), order[:R].copy())
+
+
+def align_all(seqset: SeqSet, nodes: np.ndarray, order, scheme: ScoringScheme, stats: bool = False) -> Msa:
+    """divmsa::align_all (msa_merge.hpp:47-49) on the GPU: per-level merge scheduler."""
+    order = _u32(order)
+    nd = array_to_nodes(nodes)
+    h = C.c_void_p()
+    s = dm_stats()
+    check(lib().dm_align_all(seqset.ctx.handle, seqset.handle, nd, len(nodes), _ptr(order),
+                             _ptr(scheme.table, C.c_int16), _ptr(scheme.has_symbol, C.c_uint8),
+                             scheme.open_surcharge(), scheme.gap_extend(), C.byref(h), C.byref(s)))
+    try:
+        m = _msa_from(h)
+    finally:
+        lib().dm_msa_free(h)
+    m.stats = s.as_dict()
+    return m
+
+
+def msa(seqset: SeqSet, scheme: ScoringScheme, seed: int = 42, exact_cap: int = 100) -> Msa:
+    """build_tree + align_all (pipeline.cpp:116-128), device-resident between the two."""
+    h = C.c_void_p()
+    s = dm_stats()
+    check(lib().dm_msa(seqset.ctx.handle, seqset.handle, int(seed), int(exact_cap), _ptr(scheme.table, C.c_int16),
+                       _ptr(scheme.has_symbol, C.c_uint8), scheme.open_surcharge(), scheme.gap_extend(), C.byref(h),
+                       C.byref(s)))
+    try:
+        m = _msa_from(h)
+    finally:
+        lib().dm_msa_free(h)
+    m.stats = s.as_dict()
+    return m
+
+
+def align(sequences: Sequence, alphabet: str = "auto", gap_open: int = -10, gap_extend: int = -1,
+          gap_mode: str = "affine", seed: int = 42, threads: int = 0, scheme: ScoringScheme | None = None,
+          order: str = "input", ctx: Context | None = None, summary: bool = False):
+    """divmsa.align (py_module.cpp:120-155 -> align_sequences, pipeline.cpp:78-159).
+
+    Returns gapped rows parallel to the input (RowOrder::Input). `threads` is
+    accepted for API parity; the work runs on the GPU."""
+    from ._lib import dm_align_summary
+    ctx = ctx or default_context()
+    amap = {"auto": 0, "nt": 1, "dna": None, "aa": 2}
+    if alphabet not in ("auto", "nt", "aa"):
+        raise ValueError(f"unknown alphabet '{alphabet}' (expected auto, nt or aa)")
+    flat = _flat(gap_mode)
+    data, offs = _pack(sequences)
+    rows = C.c_void_p()
+    width = C.c_uint64()
+    summ = dm_align_summary()
+    s = dm_stats()
+    check(lib().dm_align_sequences(ctx.handle, data, _ptr(offs, C.c_uint64), len(offs) - 1, amap[alphabet], gap_open,
+                                   gap_extend, int(flat), None if scheme is None else _ptr(scheme.table, C.c_int16),
+                                   None if scheme is None else _ptr(scheme.has_symbol, C.c_uint8), int(seed),
+                                   int(order == "input"), C.byref(rows), C.byref(width), C.byref(summ), C.byref(s)))
+    try:
+        W = width.value
+        raw = C.string_at(rows, W * (len(offs) - 1))
+    finally:
+        lib().dm_free(rows)
+    out = [raw[r * W:(r + 1) * W].decode("latin-1") for r in range(len(offs) - 1)]
+    if summary:
+        return out, {f: getattr(summ, f) for f, _ in summ._fields_}, s.as_dict()
+    return out
+
+
 def synth(cfg: int, scale: float = 1.0, seed: int = 0):
     """Seeded synthetic inputs of BASELINE config `cfg`.
 

@@ -32,6 +32,12 @@ class dm_stats(C.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
+class dm_align_summary(C.Structure):
+    _fields_ = [("input_count", C.c_uint64), ("unique_count", C.c_uint64), ("duplicate_count", C.c_uint64),
+                ("tree_depth", C.c_uint32), ("width", C.c_uint64), ("alphabet", C.c_int),
+                ("elapsed_s", C.c_double)]
+
+
 _P = C.c_void_p
 _u32p = C.POINTER(C.c_uint32)
 _u64p = C.POINTER(C.c_uint64)
@@ -83,6 +89,12 @@ SIGNATURES = {
     "dm_msa_nnodes": (C.c_uint64, [_P]),
     "dm_msa_copy_tree": (C.c_int, [_P, C.POINTER(dm_node), _u32p]),
     "dm_msa_free": (None, [_P]),
+    "dm_scheme_default": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _i16p, _u8p, C.POINTER(C.c_int)]),
+    "dm_scheme_custom": (C.c_int, [C.c_char_p, C.c_uint32, C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int,
+                                   C.POINTER(C.c_int), C.c_int, _i16p, _u8p, C.POINTER(C.c_int)]),
+    "dm_align_sequences": (C.c_int, [_P, C.c_char_p, _u64p, C.c_uint32, C.c_int, C.c_int, C.c_int, C.c_int, _i16p,
+                                     _u8p, C.c_uint64, C.c_int, C.POINTER(C.c_void_p), _u64p, _P,
+                                     C.POINTER(dm_stats)]),
     "dm_synth": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.POINTER(C.c_char_p), C.POINTER(_u64p), _u64p]),
     "dm_free": (None, [_P]),
 }

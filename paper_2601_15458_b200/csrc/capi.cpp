@@ -5,42 +5,23 @@
 #include <cstring>
 #include <string>
 
-#include "dm_internal.h"
+#include "capi_guard.h"
+
+namespace dm {
+std::string& last_error() {
+    thread_local std::string e;
+    return e;
+}
+}  // namespace dm
 
 namespace {
-thread_local std::string g_err;
-
-template <class F>
-int guard(F&& f) {
-    try {
-        f();
-        return DM_OK;
-    } catch (const dm::invalid_argument& e) {
-        g_err = e.what();
-        return DM_EINVAL;
-    } catch (const dm::cuda_error& e) {
-        g_err = e.what();
-        return DM_ECUDA;
-    } catch (const dm::runtime_error& e) {
-        g_err = e.what();
-        return DM_ERUNTIME;
-    } catch (const std::bad_alloc& e) {
-        g_err = "out of memory";
-        return DM_ENOMEM;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return DM_ERUNTIME;
-    }
-}
-
-void require(bool ok, const char* msg) {
-    if (!ok) throw dm::invalid_argument(msg);
-}
+using dm::guard;
+using dm::require;
 }  // namespace
 
 extern "C" {
 
-const char* dm_last_error(void) { return g_err.c_str(); }
+const char* dm_last_error(void) { return dm::last_error().c_str(); }
 int dm_abi_version(void) { return 1; }
 
 int dm_ctx_create(int device, dm_ctx** out) {

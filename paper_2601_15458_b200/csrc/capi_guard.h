@@ -1,0 +1,37 @@
+// Exception -> status-code mapping shared by the C ABI translation units.
+#pragma once
+
+#include <new>
+#include <string>
+
+#include "dm_internal.h"
+
+namespace dm {
+
+std::string& last_error();  // thread-local, defined in capi.cpp
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return DM_OK;
+    } catch (const invalid_argument& e) {
+        last_error() = e.what();
+        return DM_EINVAL;
+    } catch (const cuda_error& e) {
+        last_error() = e.what();
+        return DM_ECUDA;
+    } catch (const std::bad_alloc&) {
+        last_error() = "out of memory";
+        return DM_ENOMEM;
+    } catch (const std::exception& e) {
+        last_error() = e.what();
+        return DM_ERUNTIME;
+    }
+}
+
+inline void require(bool ok, const char* msg) {
+    if (!ok) throw invalid_argument(msg);
+}
+
+}  // namespace dm

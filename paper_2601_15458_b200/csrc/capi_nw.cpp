@@ -1,0 +1,247 @@
+// extern "C" boundary, part 2: pairwise aligner and MSA builder.
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "capi_guard.h"
+#include "nw.h"
+
+// One batch of PairwiseResults (pairwise.hpp:78-84).
+struct dm_pw {
+    struct One {
+        int64_t score = 0;
+        std::string a, b;
+        std::vector<uint32_t> gaps_a, gaps_b;  // ascending, pre-insertion coordinates
+    };
+    std::vector<One> r;
+};
+
+namespace {
+using dm::guard;
+
+// pairwise.cpp:288-297
+void check_symbols(const char* s, uint64_t n, const dm::NwScheme& sc, const char* which) {
+    for (uint64_t i = 0; i < n; ++i) {
+        const unsigned char c = (unsigned char)s[i];
+        if (c >= 128 || !sc.has[c])
+            throw dm::invalid_argument(std::string("sequence ") + which + " contains symbol '" + (char)c +
+                                       "' absent from the substitution table");
+    }
+}
+
+std::string with_gaps(const char* s, uint64_t n, const std::vector<uint32_t>& asc) {
+    std::string out;
+    out.reserve(n + asc.size());
+    size_t p = 0;
+    for (uint64_t c = 0; c < n; ++c) {
+        while (p < asc.size() && asc[p] == c) {
+            out.push_back('-');
+            ++p;
+        }
+        out.push_back(s[c]);
+    }
+    for (; p < asc.size(); ++p) out.push_back('-');
+    return out;
+}
+
+void run_batch(dm_ctx* ctx, const char* A, const uint64_t* a_off, const char* B, const uint64_t* b_off,
+               uint32_t njobs, const dm::NwScheme& sc, dm_pw* pw, dm_stats* st) {
+    for (uint32_t k = 0; k < njobs; ++k) {
+        const uint64_t na = a_off[k + 1] - a_off[k], nb = b_off[k + 1] - b_off[k];
+        if (na == 0 || nb == 0) throw dm::invalid_argument("nw_align requires non-empty inputs");
+        check_symbols(A + a_off[k], na, sc, "a");
+        check_symbols(B + b_off[k], nb, sc, "b");
+    }
+    const uint64_t abytes = a_off[njobs] - a_off[0], bbytes = b_off[njobs] - b_off[0];
+    uint8_t* d_in = (uint8_t*)ctx->rows_b.get(abytes + bbytes + 16);
+    if (abytes) DM_CUDA(cudaMemcpyAsync(d_in, A + a_off[0], abytes, cudaMemcpyHostToDevice, ctx->stream));
+    if (bbytes) DM_CUDA(cudaMemcpyAsync(d_in + abytes, B + b_off[0], bbytes, cudaMemcpyHostToDevice, ctx->stream));
+    std::vector<dm::NwJob> jobs(njobs);
+    for (uint32_t k = 0; k < njobs; ++k) {
+        jobs[k].a_off = a_off[k] - a_off[0];
+        jobs[k].n = (uint32_t)(a_off[k + 1] - a_off[k]);
+        jobs[k].b_off = abytes + (b_off[k] - b_off[0]);
+        jobs[k].m = (uint32_t)(b_off[k + 1] - b_off[k]);
+    }
+    dm::NwOut no;
+    dm::nw_run(ctx, d_in, jobs, sc, no, st != nullptr);
+    std::vector<dm::NwRes> res(njobs);
+    std::vector<uint32_t> gaps(no.gaps_total);
+    if (njobs)
+        DM_CUDA(cudaMemcpyAsync(res.data(), no.d_res, njobs * sizeof(dm::NwRes), cudaMemcpyDeviceToHost, ctx->stream));
+    if (no.gaps_total)
+        DM_CUDA(cudaMemcpyAsync(gaps.data(), no.d_gaps, no.gaps_total * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    DM_CUDA(cudaStreamSynchronize(ctx->stream));
+    pw->r.resize(njobs);
+    for (uint32_t k = 0; k < njobs; ++k) {
+        auto& o = pw->r[k];
+        o.score = res[k].score;
+        o.gaps_a.assign(gaps.begin() + jobs[k].ga_off, gaps.begin() + jobs[k].ga_off + res[k].nga);
+        o.gaps_b.assign(gaps.begin() + jobs[k].gb_off, gaps.begin() + jobs[k].gb_off + res[k].ngb);
+        std::reverse(o.gaps_a.begin(), o.gaps_a.end());  // pairwise.cpp:410-413
+        std::reverse(o.gaps_b.begin(), o.gaps_b.end());
+        o.a = with_gaps(A + a_off[k], jobs[k].n, o.gaps_a);
+        o.b = with_gaps(B + b_off[k], jobs[k].m, o.gaps_b);
+    }
+    if (st) {
+        std::memset(st, 0, sizeof(*st));
+        st->kernel_ms = no.fwd_ms + no.tb_ms;
+        st->cells = no.cells;
+        st->cells_executed = no.cells;
+        st->launches = no.launches;
+        st->nw_calls = njobs;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int dm_nw_align(dm_ctx* ctx, const char* a, uint64_t na, const char* b, uint64_t nb, const int16_t* table,
+                const uint8_t* has_symbol, int open_surcharge, int gap_extend, dm_pw** out) {
+    return guard([&] {
+        if (!ctx || !table || !has_symbol || !out) throw dm::invalid_argument("null argument");
+        const dm::NwScheme sc = dm::make_scheme(table, has_symbol, open_surcharge, gap_extend);
+        auto* pw = new dm_pw;
+        uint64_t ao[2] = {0, na}, bo[2] = {0, nb};
+        try {
+            run_batch(ctx, a, ao, b, bo, 1, sc, pw, nullptr);
+        } catch (...) {
+            delete pw;
+            throw;
+        }
+        *out = pw;
+    });
+}
+
+int dm_nw_batch(dm_ctx* ctx, const char* A, const uint64_t* a_off, const char* B, const uint64_t* b_off,
+                uint32_t njobs, const int16_t* table, const uint8_t* has_symbol, int open_surcharge, int gap_extend,
+                dm_pw** out, dm_stats* st) {
+    return guard([&] {
+        if (!ctx || !table || !has_symbol || !out || !a_off || !b_off) throw dm::invalid_argument("null argument");
+        const dm::NwScheme sc = dm::make_scheme(table, has_symbol, open_surcharge, gap_extend);
+        auto* pw = new dm_pw;
+        try {
+            run_batch(ctx, A, a_off, B, b_off, njobs, sc, pw, st);
+        } catch (...) {
+            delete pw;
+            throw;
+        }
+        *out = pw;
+    });
+}
+
+int64_t dm_pw_score(const dm_pw* p, uint32_t k) { return p->r.at(k).score; }
+uint64_t dm_pw_len(const dm_pw* p, uint32_t k) { return p->r.at(k).a.size(); }
+int dm_pw_aligned(const dm_pw* p, uint32_t k, char* a_out, char* b_out) {
+    const auto& o = p->r.at(k);
+    std::memcpy(a_out, o.a.data(), o.a.size());
+    std::memcpy(b_out, o.b.data(), o.b.size());
+    return DM_OK;
+}
+uint64_t dm_pw_ngaps_a(const dm_pw* p, uint32_t k) { return p->r.at(k).gaps_a.size(); }
+uint64_t dm_pw_ngaps_b(const dm_pw* p, uint32_t k) { return p->r.at(k).gaps_b.size(); }
+int dm_pw_gaps(const dm_pw* p, uint32_t k, uint32_t* gaps_a, uint32_t* gaps_b) {
+    const auto& o = p->r.at(k);
+    if (gaps_a && !o.gaps_a.empty()) std::memcpy(gaps_a, o.gaps_a.data(), o.gaps_a.size() * 4);
+    if (gaps_b && !o.gaps_b.empty()) std::memcpy(gaps_b, o.gaps_b.data(), o.gaps_b.size() * 4);
+    return DM_OK;
+}
+void dm_pw_free(dm_pw* p) { delete p; }
+
+int dm_insert_gap_columns(dm_ctx* ctx, const char* rows, uint64_t nrows, uint64_t width, const uint32_t* pos,
+                          uint64_t npos, char* out) {
+    return guard([&] {
+        if (!ctx) throw dm::invalid_argument("null context");
+        dm::insert_gap_columns(ctx, rows, nrows, width, pos, npos, out);
+    });
+}
+
+int dm_align_all(dm_ctx* ctx, const dm_seqset* s, const dm_node* nodes, uint64_t nnodes, const uint32_t* order,
+                 const int16_t* table, const uint8_t* has_symbol, int open_surcharge, int gap_extend,
+                 dm_msa_out** out, dm_stats* st) {
+    return guard([&] {
+        if (!ctx || !s || !nodes || !order || !table || !has_symbol || !out) throw dm::invalid_argument("null argument");
+        const dm::NwScheme sc = dm::make_scheme(table, has_symbol, open_surcharge, gap_extend);
+        std::vector<dm_node> nv(nodes, nodes + nnodes);
+        std::vector<uint32_t> ov(order, order + s->n);
+        if (st) std::memset(st, 0, sizeof(*st));
+        cudaEvent_t t0, t1;
+        DM_CUDA(cudaEventCreate(&t0));
+        DM_CUDA(cudaEventCreate(&t1));
+        DM_CUDA(cudaEventRecord(t0, ctx->stream));
+        dm_msa_out* m = dm::align_all(ctx, s, nv, ov, sc, st);
+        DM_CUDA(cudaEventRecord(t1, ctx->stream));
+        DM_CUDA(cudaEventSynchronize(t1));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, t0, t1);
+        cudaEventDestroy(t0);
+        cudaEventDestroy(t1);
+        if (st) {
+            st->align_ms = ms;
+            st->total_ms = ms;
+        }
+        *out = m;
+    });
+}
+
+int dm_msa(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_cap, const int16_t* table,
+           const uint8_t* has_symbol, int open_surcharge, int gap_extend, dm_msa_out** out, dm_stats* st) {
+    return guard([&] {
+        if (!ctx || !s || !table || !has_symbol || !out) throw dm::invalid_argument("null argument");
+        const dm::NwScheme sc = dm::make_scheme(table, has_symbol, open_surcharge, gap_extend);
+        if (st) std::memset(st, 0, sizeof(*st));
+        cudaEvent_t t0, t1, t2;
+        DM_CUDA(cudaEventCreate(&t0));
+        DM_CUDA(cudaEventCreate(&t1));
+        DM_CUDA(cudaEventCreate(&t2));
+        DM_CUDA(cudaEventRecord(t0, ctx->stream));
+        std::vector<dm_node> nodes;
+        std::vector<uint32_t> order;
+        dm_stats tree_st{};
+        dm::build_tree(ctx, s, seed, exact_cap, nodes, order, st ? &tree_st : nullptr);
+        DM_CUDA(cudaEventRecord(t1, ctx->stream));
+        dm_stats al_st{};
+        dm_msa_out* m = dm::align_all(ctx, s, nodes, order, sc, st ? &al_st : nullptr);
+        DM_CUDA(cudaEventRecord(t2, ctx->stream));
+        DM_CUDA(cudaEventSynchronize(t2));
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, t0, t1);
+        cudaEventElapsedTime(&b, t1, t2);
+        cudaEventDestroy(t0);
+        cudaEventDestroy(t1);
+        cudaEventDestroy(t2);
+        if (st) {
+            st->tree_ms = a;
+            st->align_ms = b;
+            st->total_ms = a + b;
+            st->cells = tree_st.cells + al_st.cells;
+            st->cells_executed = tree_st.cells_executed + al_st.cells;
+            st->launches = tree_st.launches + al_st.launches;
+            st->kernel_ms = tree_st.kernel_ms + al_st.kernel_ms;
+            st->nw_calls = al_st.nw_calls;
+            st->lev_calls = tree_st.lev_calls;
+        }
+        *out = m;
+    });
+}
+
+uint64_t dm_msa_width(const dm_msa_out* m) { return m->width; }
+uint64_t dm_msa_rows(const dm_msa_out* m) { return m->row_seq.size(); }
+int dm_msa_copy_rows(const dm_msa_out* m, char* buf) {
+    if (!m->rows.empty()) std::memcpy(buf, m->rows.data(), m->rows.size());
+    return DM_OK;
+}
+int dm_msa_copy_row_seq(const dm_msa_out* m, uint32_t* r) {
+    std::memcpy(r, m->row_seq.data(), m->row_seq.size() * 4);
+    return DM_OK;
+}
+uint64_t dm_msa_nnodes(const dm_msa_out* m) { return m->nodes.size(); }
+int dm_msa_copy_tree(const dm_msa_out* m, dm_node* nodes, uint32_t* order) {
+    std::memcpy(nodes, m->nodes.data(), m->nodes.size() * sizeof(dm_node));
+    std::memcpy(order, m->order.data(), m->order.size() * 4);
+    return DM_OK;
+}
+void dm_msa_free(dm_msa_out* m) { delete m; }
+
+}  // extern "C"

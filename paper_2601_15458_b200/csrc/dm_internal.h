@@ -84,7 +84,7 @@ struct dm_ctx {
     dm::DevBuf items, out, counter, aux, aux2, aux3;
     dm::PinnedBuf pin_items, pin_out;
     // scratch for the aligner / merge scheduler
-    dm::DevBuf nw_in, nw_jobs, nw_trace, nw_res, nw_gaps, rows_a, rows_b, colmap, tree_buf;
+    dm::DevBuf nw_in, nw_table, nw_jobs, nw_trace, nw_res, nw_gaps, rows_a, rows_b, colmap, tree_buf;
     uint64_t launches = 0;
 };
 
@@ -95,6 +95,7 @@ struct dm_seqset {
     int planes = 2;    // bit-planes per residue code: 2 (<=4 symbols), 5 (<=32), 8
     int nsym = 0;      // distinct residue bytes
     uint8_t code_of[256] = {};
+    bool present[256] = {};  // bytes that occur in the set
     // host mirrors
     std::vector<uint32_t> len;     // residues per sequence
     std::vector<uint64_t> off;     // byte offset of sequence i in d_codes (16-B aligned)
@@ -112,7 +113,18 @@ struct dm_seqset {
     ~dm_seqset();
 };
 
+// Result of align_all / dm_msa (host side).
+struct dm_msa_out {
+    uint64_t width = 0;
+    std::vector<char> rows;  // rows x width, tree order
+    std::vector<uint32_t> row_seq;
+    std::vector<dm_node> nodes;
+    std::vector<uint32_t> order;
+};
+
 namespace dm {
+
+struct NwScheme;
 
 // One Levenshtein job: distance(seq pat, seq txt) -> out[slot].
 struct LevItem {
@@ -141,6 +153,10 @@ dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets,
 void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_cap,
                 std::vector<dm_node>& nodes, std::vector<uint32_t>& order, dm_stats* st);
 double int32_peak(dm_ctx* ctx, int mode);
+dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node>& nodes,
+                      const std::vector<uint32_t>& order, const NwScheme& sc, dm_stats* st);
+void insert_gap_columns(dm_ctx* ctx, const char* rows, uint64_t nrows, uint64_t width, const uint32_t* pos,
+                        uint64_t npos, char* out);
 uint32_t geometric_median(dm_ctx* ctx, const dm_seqset* s, const uint32_t* members, uint64_t n,
                           uint64_t seed, uint64_t exact_cap);
 

@@ -1,0 +1,286 @@
+// MSA builder (SURVEY.md §2.2 K7/K8 + the per-level merge scheduler):
+// align_all (msa_merge.cpp:107-158) as level-synchronous batches.
+//
+// The rows of every subtree are contiguous in tree.order (cluster_tree.cpp:
+// 212-231), so the alignment lives in ONE device row buffer: row r carries
+// sequence order[r] (test_msa_merge.cpp:198) and the block of node v is rows
+// [v.begin, v.end) x columns [0, W_v). Internal nodes are merged deepest
+// level first; all merges of a level are independent:
+//   1. NW of the children's CENTER rows, read in place from the row buffer
+//      (msa_merge.cpp:82-84: left.row_of(left_child.center) etc.) — one
+//      batched nw_run;
+//   2. a column map per (merge, side) from the gap lists: original column c
+//      moves to c + #{gap positions <= c}; gap k lands at p_k + k
+//      (msa_merge.cpp:31-70);
+//   3. every row of both children is rewritten in place through its map
+//      (one CTA per row, staged through shared memory). Parent rows are
+//      left rows then right rows by construction (:94-104).
+// The result is schedule-independent exactly as the reference's task DAG
+// (:119-122).
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+#include "dm_internal.h"
+#include "nw.h"
+
+namespace dm {
+namespace {
+
+// Side descriptor: rows [r0, r1) of the buffer, old width -> new width via map.
+struct SideDesc {
+    uint32_t r0, r1;
+    uint32_t w_old, w_new;
+    uint64_t map_off;   // into the column-map buffer (w_new entries)
+    uint64_t gap_off;   // gap list, DESCENDING (path order)
+    uint32_t ngaps;
+    uint32_t pad;
+};
+
+__global__ void init_rows_kernel(const uint8_t* __restrict__ raw, const uint64_t* __restrict__ raw_off,
+                                 const uint32_t* __restrict__ order, uint32_t n, uint8_t* __restrict__ rows,
+                                 uint64_t pitch) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t r = warp; r < n; r += nw) {
+        const uint32_t s = order[r];
+        const uint64_t a = raw_off[s], e = raw_off[s + 1];
+        uint8_t* dst = rows + (uint64_t)r * pitch;
+        for (uint64_t i = a + lane; i < e; i += 32) dst[i - a] = raw[i];
+    }
+}
+
+// One CTA per side: map[o] = source column, or -1 for an inserted gap column.
+__global__ void colmap_kernel(const SideDesc* __restrict__ sides, const uint32_t* __restrict__ gaps,
+                              int32_t* __restrict__ maps) {
+    const SideDesc d = sides[blockIdx.x];
+    int32_t* map = maps + d.map_off;
+    const uint32_t* g = gaps + d.gap_off;  // descending: asc[k] = g[ng-1-k]
+    const uint32_t ng = d.ngaps;
+    for (uint32_t k = threadIdx.x; k < ng; k += blockDim.x) map[g[ng - 1 - k] + k] = -1;
+    for (uint32_t c = threadIdx.x; c < d.w_old; c += blockDim.x) {
+        // count of gap positions <= c  (upper_bound over the ascending view)
+        uint32_t lo = 0, hi = ng;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (g[ng - 1 - mid] <= c) lo = mid + 1;
+            else hi = mid;
+        }
+        map[c + lo] = (int32_t)c;
+    }
+}
+
+// Rows of all sides of a level; row -> side by binary search on prefix sums.
+__global__ void insert_rows_kernel(const SideDesc* __restrict__ sides, const uint32_t* __restrict__ side_rows_prefix,
+                                   uint32_t nsides, uint32_t total_rows, const int32_t* __restrict__ maps,
+                                   uint8_t* __restrict__ rows, uint64_t pitch) {
+    extern __shared__ uint8_t srow[];
+    for (uint32_t t = blockIdx.x; t < total_rows; t += gridDim.x) {
+        uint32_t lo = 0, hi = nsides;  // largest s with prefix[s] <= t
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (side_rows_prefix[mid] <= t) lo = mid;
+            else hi = mid;
+        }
+        const SideDesc d = sides[lo];
+        const uint32_t r = d.r0 + (t - side_rows_prefix[lo]);
+        uint8_t* row = rows + (uint64_t)r * pitch;
+        __syncthreads();
+        for (uint32_t c = threadIdx.x; c < d.w_old; c += blockDim.x) srow[c] = row[c];
+        __syncthreads();
+        const int32_t* map = maps + d.map_off;
+        for (uint32_t o = threadIdx.x; o < d.w_new; o += blockDim.x) {
+            const int32_t src = map[o];
+            row[o] = src < 0 ? (uint8_t)'-' : srow[src];
+        }
+    }
+}
+
+void grow_rows(dm_ctx* ctx, DevBuf& buf, uint64_t& pitch, uint32_t n, uint64_t need) {
+    if (need <= pitch) return;
+    const uint64_t np = ((need + need / 4) + 63) & ~uint64_t(63);
+    DevBuf nb;
+    uint8_t* dst = (uint8_t*)nb.get((uint64_t)n * np);
+    DM_CUDA(cudaMemcpy2DAsync(dst, np, buf.p, pitch, pitch, n, cudaMemcpyDeviceToDevice, ctx->stream));
+    DM_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::swap(buf.p, nb.p);
+    std::swap(buf.cap, nb.cap);
+    pitch = np;
+}
+
+// Apply one batch of sides (their gap lists already on the device).
+void apply_sides(dm_ctx* ctx, std::vector<SideDesc>& sides, const uint32_t* d_gaps, uint8_t* d_rows, uint64_t pitch,
+                 uint64_t max_w_old) {
+    if (sides.empty()) return;
+    uint64_t mtot = 0;
+    std::vector<uint32_t> prefix(sides.size() + 1, 0);
+    for (size_t i = 0; i < sides.size(); ++i) {
+        sides[i].map_off = mtot;
+        mtot += sides[i].w_new;
+        prefix[i + 1] = prefix[i] + (sides[i].r1 - sides[i].r0);
+    }
+    int32_t* d_maps = ctx->colmap.as<int32_t>(std::max<uint64_t>(mtot, 1));
+    SideDesc* d_sides = ctx->tree_buf.as<SideDesc>(sides.size());
+    uint32_t* d_prefix = ctx->aux3.as<uint32_t>(prefix.size());
+    DM_CUDA(cudaMemcpyAsync(d_sides, sides.data(), sides.size() * sizeof(SideDesc), cudaMemcpyHostToDevice,
+                            ctx->stream));
+    DM_CUDA(cudaMemcpyAsync(d_prefix, prefix.data(), prefix.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    colmap_kernel<<<(unsigned)sides.size(), 256, 0, ctx->stream>>>(d_sides, d_gaps, d_maps);
+    DM_CUDA(cudaGetLastError());
+    const uint32_t total = prefix.back();
+    const size_t smem = std::max<uint64_t>(max_w_old, 16);
+    if (smem > 48 * 1024)
+        DM_CUDA(cudaFuncSetAttribute(insert_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int grid = (int)std::max<uint32_t>(1, std::min<uint32_t>(total, (uint32_t)ctx->sm_count * 16));
+    insert_rows_kernel<<<grid, 128, smem, ctx->stream>>>(d_sides, d_prefix, (uint32_t)sides.size(), total, d_maps,
+                                                         d_rows, pitch);
+    DM_CUDA(cudaGetLastError());
+    ctx->launches += 2;
+}
+
+}  // namespace
+
+dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node>& nodes,
+                      const std::vector<uint32_t>& order, const NwScheme& sc, dm_stats* st) {
+    const uint32_t n = s->n;
+    if (order.size() != n) throw invalid_argument("tree order does not match the sequence set");
+    if (nodes.empty()) throw invalid_argument("empty tree");
+    for (int c = 0; c < 256; ++c)
+        if (s->present[c] && (c >= 128 || !sc.has[c]))
+            throw invalid_argument(std::string("sequence a contains symbol '") + (char)c +
+                                   "' absent from the substitution table");
+    auto* out = new dm_msa_out;
+    try {
+        cudaStream_t stream = ctx->stream;
+        std::vector<uint32_t> pos(n);
+        for (uint32_t r = 0; r < n; ++r) pos[order[r]] = r;
+        // widths: leaves carry their sequence
+        std::vector<uint64_t> W(nodes.size(), 0);
+        uint32_t maxdepth = 0, maxlen = 1;
+        for (uint32_t i = 0; i < n; ++i) maxlen = std::max(maxlen, s->len[i]);
+        std::vector<std::vector<uint32_t>> by_depth;
+        for (size_t v = 0; v < nodes.size(); ++v) {
+            const dm_node& nd = nodes[v];
+            if (nd.left < 0) {
+                if (nd.end - nd.begin != 1) throw invalid_argument("align_leaf requires a singleton leaf node");
+                W[v] = s->len[nd.center];
+                continue;
+            }
+            if (by_depth.size() <= nd.depth) by_depth.resize(nd.depth + 1);
+            by_depth[nd.depth].push_back((uint32_t)v);
+            maxdepth = std::max(maxdepth, nd.depth);
+        }
+        uint64_t pitch = ((uint64_t)maxlen + maxlen / 2 + 64 + 63) & ~uint64_t(63);
+        DevBuf& rowsbuf = ctx->rows_a;
+        rowsbuf.get((uint64_t)n * pitch);
+        uint32_t* d_order = ctx->rows_b.as<uint32_t>(n);
+        DM_CUDA(cudaMemcpyAsync(d_order, order.data(), (size_t)n * 4, cudaMemcpyHostToDevice, stream));
+        {
+            const int grid = (int)std::min<uint64_t>((n + 7) / 8, (uint64_t)ctx->sm_count * 16);
+            init_rows_kernel<<<std::max(grid, 1), 256, 0, stream>>>(s->d_raw, s->d_raw_off, d_order, n,
+                                                                   (uint8_t*)rowsbuf.p, pitch);
+            DM_CUDA(cudaGetLastError());
+            ctx->launches += 1;
+        }
+        float fwd_ms = 0, tb_ms = 0;
+        uint64_t cells = 0, nw_calls = 0, launches = 0;
+        for (int d = (int)by_depth.size() - 1; d >= 0; --d) {
+            const auto& lvl = by_depth[d];
+            if (lvl.empty()) continue;
+            std::vector<NwJob> jobs(lvl.size());
+            for (size_t k = 0; k < lvl.size(); ++k) {
+                const dm_node& nd = nodes[lvl[k]];
+                const dm_node& lc = nodes[nd.left];
+                const dm_node& rc = nodes[nd.right];
+                NwJob& jb = jobs[k];
+                jb.a_off = (uint64_t)pos[lc.center] * pitch;
+                jb.n = (uint32_t)W[nd.left];
+                jb.b_off = (uint64_t)pos[rc.center] * pitch;
+                jb.m = (uint32_t)W[nd.right];
+            }
+            NwOut no;
+            nw_run(ctx, (const uint8_t*)rowsbuf.p, jobs, sc, no, st != nullptr);
+            fwd_ms += no.fwd_ms;
+            tb_ms += no.tb_ms;
+            cells += no.cells;
+            nw_calls += jobs.size();
+            launches += no.launches;
+            std::vector<NwRes> res(jobs.size());
+            DM_CUDA(cudaMemcpyAsync(res.data(), no.d_res, res.size() * sizeof(NwRes), cudaMemcpyDeviceToHost, stream));
+            DM_CUDA(cudaStreamSynchronize(stream));
+            uint64_t wmax = 0, wold = 0;
+            std::vector<SideDesc> sides;
+            sides.reserve(2 * jobs.size());
+            for (size_t k = 0; k < lvl.size(); ++k) {
+                const dm_node& nd = nodes[lvl[k]];
+                const dm_node& lc = nodes[nd.left];
+                const dm_node& rc = nodes[nd.right];
+                const uint64_t w = res[k].len;
+                if (w != W[nd.left] + res[k].nga || w != W[nd.right] + res[k].ngb)
+                    throw runtime_error("internal error: aligned width does not match the gap lists");
+                W[lvl[k]] = w;
+                wmax = std::max(wmax, w);
+                wold = std::max<uint64_t>(wold, std::max(W[nd.left], W[nd.right]));
+                if (res[k].nga)
+                    sides.push_back(SideDesc{lc.begin, lc.end, (uint32_t)W[nd.left], (uint32_t)w, 0,
+                                             jobs[k].ga_off, res[k].nga, 0});
+                if (res[k].ngb)
+                    sides.push_back(SideDesc{rc.begin, rc.end, (uint32_t)W[nd.right], (uint32_t)w, 0,
+                                             jobs[k].gb_off, res[k].ngb, 0});
+            }
+            grow_rows(ctx, rowsbuf, pitch, n, wmax);
+            apply_sides(ctx, sides, no.d_gaps, (uint8_t*)rowsbuf.p, pitch, wold);
+            launches += 2;
+        }
+        const uint64_t width = W[0];
+        out->width = width;
+        out->rows.resize((uint64_t)n * width);
+        if (width)
+            DM_CUDA(cudaMemcpy2DAsync(out->rows.data(), width, rowsbuf.p, pitch, width, n, cudaMemcpyDeviceToHost,
+                                      stream));
+        DM_CUDA(cudaStreamSynchronize(stream));
+        out->row_seq = order;
+        out->nodes = nodes;
+        out->order = order;
+        if (st) {
+            st->cells += cells;
+            st->nw_calls += nw_calls;
+            st->launches += launches + 1;
+            st->kernel_ms += fwd_ms + tb_ms;
+        }
+    } catch (...) {
+        delete out;
+        throw;
+    }
+    return out;
+}
+
+void insert_gap_columns(dm_ctx* ctx, const char* rows, uint64_t nrows, uint64_t width, const uint32_t* pos,
+                        uint64_t npos, char* out) {
+    // msa_merge.cpp:31-70 (validation messages :37-44)
+    for (uint64_t i = 0; i < npos; ++i) {
+        if (pos[i] > width)
+            throw invalid_argument("gap position " + std::to_string(pos[i]) + " exceeds alignment width " +
+                                   std::to_string(width));
+        if (i > 0 && pos[i] < pos[i - 1]) throw invalid_argument("gap positions must be sorted ascending");
+    }
+    const uint64_t nw = width + npos;
+    if (nrows == 0) return;
+    if (npos == 0) {
+        std::memcpy(out, rows, nrows * width);
+        return;
+    }
+    const uint64_t pitch = (nw + 63) & ~uint64_t(63);
+    uint8_t* d_rows = (uint8_t*)ctx->rows_a.get(nrows * pitch);
+    DM_CUDA(cudaMemcpy2DAsync(d_rows, pitch, rows, width, width, nrows, cudaMemcpyHostToDevice, ctx->stream));
+    std::vector<uint32_t> desc(npos);
+    for (uint64_t i = 0; i < npos; ++i) desc[i] = pos[npos - 1 - i];
+    uint32_t* d_g = ctx->rows_b.as<uint32_t>(npos);
+    DM_CUDA(cudaMemcpyAsync(d_g, desc.data(), npos * 4, cudaMemcpyHostToDevice, ctx->stream));
+    std::vector<SideDesc> sides{SideDesc{0, (uint32_t)nrows, (uint32_t)width, (uint32_t)nw, 0, 0, (uint32_t)npos, 0}};
+    apply_sides(ctx, sides, d_g, d_rows, pitch, width);
+    DM_CUDA(cudaMemcpy2DAsync(out, nw, d_rows, pitch, nw, nrows, cudaMemcpyDeviceToHost, ctx->stream));
+    DM_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+}  // namespace dm

@@ -1,0 +1,55 @@
+// Batched Gotoh NW (nw.cu) — shared by the pairwise C ABI and the merge
+// scheduler (msa.cu).
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "dm_internal.h"
+
+namespace dm {
+
+// One alignment of a = chars[a_off, a_off+n) against b = chars[b_off, b_off+m).
+struct NwJob {
+    uint64_t a_off, b_off;
+    uint32_t n, m;
+    uint64_t t_off;   // trace bytes: m columns x round16(n) rows (filled by nw_run)
+    uint64_t ga_off;  // gaps_into_a output (capacity m), path order (descending)
+    uint64_t gb_off;  // gaps_into_b output (capacity n), path order (descending)
+};
+
+struct NwRes {
+    int64_t score;
+    uint32_t final_tag;  // 2 - final state
+    uint32_t len;        // aligned length
+    uint32_t nga, ngb;   // gap counts
+};
+
+// Scoring scheme in device form: chars -> dense codes, 4*score table.
+struct NwScheme {
+    uint8_t lut[128] = {};
+    int K = 0, Kp = 1;
+    std::vector<int32_t> table4;  // K x Kp
+    int64_t open = 0, extend = 0;
+    int maxabs = 0;
+    bool has[128] = {};
+};
+
+NwScheme make_scheme(const int16_t* table, const uint8_t* has_symbol, int open_surcharge, int gap_extend);
+
+// Device outputs of one batch (valid until the next nw_run on this ctx).
+struct NwOut {
+    NwRes* d_res = nullptr;
+    uint32_t* d_gaps = nullptr;
+    uint64_t gaps_total = 0;
+    float fwd_ms = 0.f, tb_ms = 0.f;
+    uint64_t cells = 0;
+    uint64_t launches = 0;
+};
+
+// Runs forward + traceback over `jobs` (host array; t_off/ga_off/gb_off are
+// assigned here). `d_chars` is device memory holding every a and b.
+void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const NwScheme& sc,
+            NwOut& out, bool time_kernels);
+
+}  // namespace dm

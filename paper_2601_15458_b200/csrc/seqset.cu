@@ -137,7 +137,10 @@ dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets,
         uint8_t lut[256] = {};
         int nsym = 0;
         for (int c = 0; c < 256; ++c)
-            if (present[c >> 5] & (1u << (c & 31))) lut[c] = (uint8_t)nsym++;
+            if (present[c >> 5] & (1u << (c & 31))) {
+                lut[c] = (uint8_t)nsym++;
+                s->present[c] = true;
+            }
         std::memcpy(s->code_of, lut, 256);
         s->nsym = nsym;
         s->planes = nsym <= 4 ? 2 : (nsym <= 32 ? 5 : 8);
