@@ -1,0 +1,71 @@
+#!/usr/bin/env python
+"""End-to-end MSA timings on the BASELINE MSA configs (cfg0, cfg2, cfg3, cfg4):
+in-memory sequences -> guide tree -> merged MSA rows in host memory, through
+the public API (dm.msa on a SeqSet). Prints one JSON line per config with the
+tree / align device times, the oracle-equivalent Levenshtein + NW cells and
+GCUPS, and (when tests/golden/msa_configs.json has the config) whether the
+output hashes equal the reference's.
+
+    python bench_msa.py --configs 0,3,2 [--scale2 1.0] [--scale4 0.1]
+"""
+import argparse
+import hashlib
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="0,3,2")
+    ap.add_argument("--scale2", type=float, default=1.0)
+    ap.add_argument("--scale4", type=float, default=0.1)
+    ap.add_argument("--repeat", type=int, default=2)
+    args = ap.parse_args()
+    import paper_2601_15458_b200 as dm
+    ctx = dm.default_context(0)
+    golden = {}
+    gp = os.path.join(ROOT, "tests", "golden", "msa_configs.json")
+    if os.path.exists(gp):
+        golden = json.load(open(gp))
+    for cfg in [int(c) for c in args.configs.split(",")]:
+        scale = {2: args.scale2, 4: args.scale4}.get(cfg, 1.0)
+        data, offs = dm.synth(cfg, scale)
+        seqs = list(dict.fromkeys(s.decode() for s in dm.split(data, offs)))
+        sc = dm.ScoringScheme.protein() if cfg == 3 else dm.ScoringScheme.nucleotide()
+        best = None
+        for _ in range(args.repeat):
+            t0 = time.perf_counter()
+            ss = dm.SeqSet(seqs, ctx)
+            m = dm.msa(ss, sc, seed=42)
+            wall = time.perf_counter() - t0
+            if best is None or wall < best[0]:
+                best = (wall, m)
+            del ss
+        wall, m = best
+        st = m.stats
+        key = f"cfg{cfg}@{scale}"
+        match = None
+        if key in golden:
+            h = hashlib.sha256()
+            for r in m.rows:
+                h.update(r.encode())
+                h.update(b"\n")
+            match = h.hexdigest() == golden[key]["rows_sha256"]
+        line = {"config": key, "n": len(seqs), "width": m.width, "wall_s": wall,
+                "tree_ms": st["tree_ms"], "align_ms": st["align_ms"], "cells": st["cells"],
+                "gcups_e2e": st["cells"] / wall / 1e9, "launches": st["launches"], "nw_calls": st["nw_calls"],
+                "reference_match": match,
+                "reference_cpu_s": (golden[key]["tree_s"] + golden[key]["align_s"]) if key in golden else None,
+                "reference_threads": golden[key]["threads"] if key in golden else None}
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

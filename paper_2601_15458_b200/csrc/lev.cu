@@ -29,25 +29,27 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "dm_internal.h"
+#include "lev_chains.h"
 
 namespace dm {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-// Register budget per lane: 4R words of Pv/Mv state + 2*NP*R words of planes.
+// Words (32 rows each) per lane: the register budget is ~(NP + 6) * W.
 template <int NP>
-struct RMax;
+struct WMax;
 template <>
-struct RMax<2> { static constexpr int value = 12; };
+struct WMax<2> { static constexpr int value = 16; };
 template <>
-struct RMax<5> { static constexpr int value = 6; };
+struct WMax<5> { static constexpr int value = 10; };
 template <>
-struct RMax<8> { static constexpr int value = 4; };
+struct WMax<8> { static constexpr int value = 6; };
 
-int rmax_for(int np) { return np == 2 ? RMax<2>::value : (np == 5 ? RMax<5>::value : RMax<8>::value); }
+int wmax_for(int np) { return np == 2 ? WMax<2>::value : (np == 5 ? WMax<5>::value : WMax<8>::value); }
 
 struct LevArgs {
     const LevItem* items;
@@ -60,10 +62,57 @@ struct LevArgs {
     const uint64_t* planes;
     uint32_t* out;
     uint32_t* counter;
+    uint32_t one;  // == 1; opaque to ptxas so the carry chains stay on the FMA pipe
 };
 
-template <int NP, int R>
-__global__ void __launch_bounds__(256) lev_kernel(const LevArgs a) {
+// One lane = W consecutive 32-bit words of the pattern, handled as ONE
+// multi-precision bit-vector (Myers' recurrence needs its addition and
+// shifts to carry across the whole vector; inside a lane the carry flag does
+// it, between lanes the horizontal delta h_in/h_out does, as in Myers'
+// block formulation). Per word and column: NP IMAD (match mask from the
+// bit-planes: P ^ ~m == P * (1 + 2t) + t with t = ~m in {0,-1}), 8 LOP3 and
+// 3 carry-chained adds (add + two 1-bit shifts).
+// FMA-pipe integer helper: with an opaque multiplier (`two`, `one` derive
+// from a runtime 1) ptxas keeps IMAD instead of strength-reducing to ALU ops.
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+template <int LUT>
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+    return d;
+}
+
+// v = (v << 1) | cin over W words; returns the bit shifted out. Per word one
+// IMAD.WIDE (v * 2: low half = v << 1, high half = the bit leaving the word)
+// plus one IMAD folding in the carry from the word below — all on the FMA
+// pipe, which co-issues with the LOP3 stream (IMAD.HI / SHF.L.W do not;
+// measured in tools/ubench/pipes.cu).
+template <int W>
+__device__ __forceinline__ uint32_t shl1(uint32_t (&v)[W], uint32_t cin, uint32_t two, uint32_t one) {
+    uint32_t carry = cin;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        uint32_t lo, hi;
+        asm("{\n\t.reg .u64 t;\n\tmul.wide.u32 t, %2, %3;\n\tmov.b64 {%0, %1}, t;\n\t}"
+            : "=r"(lo), "=r"(hi)
+            : "r"(v[w]), "r"(two));
+        v[w] = imad(lo, one, carry);
+        carry = hi;
+    }
+    return carry;
+}
+
+template <int NP, int W>
+__global__ void __launch_bounds__(256, NP == 2 ? 3 : 1) lev_kernel(const LevArgs a) {
+    constexpr bool TAB = NP == 2;
+    extern __shared__ uint32_t s_tab[];  // TAB: 4 codes x W words x 256 threads
+    // opaque constants (derived from the runtime 1) keep the bit arithmetic on IMAD
+    const uint32_t two = a.one + a.one, four = two + two;
     const int lane = threadIdx.x & 31;
     const int lgG = a.lgG;
     const int G = 1 << lgG;
@@ -82,123 +131,161 @@ __global__ void __launch_bounds__(256) lev_kernel(const LevArgs a) {
         if (valid) item = a.items[it];
         const uint32_t m = valid ? a.len[item.pat] : 0;
         const uint32_t n = valid ? a.len[item.txt] : 0;
-        const uint32_t nb = (m + 63) >> 6;
+        const uint32_t nwords = (m + 31) >> 5;
 
-        uint64_t P[R][NP];
-        uint64_t Pv[R], Mv[R];
-        const uint64_t* pp = a.planes + a.blk[item.pat] * NP;
+        // NP == 2 (<= 4 residue codes, DNA): the lane's match masks for all
+        // four codes live in shared memory, [code][word][thread] so a warp's
+        // 32 lanes always hit 32 distinct banks whatever codes they look up.
+        // Otherwise the bit-planes stay in registers and Eq is rebuilt per
+        // column with one IMAD per plane.
+        constexpr int NPR = TAB ? 1 : NP;
+        uint32_t P[NPR][W];
+        uint32_t Pv[W], Mv[W];
+        const uint32_t* pp = reinterpret_cast<const uint32_t*>(a.planes + a.blk[item.pat] * NP);
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const uint32_t b = (uint32_t)g * R + r;
+        for (int w = 0; w < W; ++w) {
+            const uint32_t gw = (uint32_t)g * W + w;  // global word index in the pattern
+            if constexpr (TAB) {
+                const bool in = valid && gw < nwords;
+                const uint32_t p0 = in ? __ldg(pp + (uint64_t)(gw >> 1) * 4 + (gw & 1)) : 0u;
+                const uint32_t p1 = in ? __ldg(pp + (uint64_t)(gw >> 1) * 4 + 2 + (gw & 1)) : 0u;
+                s_tab[(0 * W + w) * 256 + threadIdx.x] = ~p0 & ~p1;
+                s_tab[(1 * W + w) * 256 + threadIdx.x] = p0 & ~p1;
+                s_tab[(2 * W + w) * 256 + threadIdx.x] = ~p0 & p1;
+                s_tab[(3 * W + w) * 256 + threadIdx.x] = p0 & p1;
+            } else {
 #pragma unroll
-            for (int k = 0; k < NP; ++k) P[r][k] = (valid && b < nb) ? __ldg(pp + (uint64_t)b * NP + k) : 0ull;
-            Pv[r] = ~0ull;
-            Mv[r] = 0ull;
+                for (int k = 0; k < NP; ++k)
+                    P[k][w] = (valid && gw < nwords) ? __ldg(pp + (uint64_t)(gw >> 1) * (2 * NP) + 2 * k + (gw & 1)) : 0u;
+            }
+            Pv[w] = ~0u;
+            Mv[w] = 0u;
         }
-        // rows this lane owns that are real pattern rows
-        const int first_row = g * R * 64;
-        const int own = max(0, min((int)m - first_row, R * 64));
-        int partial = own;  // sum of vertical deltas at column 0 (all +1)
+        const int first_row = g * W * 32;
+        int partial = max(0, min((int)m - first_row, W * 32));
 
         uint32_t steps = valid ? n + (uint32_t)G - 1u : 0u;
         steps = __reduce_max_sync(FULL, steps);
         const uint8_t* tp = a.codes + a.off[item.txt];
         uint32_t word = 0;
         for (uint32_t s = 0; s < steps; ++s) {
+            // word = code << 2 | h_minus << 1 | h_plus; lane 0 synthesises its
+            // own (text code, h_in = +1).
             const uint32_t recv = __shfl_up_sync(FULL, word, 1, G);
-            uint32_t c, hp, hm;
-            if (g == 0) {
-                c = (s < n) ? (uint32_t)tp[s] : 0u;
-                hp = 1u;
-                hm = 0u;
-            } else {
-                c = recv >> 2;
-                hp = recv & 1u;
-                hm = (recv >> 1) & 1u;
-            }
+            const uint32_t own = (g == 0 && s < n) ? (uint32_t)tp[s] : 0u;
+            const uint32_t r = (g == 0) ? imad(own, four, a.one) : recv;
+            const uint32_t c = r >> 2;
+            uint32_t hm = (r >> 1) & 1u;
+            uint32_t hp = r & 1u;
             const uint32_t j = s - (uint32_t)g;
             if (j < n) {
-                uint64_t msk[NP];
+                // t_k = bit_k(c) - 1 (0 or all-ones), s_k = 2 t_k + 1 (+1 / -1)
+                uint32_t ts[NP], ss[NP];
+                if constexpr (!TAB) {
 #pragma unroll
-                for (int k = 0; k < NP; ++k) msk[k] = 0ull - (uint64_t)((c >> k) & 1u);
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    uint64_t eq = ~(P[r][0] ^ msk[0]);
-#pragma unroll
-                    for (int k = 1; k < NP; ++k) eq &= ~(P[r][k] ^ msk[k]);
-                    const uint64_t pv = Pv[r], mv = Mv[r];
-                    const uint64_t xv = eq | mv;
-                    const uint64_t e = eq | (uint64_t)hm;
-                    const uint64_t xh = (((e & pv) + pv) ^ pv) | e;
-                    uint64_t ph = mv | ~(xh | pv);
-                    uint64_t mh = pv & xh;
-                    const uint32_t hpo = (uint32_t)(ph >> 63);
-                    const uint32_t hmo = (uint32_t)(mh >> 63);
-                    ph = (ph << 1) | (uint64_t)hp;
-                    mh = (mh << 1) | (uint64_t)hm;
-                    Pv[r] = mh | ~(xv | ph);
-                    Mv[r] = ph & xv;
-                    hp = hpo;
-                    hm = hmo;
+                    for (int k = 0; k < NP; ++k) {
+                        ts[k] = ((c >> k) & 1u) - 1u;
+                        ss[k] = imad(ts[k], two, a.one);
+                    }
                 }
+                // Myers step, rewritten so Xh is never materialised (7 LOP3 per
+                // word): with E = Eq (| h_minus on row 0), X = E & Pv, S = X + Pv,
+                //   Mh = Pv & Xh         = (Pv & ~S) | X
+                //   Ph = Mv | ~(Xh | Pv) = Mv | ~(S | Pv | Xv (| h_minus))
+                // (on Pv bits S^Pv = ~S; off Pv bits Xh = S | E; Mv bits force Ph).
+                // LUT constants: lop3(a, b, c) truth table over (0xF0, 0xCC, 0xAA).
+                uint32_t X[W], S[W], Ph[W], Mh[W], Xv[W], T[W];
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    uint32_t e;
+                    if constexpr (TAB) {
+                        e = s_tab[(c * W + w) * 256 + threadIdx.x];
+                    } else {
+                        e = imad(P[0][w], ss[0], ts[0]);
+#pragma unroll
+                        for (int k = 1; k < NP; ++k) e &= imad(P[k][w], ss[k], ts[k]);
+                    }
+                    Xv[w] = e | Mv[w];
+                    // row 0 of the lane: h_in = -1 enters as a carry
+                    X[w] = w == 0 ? lop3<0xA8>(e, hm, Pv[w]) : (e & Pv[w]);  // (e | hm) & Pv
+                    T[w] = w == 0 ? lop3<0xFE>(Pv[w], Xv[w], hm) : (Pv[w] | Xv[w]);
+                }
+                Chain<W>::add(S, X, Pv);
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    Mh[w] = lop3<0xBA>(Pv[w], S[w], X[w]);  // (Pv & ~S) | X
+                    Ph[w] = lop3<0xF1>(Mv[w], S[w], T[w]);  // Mv | ~(S | T)
+                }
+                const uint32_t hpo = shl1<W>(Ph, hp, two, a.one);
+                const uint32_t hmo = shl1<W>(Mh, hm, two, a.one);
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    Pv[w] = lop3<0xF1>(Mh[w], Xv[w], Ph[w]);  // Mh | ~(Xv | Ph)
+                    Mv[w] = Ph[w] & Xv[w];
+                }
+                hp = hpo;
+                hm = hmo;
                 if (j == n - 1) {
                     int acc = 0;
 #pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        const int lo = first_row + r * 64;
-                        const int cnt = max(0, min((int)m - lo, 64));
-                        const uint64_t rm = cnt >= 64 ? ~0ull : ((1ull << cnt) - 1ull);
-                        acc += __popcll(Pv[r] & rm) - __popcll(Mv[r] & rm);
+                    for (int w = 0; w < W; ++w) {
+                        const int lo = first_row + w * 32;
+                        const int cnt = max(0, min((int)m - lo, 32));
+                        const uint32_t rm = cnt >= 32 ? ~0u : ((1u << cnt) - 1u);
+                        acc += __popc(Pv[w] & rm) - __popc(Mv[w] & rm);
                     }
                     partial = acc;
                 }
             }
-            word = (c << 2) | (hm << 1) | hp;
+            word = imad(c, four, imad(hm, two, hp));
         }
         for (int o = G >> 1; o > 0; o >>= 1) partial += __shfl_down_sync(FULL, partial, o, G);
         if (valid && g == 0) a.out[item.slot] = n + (uint32_t)partial;
     }
 }
 
-template <int NP, int R>
+template <int NP, int W>
 void launch_one(const LevArgs& a, int sm_count, cudaStream_t st) {
     static int occ = -1;
+    const size_t smem = NP == 2 ? (size_t)4 * W * 256 * sizeof(uint32_t) : 0;
     if (occ < 0) {
-        DM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lev_kernel<NP, R>, 256, 0));
+        if (smem > 48 * 1024)
+            DM_CUDA(cudaFuncSetAttribute(lev_kernel<NP, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        DM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lev_kernel<NP, W>, 256, smem));
         occ = std::max(occ, 1);
     }
     const uint64_t lanes = (uint64_t)a.nitems << a.lgG;
     const uint64_t want = (lanes + 255) / 256;
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)occ * sm_count));
-    lev_kernel<NP, R><<<grid, 256, 0, st>>>(a);
+    lev_kernel<NP, W><<<grid, 256, smem, st>>>(a);
 }
 
-template <int NP, int R>
-void dispatch_r(int r, const LevArgs& a, int sm, cudaStream_t st) {
-    if constexpr (R <= RMax<NP>::value) {
-        if (r == R) {
-            launch_one<NP, R>(a, sm, st);
+template <int NP, int W>
+void dispatch_w(int w, const LevArgs& a, int sm, cudaStream_t st) {
+    if constexpr (W <= WMax<NP>::value) {
+        if (w == W) {
+            launch_one<NP, W>(a, sm, st);
             return;
         }
-        dispatch_r<NP, R + 1>(r, a, sm, st);
+        dispatch_w<NP, W + 1>(w, a, sm, st);
     } else {
-        throw runtime_error("distance engine: unsupported block count");
+        throw runtime_error("distance engine: unsupported word count");
     }
 }
 
-void launch_bucket(int np, int r, const LevArgs& a, int sm, cudaStream_t st) {
-    if (np == 2) dispatch_r<2, 1>(r, a, sm, st);
-    else if (np == 5) dispatch_r<5, 1>(r, a, sm, st);
-    else dispatch_r<8, 1>(r, a, sm, st);
+void launch_bucket(int np, int w, const LevArgs& a, int sm, cudaStream_t st) {
+    if (np == 2) dispatch_w<2, 1>(w, a, sm, st);
+    else if (np == 5) dispatch_w<5, 1>(w, a, sm, st);
+    else dispatch_w<8, 1>(w, a, sm, st);
 }
 
-constexpr int kBuckets = 6 * 16;
+constexpr int kBuckets = 6 * 32;  // (log2 G) * 32 + W
 
 // Orient each job (shorter string = pattern), pick (G, R) and build the
 // radix key (bucket << 32 | ~n) so one sort groups buckets and balances warps.
 __global__ void plan_kernel(const uint32_t* __restrict__ ia, const uint32_t* __restrict__ ib,
                             const LevItem* __restrict__ in_items, uint64_t n,
-                            const uint32_t* __restrict__ len, int lg_gpar, int rmax,
+                            const uint32_t* __restrict__ len, int lg_gpar, int wmax,
                             LevItem* __restrict__ items, uint64_t* __restrict__ keys,
                             uint32_t* __restrict__ idx, unsigned int* __restrict__ hist,
                             unsigned long long* __restrict__ cells) {
@@ -225,19 +312,19 @@ __global__ void plan_kernel(const uint32_t* __restrict__ ia, const uint32_t* __r
             const uint32_t t = x; x = y; y = t;
             const uint32_t tl = lx; lx = ly; ly = tl;
         }
-        const uint32_t B = (lx + 63) >> 6;
+        const uint32_t B = (lx + 31) >> 5;  // 32-row words of the pattern
         int lg = lg_gpar;
-        while ((uint32_t)(rmax << lg) < B && lg < 5) ++lg;
-        uint32_t R = (B + (1u << lg) - 1) >> lg;
+        while ((uint32_t)(wmax << lg) < B && lg < 5) ++lg;
+        uint32_t R = (B + (1u << lg) - 1) >> lg;  // words per lane
         if (R < 1) R = 1;
-        uint32_t bucket = (uint32_t)lg * 16 + R;
-        if (R > (uint32_t)rmax) bucket = kBuckets - 1;  // too long: flagged below
+        uint32_t bucket = (uint32_t)lg * 32 + R;
+        if (R > (uint32_t)wmax) bucket = kBuckets - 1;  // too long: flagged below
         items[i] = LevItem{x, y, slot};
         keys[i] = ((uint64_t)bucket << 32) | (uint64_t)(0xffffffffu - ly);
         idx[i] = (uint32_t)i;
         atomicAdd(&sh[bucket], 1u);
         c0 += (unsigned long long)lx * ly;
-        c1 += (unsigned long long)(R << lg) * 64ull * ly;
+        c1 += (unsigned long long)(R << lg) * 32ull * ly;
     }
     atomicAdd(&scells[0], c0);
     atomicAdd(&scells[1], c1);
@@ -263,7 +350,11 @@ void run_planned(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const ui
     if (n > 0xffffffffull) throw invalid_argument("too many distance jobs in one batch");
     cudaStream_t st = ctx->stream;
     const int np = s->planes;
-    const int rmax = rmax_for(np);
+    int wmax = wmax_for(np);
+    if (const char* e = std::getenv("DM_LEV_WMAX")) {  // tuning knob: cap words per lane
+        const int v = std::atoi(e);
+        if (v >= 1 && v < wmax) wmax = v;
+    }
     const uint64_t target = (uint64_t)ctx->sm_count * 512;  // lanes wanted in flight
     int lg_gpar = 0;
     while (lg_gpar < 5 && (n << lg_gpar) < target) ++lg_gpar;
@@ -291,7 +382,7 @@ void run_planned(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const ui
 
     DM_CUDA(cudaMemsetAsync(hist, 0, hist_b, st));
     const int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)ctx->sm_count * 8);
-    plan_kernel<<<grid, 256, 0, st>>>(d_ia, d_ib, d_in_items, n, s->d_len, lg_gpar, rmax, it0, k0, i0,
+    plan_kernel<<<grid, 256, 0, st>>>(d_ia, d_ib, d_in_items, n, s->d_len, lg_gpar, wmax, it0, k0, i0,
                                       hist, cells);
     DM_CUDA(cudaGetLastError());
     DM_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_b, k0, k1, i0, i1, (int)n, 0, 40, st));
@@ -304,7 +395,7 @@ void run_planned(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const ui
     DM_CUDA(cudaStreamSynchronize(st));
     if (h[kBuckets - 1])
         throw invalid_argument("sequence too long for the distance engine (max " +
-                               std::to_string(32 * rmax * 64) + " residues for this alphabet)");
+                               std::to_string(32 * wmax * 32) + " residues for this alphabet)");
     if (time_kernels) DM_CUDA(cudaEventRecord(ctx->ev0, st));
     uint64_t start = 0;
     int launches = 0;
@@ -313,7 +404,7 @@ void run_planned(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const ui
         LevArgs a;
         a.items = it1 + start;
         a.nitems = h[b];
-        a.lgG = b / 16;
+        a.lgG = b / 32;
         a.codes = s->d_codes;
         a.off = s->d_off;
         a.len = s->d_len;
@@ -321,7 +412,8 @@ void run_planned(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const ui
         a.planes = s->d_planes;
         a.out = d_out;
         a.counter = counters + b;
-        launch_bucket(np, b % 16, a, ctx->sm_count, st);
+        a.one = 1u;
+        launch_bucket(np, b % 32, a, ctx->sm_count, st);
         DM_CUDA(cudaGetLastError());
         start += h[b];
         ++launches;

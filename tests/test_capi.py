@@ -1,0 +1,77 @@
+"""CPU: the C ABI library loads, exports every symbol include/dm_b200.h
+declares, and its host-only entry points behave (no GPU compute here)."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "dm_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(dm_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol(dm):
+    from paper_2601_15458_b200._lib import LIB_PATH, SIGNATURES
+    L = C.CDLL(LIB_PATH)
+    decl = declared_symbols()
+    assert len(decl) >= 40
+    missing = [s for s in decl if not hasattr(L, s)]
+    assert not missing, missing
+    unbound = [s for s in decl if s not in SIGNATURES]
+    assert not unbound, unbound
+
+
+def test_library_is_sm100a(dm):
+    import subprocess
+    from paper_2601_15458_b200._lib import LIB_PATH
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", LIB_PATH], capture_output=True, text=True)
+    assert out.returncode == 0
+    assert "sm_100a" in out.stdout
+
+
+def test_no_gpu_fails_loudly(dm):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    with pytest.raises(dm.DmError):
+        dm.Context(0)
+
+
+def test_scheme_tables_host_side(dm, orc):
+    s = dm.ScoringScheme.nucleotide()
+    assert np.array_equal(s.table, orc.table("nt"))
+    assert s.open_surcharge() == -10
+    p = dm.ScoringScheme.protein(-11, -2, "flat")
+    assert np.array_equal(p.table, orc.table("aa", -2)) and p.open_surcharge() == 0
+    with pytest.raises(ValueError, match="not symmetric"):
+        dm.ScoringScheme.custom("AC", [1, -1, -2, 1], -5, -1)
+    with pytest.raises(ValueError):
+        dm.ScoringScheme.custom("AC", [1, -1, -1, 1], -1, -5)
+
+
+def test_scheme_tables_match_reference(dm, ref):
+    for kind, ctor in (("nt", dm.ScoringScheme.nucleotide), ("aa", dm.ScoringScheme.protein)):
+        t, osur = ref.scheme_table(kind, -7, -3, False)
+        s = ctor(-7, -3)
+        assert np.array_equal(s.table, t) and s.open_surcharge() == osur
+
+
+def test_synth_shapes_and_determinism(dm):
+    d0, o0 = dm.synth(0, scale=0.2)
+    d1, o1 = dm.synth(0, scale=0.2)
+    assert d0 == d1 and np.array_equal(o0, o1)
+    assert len(o0) - 1 == 200
+    lens = np.diff(o0)
+    assert 200 < lens.mean() < 400
+    assert set(d0) <= set(b"ACGT")
+    d, o = dm.synth(3, scale=0.01)
+    assert set(d) <= set(b"ARNDCQEGHILKMFPSTWYV")
+    d, o = dm.synth(1, scale=0.0005)
+    lens = np.diff(o)
+    assert len(lens) == 1000 and lens[0::2].min() >= 500 and lens[0::2].max() <= 1500

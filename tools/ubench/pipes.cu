@@ -1,0 +1,59 @@
+// Pipe-throughput microbenchmark: lane-ops/s of instruction mixes on one B200.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+template <int MODE>
+__global__ void k(uint32_t* out, int iters, uint32_t seed) {
+  uint32_t a[8], b = seed * 2654435761u + threadIdx.x, c = seed ^ (blockIdx.x * 7919u), one = seed;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) a[q] = threadIdx.x * (q + 3) + seed;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (MODE == 0) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[q]) : "r"(b), "r"(c));
+        if (MODE == 1) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[q]) : "r"(b | 1u), "r"(c));
+        if (MODE == 2) asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(a[q]) : "r"(b | 1u), "r"(c));
+        if (MODE == 3) { if (q & 1) asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(a[q]) : "r"(b | 1u), "r"(c));
+                         else asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[q]) : "r"(b), "r"(c)); }
+        if (MODE == 4) { if (q & 1) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[q]) : "r"(b | 1u), "r"(c));
+                         else asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[q]) : "r"(b), "r"(c)); }
+        if (MODE == 5) asm volatile("shf.l.wrap.b32 %0, %0, %1, 1;" : "+r"(a[q]) : "r"(b));
+        if (MODE == 7) { uint64_t w; asm volatile("mad.wide.u32 %0, %1, %2, %3;" : "=l"(w) : "r"(a[q]), "r"(b | 1u), "l"((uint64_t)c)); a[q] = (uint32_t)w ^ (uint32_t)(w >> 32); }
+        if (MODE == 8) { if (q & 1) { uint64_t w; asm volatile("mad.wide.u32 %0, %1, %2, %3;" : "=l"(w) : "r"(a[q]), "r"(b | 1u), "l"((uint64_t)c)); a[q] = (uint32_t)w; }
+                         else asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[q]) : "r"(b), "r"(c)); }
+        if (MODE == 9) { if (q & 1) asm volatile("add.cc.u32 %0, %0, %1;\n\taddc.u32 %0, %0, %1;" : "+r"(a[q]) : "r"(b));
+                         else asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[q]) : "r"(b | 1u), "r"(c)); }
+        if (MODE == 6) { if (q & 1) asm volatile("shf.l.wrap.b32 %0, %0, %1, 1;" : "+r"(a[q]) : "r"(b));
+                         else asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[q]) : "r"(b | 1u), "r"(c)); }
+      }
+    }
+    b += 0x9e3779b9u; c ^= b;
+  }
+  uint32_t r = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) r ^= a[q];
+  if (r == 0x12345678u) out[0] = r + one;
+}
+
+template <int M> double run(uint32_t* d, int sms) {
+  const int iters = 2048, blocks = sms * 8;
+  k<M><<<blocks, 256>>>(d, iters, 1u);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int r = 0; r < 5; ++r) k<M><<<blocks, 256>>>(d, iters, 1u);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  return (double)blocks * 256 * iters * 16 * 8 * 5 / (ms * 1e-3);
+}
+
+int main() {
+  uint32_t* d; cudaMalloc(&d, 64);
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const char* names[] = {"LOP3", "IMAD", "IMAD.HI", "LOP3+IMAD.HI", "LOP3+IMAD", "SHF.L.W", "SHF+IMAD", "IMAD.WIDE(+LOP3)", "LOP3+IMAD.WIDE", "IADD3cc+IMAD"};
+  double v[10] = {run<0>(d, sms), run<1>(d, sms), run<2>(d, sms), run<3>(d, sms), run<4>(d, sms), run<5>(d, sms), run<6>(d, sms), run<7>(d, sms), run<8>(d, sms), run<9>(d, sms)};
+  for (int i = 0; i < 10; ++i) printf("%-14s %.3e lane-ops/s\n", names[i], v[i]);
+  return 0;
+}
