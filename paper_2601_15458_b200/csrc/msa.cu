@@ -18,6 +18,9 @@
 // The result is schedule-independent exactly as the reference's task DAG
 // (:119-122).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -182,6 +185,7 @@ dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node
             DM_CUDA(cudaGetLastError());
             ctx->launches += 1;
         }
+        const bool trace = std::getenv("DM_TRACE") != nullptr;
         float fwd_ms = 0, tb_ms = 0;
         uint64_t cells = 0, nw_calls = 0, launches = 0;
         for (int d = (int)by_depth.size() - 1; d >= 0; --d) {
@@ -199,7 +203,8 @@ dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node
                 jb.m = (uint32_t)W[nd.right];
             }
             NwOut no;
-            nw_run(ctx, (const uint8_t*)rowsbuf.p, jobs, sc, no, st != nullptr);
+            const auto h0 = std::chrono::steady_clock::now();
+            nw_run(ctx, (const uint8_t*)rowsbuf.p, jobs, sc, no, st != nullptr || trace);
             fwd_ms += no.fwd_ms;
             tb_ms += no.tb_ms;
             cells += no.cells;
@@ -231,6 +236,13 @@ dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node
             grow_rows(ctx, rowsbuf, pitch, n, wmax);
             apply_sides(ctx, sides, no.d_gaps, (uint8_t*)rowsbuf.p, pitch, wold);
             launches += 2;
+            if (trace) {
+                DM_CUDA(cudaStreamSynchronize(stream));
+                const double ms =
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+                std::fprintf(stderr, "[dm align] depth %d merges %zu cells %.3e fwd %.3f ms tb %.3f ms level %.3f ms\n",
+                             d, jobs.size(), (double)no.cells, no.fwd_ms, no.tb_ms, ms);
+            }
         }
         const uint64_t width = W[0];
         out->width = width;

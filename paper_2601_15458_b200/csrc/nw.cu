@@ -32,170 +32,12 @@
 
 #include "dm_internal.h"
 #include "nw.h"
+#include "nw_fwd.cuh"
 
 namespace dm {
 namespace {
 
-constexpr unsigned FULL = 0xffffffffu;
-constexpr int RR = 16;  // rows per lane
-constexpr int PASS = 32 * RR;
-
-template <class V>
-__device__ __forceinline__ V neg_inf();
-template <>
-__device__ __forceinline__ int32_t neg_inf<int32_t>() { return -(1 << 30); }
-template <>
-__device__ __forceinline__ int64_t neg_inf<int64_t>() { return -(1ll << 60); }
-
-__device__ __forceinline__ int32_t vmax3(int32_t a, int32_t b, int32_t c) { return __vimax3_s32(a, b, c); }
-__device__ __forceinline__ int64_t vmax3(int64_t a, int64_t b, int64_t c) { return max(max(a, b), c); }
-__device__ __forceinline__ int32_t addmax(int32_t a, int32_t b, int32_t c) { return __viaddmax_s32(a, b, c); }
-__device__ __forceinline__ int64_t addmax(int64_t a, int64_t b, int64_t c) { return max(a + b, c); }
-
-template <class V>
-__device__ __forceinline__ V shfl_up(V v) {
-    if constexpr (sizeof(V) == 4) {
-        return __shfl_up_sync(FULL, v, 1);
-    } else {
-        return (V)__shfl_up_sync(FULL, (long long)v, 1);
-    }
-}
-
-struct FwdArgs {
-    const uint8_t* chars;
-    const NwJob* jobs;
-    uint32_t njobs;
-    const uint8_t* lut;
-    const int32_t* table;  // 4*score, K x Kp
-    int K, Kp;
-    int64_t O4, E4;
-    uint8_t* trace;
-    void* passbuf;  // per warp: 3 x (mmax+1) values
-    uint32_t mmax;
-    NwRes* res;
-    uint32_t* counter;
-};
-
-template <class V>
-__global__ void __launch_bounds__(128) nw_fwd_kernel(const FwdArgs a) {
-    extern __shared__ int32_t s_table[];
-    __shared__ uint8_t s_lut[128];
-    for (int x = threadIdx.x; x < a.K * a.Kp; x += blockDim.x) s_table[x] = a.table[x];
-    for (int x = threadIdx.x; x < 128; x += blockDim.x) s_lut[x] = a.lut[x];
-    __syncthreads();
-    const int g = threadIdx.x & 31;
-    const uint32_t wglob = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    V* pbuf = reinterpret_cast<V*>(a.passbuf) + (uint64_t)wglob * 3 * (a.mmax + 1);
-    const V NEG = neg_inf<V>();
-    const V O4 = (V)a.O4, E4 = (V)a.E4;
-    for (;;) {
-        uint32_t jid = 0;
-        if (g == 0) jid = atomicAdd(a.counter, 1u);
-        jid = __shfl_sync(FULL, jid, 0);
-        if (jid >= a.njobs) break;
-        const NwJob job = a.jobs[jid];
-        const uint32_t n = job.n, m = job.m;
-        const uint8_t* A = a.chars + job.a_off;
-        const uint8_t* B = a.chars + job.b_off;
-        const uint32_t pa = (n + 15) & ~15u;
-        uint8_t* T = a.trace + job.t_off;
-        for (uint32_t p0 = 0; p0 < n; p0 += PASS) {
-            const uint32_t i0 = p0 + (uint32_t)g * RR + 1;
-            int ca[RR];
-            V LM[RR], LGB[RR], LGA[RR];
-#pragma unroll
-            for (int r = 0; r < RR; ++r) {
-                const uint32_t i = i0 + r;
-                ca[r] = i <= n ? (int)s_lut[A[i - 1] & 127] * a.Kp : 0;
-                LM[r] = (V)(NEG | 2);
-                LGA[r] = NEG;
-                LGB[r] = (V)((a.O4 + (int64_t)i * a.E4) | 1);  // column 0: GB = open + i*extend
-            }
-            // values of row i0-1 at column 0 (the first row's diagonal at column 1)
-            V pM, pGB, pGA;
-            if (i0 == 1) {
-                pM = 2;  // M[0][0] = 0
-                pGB = (V)(NEG | 1);
-                pGA = NEG;
-            } else {
-                pM = (V)(NEG | 2);
-                pGB = (V)((a.O4 + (int64_t)(i0 - 1) * a.E4) | 1);
-                pGA = NEG;
-            }
-            V sM = 0, sGB = 0, sGA = 0;
-            const bool store_pass = (g == 31) && (p0 + PASS < n);
-            const uint32_t steps = m + 31;
-            for (uint32_t s = 0; s < steps; ++s) {
-                const V rM = shfl_up(sM), rGB = shfl_up(sGB), rGA = shfl_up(sGA);
-                const uint32_t j = s - (uint32_t)g + 1;  // 1..m when active
-                if (j - 1 < m) {
-                    V uM, uGB, uGA;
-                    if (g == 0) {
-                        if (p0 == 0) {  // row 0 (pairwise.cpp:322-330)
-                            uM = (V)(NEG | 2);
-                            uGB = (V)(NEG | 1);
-                            uGA = (V)(a.O4 + (int64_t)j * a.E4);
-                        } else {
-                            uM = pbuf[j];
-                            uGB = pbuf[(a.mmax + 1) + j];
-                            uGA = pbuf[2 * (a.mmax + 1) + j];
-                        }
-                    } else {
-                        uM = rM;
-                        uGB = rGB;
-                        uGA = rGA;
-                    }
-                    V dM = pM, dGB = pGB, dGA = pGA;
-                    pM = uM;
-                    pGB = uGB;
-                    pGA = uGA;
-                    const int cb = s_lut[B[j - 1] & 127];
-                    uint32_t tw[RR / 4];
-#pragma unroll
-                    for (int q = 0; q < RR / 4; ++q) tw[q] = 0;
-#pragma unroll
-                    for (int r = 0; r < RR; ++r) {
-                        const V mraw = vmax3(dM, dGB, dGA) + (V)s_table[ca[r] + cb];
-                        const V gbraw = addmax(uGA, O4, addmax(uM, O4, uGB)) + E4;
-                        const V garaw = addmax(LGB[r], O4, addmax(LM[r], O4, LGA[r])) + E4;
-                        const V nM = (mraw & ~(V)3) | 2;
-                        const V nGB = (gbraw & ~(V)3) | 1;
-                        const V nGA = garaw & ~(V)3;
-                        const uint32_t code = ((uint32_t)mraw & 3u) | (((uint32_t)gbraw & 3u) << 2) |
-                                              (((uint32_t)garaw & 3u) << 4);
-                        tw[r >> 2] |= code << ((r & 3) * 8);
-                        if (j == m && i0 + r == n) {  // pairwise.cpp:374-375
-                            const V fin = vmax3(nM, nGB, nGA);
-                            a.res[jid].score = (int64_t)(fin >> 2);
-                            a.res[jid].final_tag = (uint32_t)(fin & 3);
-                        }
-                        dM = LM[r];
-                        dGB = LGB[r];
-                        dGA = LGA[r];
-                        LM[r] = nM;
-                        LGB[r] = nGB;
-                        LGA[r] = nGA;
-                        uM = nM;
-                        uGB = nGB;
-                        uGA = nGA;
-                    }
-                    sM = uM;
-                    sGB = uGB;
-                    sGA = uGA;
-                    if (store_pass) {
-                        pbuf[j] = uM;
-                        pbuf[(a.mmax + 1) + j] = uGB;
-                        pbuf[2 * (a.mmax + 1) + j] = uGA;
-                    }
-                    if (i0 <= n)
-                        *reinterpret_cast<uint4*>(T + (uint64_t)(j - 1) * pa + (i0 - 1)) =
-                            make_uint4(tw[0], tw[1], tw[2], tw[3]);
-                }
-            }
-            __syncwarp();
-        }
-    }
-}
+using nwk::FULL;
 
 struct TbArgs {
     const NwJob* jobs;
@@ -224,7 +66,8 @@ __global__ void __launch_bounds__(128) nw_traceback_kernel(const TbArgs a) {
         const uint8_t* T = a.trace + job.t_off;
         uint32_t* ga = a.gaps + job.ga_off;
         uint32_t* gb = a.gaps + job.gb_off;
-        uint32_t state = 2u - a.res[jid].final_tag;  // 0 M, 1 GapB, 2 GapA
+        NwRes& res = a.res[job.slot];
+        uint32_t state = 2u - res.final_tag;  // 0 M, 1 GapB, 2 GapA
         uint32_t i = n, j = job.m, len = 0, nga = 0, ngb = 0;
         while (i > 0 && j > 0) {
             const uint32_t jtop = j;
@@ -275,25 +118,37 @@ __global__ void __launch_bounds__(128) nw_traceback_kernel(const TbArgs a) {
                 --i;
                 ++len;
             }
-            a.res[jid].len = len;
-            a.res[jid].nga = nga;
-            a.res[jid].ngb = ngb;
+            res.len = len;
+            res.nga = nga;
+            res.ngb = ngb;
         }
     }
 }
 
-template <class V>
-void launch_fwd(dm_ctx* ctx, const FwdArgs& fa, int grid, size_t smem) {
-    DM_CUDA(cudaFuncSetAttribute(nw_fwd_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    nw_fwd_kernel<V><<<grid, 128, smem, ctx->stream>>>(fa);
+template <class V, int NWW>
+void launch_fwd(dm_ctx* ctx, const nwk::FwdArgs& fa, size_t smem) {
+    static int occ = -1;
+    if (occ < 0) {
+        DM_CUDA(cudaFuncSetAttribute(nwk::nw_fwd_kernel<V, NWW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     48 * 1024));
+        DM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nwk::nw_fwd_kernel<V, NWW>, NWW * 32, smem));
+        occ = std::max(occ, 1);
+    }
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(fa.njobs, (uint64_t)occ * ctx->sm_count));
+    nwk::nw_fwd_kernel<V, NWW><<<grid, NWW * 32, smem, ctx->stream>>>(fa);
 }
 
 template <class V>
-int fwd_occupancy(size_t smem) {
-    int occ = 0;
-    DM_CUDA(cudaFuncSetAttribute(nw_fwd_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    DM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nw_fwd_kernel<V>, 128, smem));
-    return std::max(occ, 1);
+void launch_group(dm_ctx* ctx, int nww, const nwk::FwdArgs& fa, size_t smem) {
+    if (nww == 1) launch_fwd<V, 1>(ctx, fa, smem);
+    else if (nww == 4) launch_fwd<V, 4>(ctx, fa, smem);
+    else launch_fwd<V, 8>(ctx, fa, smem);
+}
+
+// warps per alignment: one band per warp up to 8 bands
+int group_of(uint32_t n) {
+    const uint32_t nb = (n + nwk::BAND - 1) / nwk::BAND;
+    return nb <= 1 ? 1 : (nb <= 4 ? 4 : 8);
 }
 
 }  // namespace
@@ -354,35 +209,50 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
                             ctx->stream));
     DM_CUDA(cudaMemcpyAsync(d_lut, sc.lut, 128, cudaMemcpyHostToDevice, ctx->stream));
 
-    // chunk by trace budget
-    const uint64_t budget = std::max<uint64_t>(ttot < (6ull << 30) ? ttot : (6ull << 30), 1);
-    const int occ = wide ? fwd_occupancy<int64_t>(smem) : fwd_occupancy<int32_t>(smem);
+    // Larger alignments first (better tail balance), grouped by warps per
+    // alignment; chunked by a trace-memory budget.
+    std::vector<NwJob> sj(jobs);
+    for (size_t k = 0; k < nj; ++k) sj[k].slot = (uint32_t)k;
+    std::stable_sort(sj.begin(), sj.end(), [](const NwJob& x, const NwJob& y) {
+        const int gx = group_of(x.n), gy = group_of(y.n);
+        if (gx != gy) return gx > gy;
+        return (uint64_t)x.n * x.m > (uint64_t)y.n * y.m;
+    });
+    const uint64_t budget = std::max<uint64_t>(std::min<uint64_t>(ttot, 6ull << 30), 1);
     size_t c0 = 0;
     while (c0 < nj) {
         size_t c1 = c0;
         uint64_t tb = 0;
         while (c1 < nj) {
-            const uint64_t t = (uint64_t)jobs[c1].m * ((jobs[c1].n + 15) & ~15u);
+            const uint64_t t = (uint64_t)sj[c1].m * ((sj[c1].n + 15) & ~15u);
             if (c1 > c0 && tb + t > budget) break;
-            jobs[c1].t_off = tb;
+            sj[c1].t_off = tb;
             tb += t;
             ++c1;
         }
         const uint32_t cnt = (uint32_t)(c1 - c0);
         uint8_t* d_trace = (uint8_t*)ctx->nw_trace.get(tb + 64);
         NwJob* d_jobs = ctx->nw_jobs.as<NwJob>(cnt);
-        DM_CUDA(cudaMemcpyAsync(d_jobs, jobs.data() + c0, cnt * sizeof(NwJob), cudaMemcpyHostToDevice, ctx->stream));
-        uint32_t* d_cnt = ctx->counter.as<uint32_t>(2);
-        DM_CUDA(cudaMemsetAsync(d_cnt, 0, 8, ctx->stream));
-        const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((cnt + 3) / 4, (uint64_t)occ * ctx->sm_count));
-        const uint64_t warps = (uint64_t)grid * 4;
-        void* d_pass = ctx->nw_in.get(warps * 3 * (mmax + 1) * (wide ? 8 : 4));
-        FwdArgs fa{d_chars, d_jobs, cnt, d_lut, d_table, sc.K, sc.Kp, 4 * sc.open, 4 * sc.extend, d_trace, d_pass,
-                   mmax, out.d_res + c0, d_cnt};
+        DM_CUDA(cudaMemcpyAsync(d_jobs, sj.data() + c0, cnt * sizeof(NwJob), cudaMemcpyHostToDevice, ctx->stream));
+        uint32_t* d_cnt = ctx->counter.as<uint32_t>(4);
+        DM_CUDA(cudaMemsetAsync(d_cnt, 0, 16, ctx->stream));
         if (time_kernels) DM_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-        if (wide) launch_fwd<int64_t>(ctx, fa, grid, smem);
-        else launch_fwd<int32_t>(ctx, fa, grid, smem);
-        DM_CUDA(cudaGetLastError());
+        size_t g0 = c0;
+        int gi = 0;
+        while (g0 < c1) {  // one launch per warps-per-alignment group
+            const int grp = group_of(sj[g0].n);
+            size_t g1 = g0;
+            while (g1 < c1 && group_of(sj[g1].n) == grp) ++g1;
+            nwk::FwdArgs fa{d_chars, d_jobs + (g0 - c0), (uint32_t)(g1 - g0), d_lut, d_table, sc.K, sc.Kp,
+                            4 * sc.open, 4 * sc.extend, d_trace, out.d_res, d_cnt + gi};
+            if (wide) launch_group<int64_t>(ctx, grp, fa, smem);
+            else launch_group<int32_t>(ctx, grp, fa, smem);
+            DM_CUDA(cudaGetLastError());
+            out.launches += 1;
+            ctx->launches += 1;
+            g0 = g1;
+            ++gi;
+        }
         if (time_kernels) {
             DM_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
             DM_CUDA(cudaEventSynchronize(ctx->ev1));
@@ -391,7 +261,7 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
             out.fwd_ms += ms;
             DM_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
         }
-        TbArgs ta{d_jobs, cnt, d_trace, out.d_res + c0, out.d_gaps, d_cnt + 1};
+        TbArgs ta{d_jobs, cnt, d_trace, out.d_res, out.d_gaps, d_cnt + 3};
         const int tgrid = (int)std::max<uint64_t>(1, std::min<uint64_t>((cnt + 3) / 4, (uint64_t)ctx->sm_count * 8));
         nw_traceback_kernel<<<tgrid, 128, 0, ctx->stream>>>(ta);
         DM_CUDA(cudaGetLastError());
@@ -402,8 +272,8 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
             DM_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
             out.tb_ms += ms;
         }
-        out.launches += 2;
-        ctx->launches += 2;
+        out.launches += 1;
+        ctx->launches += 1;
         if (c1 < nj) DM_CUDA(cudaStreamSynchronize(ctx->stream));  // trace buffer reused by the next chunk
         c0 = c1;
     }

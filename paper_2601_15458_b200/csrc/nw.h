@@ -16,6 +16,8 @@ struct NwJob {
     uint64_t t_off;   // trace bytes: m columns x round16(n) rows (filled by nw_run)
     uint64_t ga_off;  // gaps_into_a output (capacity m), path order (descending)
     uint64_t gb_off;  // gaps_into_b output (capacity n), path order (descending)
+    uint32_t slot;    // index of the result (set by nw_run)
+    uint32_t pad;
 };
 
 struct NwRes {

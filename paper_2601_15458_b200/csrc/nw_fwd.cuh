@@ -1,0 +1,243 @@
+// Gotoh NW forward pass (K5), included by nw.cu. See nw.cu for the tagged
+// score encoding and the trace layout.
+//
+// Work decomposition: one alignment per CTA of NWW warps. The rows of a are
+// cut into bands of 32*RR rows; warp w sweeps bands w, w+NWW, ... Inside a
+// band the 32 lanes form a diagonal pipeline over the columns of b (lane g
+// is on column s-g+1 at step s; the bottom row of lane g-1 arrives by three
+// __shfl_up). Between bands, lane 31 of the band above streams its bottom
+// row (M, GapB, GapA per column) through a shared-memory ring to lane 0 of
+// the band below, so all bands of one alignment run concurrently, a few
+// columns apart, instead of one after another: the latency of a 2400 x 2400
+// merge drops from 5 sequential passes to ~1. Flow control is two monotonic
+// sequence counters per ring (published / consumed), checked once per
+// CHUNK columns. NWW = 1 is the plain warp-per-alignment kernel for
+// single-band alignments.
+#pragma once
+
+namespace dm {
+namespace nwk {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int RR = 16;           // rows per lane
+constexpr int BAND = 32 * RR;    // rows per band (one warp)
+constexpr int RING = 128;        // columns buffered between two bands
+constexpr int CHUNK = 16;        // flow-control granularity (columns)
+
+template <class V>
+__device__ __forceinline__ V neg_inf();
+template <>
+__device__ __forceinline__ int32_t neg_inf<int32_t>() { return -(1 << 30); }
+template <>
+__device__ __forceinline__ int64_t neg_inf<int64_t>() { return -(1ll << 60); }
+
+__device__ __forceinline__ int32_t vmax3(int32_t a, int32_t b, int32_t c) { return __vimax3_s32(a, b, c); }
+__device__ __forceinline__ int64_t vmax3(int64_t a, int64_t b, int64_t c) { return max(max(a, b), c); }
+__device__ __forceinline__ int32_t addmax(int32_t a, int32_t b, int32_t c) { return __viaddmax_s32(a, b, c); }
+__device__ __forceinline__ int64_t addmax(int64_t a, int64_t b, int64_t c) { return max(a + b, c); }
+
+template <class V>
+__device__ __forceinline__ V shfl_up1(V v) {
+    if constexpr (sizeof(V) == 4) {
+        return __shfl_up_sync(FULL, v, 1);
+    } else {
+        return (V)__shfl_up_sync(FULL, (long long)v, 1);
+    }
+}
+
+// low bytes of four values -> one word (byte k = low byte of value k)
+__device__ __forceinline__ uint32_t gather_lo(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    const uint32_t ab = __byte_perm(a, b, 0x0040);
+    const uint32_t cd = __byte_perm(c, d, 0x0040);
+    return __byte_perm(ab, cd, 0x5410);
+}
+
+struct FwdArgs {
+    const uint8_t* chars;
+    const NwJob* jobs;
+    uint32_t njobs;
+    const uint8_t* lut;
+    const int32_t* table;  // 4*score, K x Kp
+    int K, Kp;
+    int64_t O4, E4;
+    uint8_t* trace;
+    NwRes* res;
+    uint32_t* counter;
+};
+
+template <class V, int NWW>
+struct FwdSmem {
+    V ring[NWW > 1 ? NWW : 1][RING][3];
+    volatile uint32_t pub[NWW], con[NWW];
+    uint32_t jid;
+    uint8_t lut[128];
+};
+
+template <class V, int NWW>
+__global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
+    extern __shared__ int32_t s_table[];
+    __shared__ FwdSmem<V, NWW> sm;
+    for (int x = threadIdx.x; x < a.K * a.Kp; x += blockDim.x) s_table[x] = a.table[x];
+    for (int x = threadIdx.x; x < 128; x += blockDim.x) sm.lut[x] = a.lut[x];
+    const int g = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5;
+    const V NEG = neg_inf<V>();
+    const V O4 = (V)a.O4, E4 = (V)a.E4;
+    const char* tbytes = reinterpret_cast<const char*>(s_table);
+    for (;;) {
+        __syncthreads();  // previous job fully done; table/lut loaded
+        if (threadIdx.x == 0) sm.jid = atomicAdd(a.counter, 1u);
+        if (threadIdx.x < NWW) {
+            sm.pub[threadIdx.x] = 0;
+            sm.con[threadIdx.x] = 0;
+        }
+        __syncthreads();
+        const uint32_t jid = sm.jid;
+        if (jid >= a.njobs) break;
+        const NwJob job = a.jobs[jid];
+        const uint32_t n = job.n, m = job.m;
+        const uint8_t* A = a.chars + job.a_off;
+        const uint8_t* B = a.chars + job.b_off;
+        const uint32_t pa = (n + 15) & ~15u;
+        uint8_t* T = a.trace + job.t_off;
+        const uint32_t nbands = (n + BAND - 1) / BAND;
+        for (uint32_t band = w; band < nbands; band += NWW) {
+            const uint32_t i0 = band * BAND + (uint32_t)g * RR + 1;
+            int rowoff[RR];  // byte offset of the score-table row of a[i]
+            V LM[RR], LGB[RR], LGA[RR];
+#pragma unroll
+            for (int r = 0; r < RR; ++r) {
+                const uint32_t i = i0 + r;
+                rowoff[r] = (i <= n ? (int)sm.lut[A[i - 1] & 127] : 0) * a.Kp * 4;
+                LM[r] = (V)(NEG | 2);
+                LGA[r] = NEG;
+                LGB[r] = (V)((a.O4 + (int64_t)i * a.E4) | 1);  // column 0: GB = open + i*extend
+            }
+            // row i0-1 at column 0: the first row's diagonal at column 1
+            // (as the max over its three states: all the M recurrence needs)
+            V pmax = i0 == 1 ? (V)2 /* M[0][0] = 0 */ : (V)((a.O4 + (int64_t)(i0 - 1) * a.E4) | 1);
+            // ring in (from band-1) and out (to band+1); sequence = gen*(m+1)+j
+            const int rin = (int)(band % NWW), rout = (int)((band + 1) % NWW);
+            const uint32_t seq_in = (band / NWW) * (m + 1), seq_out = ((band + 1) / NWW) * (m + 1);
+            const bool has_in = NWW > 1 && band > 0;
+            const bool has_out = NWW > 1 && band + 1 < nbands;
+            V sM = 0, sGB = 0, sGA = 0;
+            const uint32_t steps = m + 31;
+            for (uint32_t s = 0; s < steps; ++s) {
+                const V rM = shfl_up1(sM), rGB = shfl_up1(sGB), rGA = shfl_up1(sGA);
+                if constexpr (NWW > 1) {
+                    // consumer side (lane 0 reads column s+1 this step)
+                    if (has_in && (s % CHUNK) == 0 && s < m) {
+                        if (g == 0) {
+                            const uint32_t need = seq_in + min(s + CHUNK, m);
+                            while (sm.pub[rin] < need) {
+                            }
+                        }
+                        __syncwarp();
+                    }
+                    // producer side (lane 31 writes column s-30 this step)
+                    if (has_out && s >= 31 && ((s - 31) % CHUNK) == 0 && s - 31 < m) {
+                        if (g == 31) {
+                            const uint32_t jj = s - 30;  // first column of the chunk
+                            const uint32_t last = seq_out + min(jj + CHUNK - 1, m);
+                            while (sm.con[rout] + RING < last + 1) {
+                            }
+                        }
+                        __syncwarp();
+                    }
+                }
+                const uint32_t j = s - (uint32_t)g + 1;  // 1..m when active
+                if (j - 1 < m) {
+                    V uM, uGB, uGA;
+                    if (g == 0) {
+                        if (band == 0) {  // row 0 (pairwise.cpp:322-330)
+                            uM = (V)(NEG | 2);
+                            uGB = (V)(NEG | 1);
+                            uGA = (V)(a.O4 + (int64_t)j * a.E4);
+                        } else {
+                            const V* e = sm.ring[rin][(seq_in + j) % RING];
+                            uM = e[0];
+                            uGB = e[1];
+                            uGA = e[2];
+                        }
+                    } else {
+                        uM = rM;
+                        uGB = rGB;
+                        uGA = rGA;
+                    }
+                    // diagonal of row r = old (previous column) values of row r-1,
+                    // pre-reduced to their max before row r-1 is overwritten, so
+                    // every state updates in place (no register rotation)
+                    V dmax = pmax;
+                    pmax = vmax3(uM, uGB, uGA);
+                    const int cb4 = (int)sm.lut[B[j - 1] & 127] * 4;
+                    uint32_t tw[RR / 4];
+                    uint32_t tm[4], tgb[4], tga[4];
+#pragma unroll
+                    for (int r = 0; r < RR; ++r) {
+                        const int32_t sc = *reinterpret_cast<const int32_t*>(tbytes + rowoff[r] + cb4);
+                        const V mraw = dmax + (V)sc;
+                        dmax = vmax3(LM[r], LGB[r], LGA[r]);
+                        const V gbraw = addmax(uGA, O4, addmax(uM, O4, uGB)) + E4;
+                        const V garaw = addmax(LGB[r], O4, addmax(LM[r], O4, LGA[r])) + E4;
+                        tm[r & 3] = (uint32_t)mraw;
+                        tgb[r & 3] = (uint32_t)gbraw;
+                        tga[r & 3] = (uint32_t)garaw;
+                        if ((r & 3) == 3) {  // four rows of codes -> one trace word
+                            const uint32_t wm = gather_lo(tm[0], tm[1], tm[2], tm[3]);
+                            const uint32_t wb = gather_lo(tgb[0], tgb[1], tgb[2], tgb[3]);
+                            const uint32_t wa = gather_lo(tga[0], tga[1], tga[2], tga[3]);
+                            tw[r >> 2] = (wm & 0x03030303u) | ((wb & 0x03030303u) << 2) | ((wa & 0x03030303u) << 4);
+                        }
+                        LM[r] = (mraw & ~(V)3) | 2;
+                        LGB[r] = (gbraw & ~(V)3) | 1;
+                        LGA[r] = garaw & ~(V)3;
+                        uM = LM[r];
+                        uGB = LGB[r];
+                        uGA = LGA[r];
+                    }
+                    sM = uM;
+                    sGB = uGB;
+                    sGA = uGA;
+                    if (i0 <= n)
+                        *reinterpret_cast<uint4*>(T + (uint64_t)(j - 1) * pa + (i0 - 1)) =
+                            make_uint4(tw[0], tw[1], tw[2], tw[3]);
+                    if constexpr (NWW > 1) {
+                        if (has_out && g == 31) {
+                            V* e = sm.ring[rout][(seq_out + j) % RING];
+                            e[0] = uM;
+                            e[1] = uGB;
+                            e[2] = uGA;
+                            if ((j % CHUNK) == 0 || j == m) {
+                                __threadfence_block();
+                                sm.pub[rout] = seq_out + j;
+                            }
+                        }
+                        if (has_in && g == 0 && ((j % CHUNK) == 0 || j == m)) {
+                            __threadfence_block();  // ring reads complete before the slot is released
+                            sm.con[rin] = seq_in + j;
+                        }
+                    }
+                }
+            }
+            // final state at (n, m) (pairwise.cpp:374-375): the lane owning row n
+            if (n >= i0 && n < i0 + RR) {
+                V fM = LM[0], fGB = LGB[0], fGA = LGA[0];
+#pragma unroll
+                for (int r = 1; r < RR; ++r)
+                    if (i0 + r == n) {
+                        fM = LM[r];
+                        fGB = LGB[r];
+                        fGA = LGA[r];
+                    }
+                const V fin = vmax3(fM, fGB, fGA);
+                a.res[job.slot].score = (int64_t)(fin >> 2);
+                a.res[job.slot].final_tag = (uint32_t)(fin & 3);
+            }
+            __syncwarp();
+        }
+    }
+}
+
+}  // namespace nwk
+}  // namespace dm

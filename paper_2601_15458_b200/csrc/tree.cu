@@ -22,6 +22,9 @@
 // (:48-50, :159-163); the partition is stable (:98-109); children are numbered
 // left then right in frontier order (:212-231) by a final BFS renumbering.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <random>
@@ -402,8 +405,18 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
     uint32_t* d_dr = sc.dr.as<uint32_t>(n);
     std::vector<LevItem> items;
 
+    const bool trace = std::getenv("DM_TRACE") != nullptr;
+    auto tnow = [&] {
+        if (trace) DM_CUDA(cudaStreamSynchronize(stream));
+        return std::chrono::steady_clock::now();
+    };
+    auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+        return std::chrono::duration<double, std::milli>(b - a).count();
+    };
+    int level = 0;
     while (!big.empty()) {
         const size_t B = big.size();
+        const auto t0 = tnow();
         // ---- phase 1: median candidates (host seeds) + all-pairs batch
         std::vector<uint64_t> mat_off(B), cand_off(B);
         std::vector<uint32_t> kk(B), cand, nb(B), ne(B);
@@ -434,6 +447,7 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
         }
         uint32_t* d_mat = sc.mat.as<uint32_t>(mtot);
         lev_run_host_items(ctx, s, items, d_mat, &tot, timing);
+        const auto t_med = tnow();
         uint32_t* d_center = sc.res1.as<uint32_t>(B);
         median_argmin_kernel<<<(unsigned)B, 128, 0, stream>>>(
             d_mat, upload(ctx, sc.matoff, mat_off), upload(ctx, sc.kk, kk), upload(ctx, sc.cand, cand),
@@ -501,6 +515,14 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
                 if (m >= 2) (m <= T ? small : next).push_back(cid);
             }
         }
+        if (trace) {
+            const auto t5 = tnow();
+            uint64_t mem = 0;
+            for (size_t v = 0; v < B; ++v) mem += ne[v] - nb[v];
+            std::fprintf(stderr, "[dm tree] level %d big %zu members %llu median %.3f ms sweeps %.3f ms total %.3f ms\n",
+                         level, B, (unsigned long long)mem, ms(t0, t_med), ms(t_med, t5), ms(t0, t5));
+        }
+        ++level;
         big.swap(next);
     }
 
@@ -525,8 +547,13 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
             mtot += (uint64_t)k * k;
             rtot += 2ull * k - 1;
         }
+        const auto s0 = tnow();
         uint32_t* d_mat = sc.sub_mat.as<uint32_t>(mtot);
         lev_run_host_items(ctx, s, items, d_mat, &tot, timing);
+        const auto s1 = tnow();
+        if (trace)
+            std::fprintf(stderr, "[dm tree] small subtrees %zu pairs %zu all-pairs %.3f ms\n", S, items.size(),
+                         ms(s0, s1));
         SubRec* d_recs = sc.sub_recs.as<SubRec>(rtot);
         int* d_err = sc.err.as<int>(1);
         DM_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), stream));
