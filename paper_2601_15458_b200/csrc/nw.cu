@@ -244,7 +244,7 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
             size_t g1 = g0;
             while (g1 < c1 && group_of(sj[g1].n) == grp) ++g1;
             nwk::FwdArgs fa{d_chars, d_jobs + (g0 - c0), (uint32_t)(g1 - g0), d_lut, d_table, sc.K, sc.Kp,
-                            4 * sc.open, 4 * sc.extend, d_trace, out.d_res, d_cnt + gi};
+                            4 * sc.open, 4 * sc.extend, d_trace, out.d_res, d_cnt + gi, 1};
             if (wide) launch_group<int64_t>(ctx, grp, fa, smem);
             else launch_group<int32_t>(ctx, grp, fa, smem);
             DM_CUDA(cudaGetLastError());

@@ -45,6 +45,14 @@ __device__ __forceinline__ V shfl_up1(V v) {
     }
 }
 
+// x + y on the FMA pipe (the forward pass is ALU-bound): `one` is an opaque 1
+__device__ __forceinline__ int32_t add_fma(int32_t x, int32_t y, int32_t one) {
+    int32_t d;
+    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "r"(one), "r"(y));
+    return d;
+}
+__device__ __forceinline__ int64_t add_fma(int64_t x, int64_t y, int32_t) { return x + y; }
+
 // low bytes of four values -> one word (byte k = low byte of value k)
 __device__ __forceinline__ uint32_t gather_lo(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     const uint32_t ab = __byte_perm(a, b, 0x0040);
@@ -63,6 +71,7 @@ struct FwdArgs {
     uint8_t* trace;
     NwRes* res;
     uint32_t* counter;
+    int32_t one;  // == 1 (opaque to ptxas)
 };
 
 template <class V, int NWW>
@@ -176,10 +185,10 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
 #pragma unroll
                     for (int r = 0; r < RR; ++r) {
                         const int32_t sc = *reinterpret_cast<const int32_t*>(tbytes + rowoff[r] + cb4);
-                        const V mraw = dmax + (V)sc;
+                        const V mraw = add_fma(dmax, (V)sc, a.one);
                         dmax = vmax3(LM[r], LGB[r], LGA[r]);
-                        const V gbraw = addmax(uGA, O4, addmax(uM, O4, uGB)) + E4;
-                        const V garaw = addmax(LGB[r], O4, addmax(LM[r], O4, LGA[r])) + E4;
+                        const V gbraw = add_fma(addmax(uGA, O4, addmax(uM, O4, uGB)), E4, a.one);
+                        const V garaw = add_fma(addmax(LGB[r], O4, addmax(LM[r], O4, LGA[r])), E4, a.one);
                         tm[r & 3] = (uint32_t)mraw;
                         tgb[r & 3] = (uint32_t)gbraw;
                         tga[r & 3] = (uint32_t)garaw;
