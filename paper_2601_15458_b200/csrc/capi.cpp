@@ -40,6 +40,12 @@ int dm_ctx_create(int device, dm_ctx** out) {
             throw dm::cuda_error(std::string("libdmb200 is built for sm_100a; device is ") + prop.name);
         }
         c->sm_count = prop.multiProcessorCount;
+        // sequence sets are stream-ordered allocations: keep freed memory in the
+        // pool so repeated create/destroy (one per batch) never returns to the driver
+        cudaMemPool_t pool;
+        DM_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t keep = UINT64_MAX;
+        DM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
         DM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         c->own_stream = c->stream;
         DM_CUDA(cudaEventCreate(&c->ev0));

@@ -19,18 +19,49 @@
 namespace dm {
 namespace {
 
+// Byte census: each thread ORs 16 bytes per uint4 into a private 256-bit
+// mask (4 x u64 in registers), then one warp-reduced atomicOr per word.
 __global__ void census_kernel(const uint8_t* __restrict__ raw, uint64_t nbytes,
-                              unsigned int* __restrict__ present) {
-    __shared__ unsigned int sm[8];
-    if (threadIdx.x < 8) sm[threadIdx.x] = 0;
-    __syncthreads();
+                              unsigned long long* __restrict__ present) {
+    unsigned long long m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+    auto put = [&](uint32_t c) {
+        const unsigned long long bit = 1ull << (c & 63);
+        const uint32_t q = c >> 6;
+        m0 |= q == 0 ? bit : 0ull;
+        m1 |= q == 1 ? bit : 0ull;
+        m2 |= q == 2 ? bit : 0ull;
+        m3 |= q == 3 ? bit : 0ull;
+    };
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nbytes; i += stride) {
-        const unsigned c = raw[i];
-        atomicOr(&sm[c >> 5], 1u << (c & 31));
+    const uint64_t head = (16 - ((uintptr_t)raw & 15)) & 15;
+    const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t0 < head && t0 < nbytes) put(raw[t0]);
+    const uint64_t nvec = nbytes > head ? (nbytes - head) / 16 : 0;
+    const uint4* v = reinterpret_cast<const uint4*>(raw + head);
+    for (uint64_t i = t0; i < nvec; i += stride) {
+        const uint4 x = v[i];
+        const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            put(w[k] & 0xff);
+            put((w[k] >> 8) & 0xff);
+            put((w[k] >> 16) & 0xff);
+            put(w[k] >> 24);
+        }
     }
-    __syncthreads();
-    if (threadIdx.x < 8 && sm[threadIdx.x]) atomicOr(&present[threadIdx.x], sm[threadIdx.x]);
+    for (uint64_t i = head + nvec * 16 + t0; i < nbytes; i += stride) put(raw[i]);
+    for (int o = 16; o > 0; o >>= 1) {
+        m0 |= __shfl_xor_sync(0xffffffffu, m0, o);
+        m1 |= __shfl_xor_sync(0xffffffffu, m1, o);
+        m2 |= __shfl_xor_sync(0xffffffffu, m2, o);
+        m3 |= __shfl_xor_sync(0xffffffffu, m3, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (m0) atomicOr(&present[0], m0);
+        if (m1) atomicOr(&present[1], m1);
+        if (m2) atomicOr(&present[2], m2);
+        if (m3) atomicOr(&present[3], m3);
+    }
 }
 
 // One warp per sequence: recode raw bytes into the 16-B aligned code buffer.
@@ -73,10 +104,18 @@ __global__ void planes_kernel(const uint8_t* __restrict__ codes, const uint64_t*
         uint64_t w[NP];
 #pragma unroll
         for (int k = 0; k < NP; ++k) w[k] = 0;
-        for (int t = 0; t < cnt; ++t) {
-            const unsigned c = p[t];
+        // codes are 16-B aligned per sequence and zero-padded past the end
+        const uint4* pv = reinterpret_cast<const uint4*>(p);
+        for (int q = 0; q < (cnt + 15) / 16; ++q) {
+            const uint4 x = pv[q];
+            const uint32_t ww[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-            for (int k = 0; k < NP; ++k) w[k] |= (uint64_t)((c >> k) & 1u) << t;
+            for (int k4 = 0; k4 < 16; ++k4) {
+                const int t = q * 16 + k4;
+                const unsigned c = t < cnt ? (ww[k4 >> 2] >> ((k4 & 3) * 8)) & 0xffu : 0u;
+#pragma unroll
+                for (int k = 0; k < NP; ++k) w[k] |= (uint64_t)((c >> k) & 1u) << t;
+            }
         }
 #pragma unroll
         for (int k = 0; k < NP; ++k) planes[b * NP + k] = w[k];
@@ -114,8 +153,8 @@ dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets,
 
         uint8_t* d_raw = nullptr;
         uint64_t* d_raw_off = nullptr;
-        DM_CUDA(cudaMalloc(&d_raw, nbytes + 16));
-        DM_CUDA(cudaMalloc(&d_raw_off, (n + 1) * sizeof(uint64_t)));
+        DM_CUDA(cudaMallocAsync(&d_raw, nbytes + 16, st));
+        DM_CUDA(cudaMallocAsync(&d_raw_off, (n + 1) * sizeof(uint64_t), st));
         s->d_raw = d_raw;
         s->d_raw_off = d_raw_off;
         std::vector<uint64_t> rel(n + 1);
@@ -127,8 +166,9 @@ dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets,
         unsigned int* d_present = ctx->aux.as<unsigned int>(8);
         DM_CUDA(cudaMemsetAsync(d_present, 0, 32, st));
         if (nbytes) {
-            const int grid = (int)std::min<uint64_t>((nbytes + 4095) / 4096, (uint64_t)ctx->sm_count * 8);
-            census_kernel<<<std::max(grid, 1), 256, 0, st>>>(d_raw, nbytes, d_present);
+            const int grid = (int)std::min<uint64_t>((nbytes + 4095) / 4096, (uint64_t)ctx->sm_count * 16);
+            census_kernel<<<std::max(grid, 1), 256, 0, st>>>(d_raw, nbytes,
+                                                             reinterpret_cast<unsigned long long*>(d_present));
             DM_CUDA(cudaGetLastError());
         }
         unsigned int present[8];
@@ -145,11 +185,11 @@ dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets,
         s->nsym = nsym;
         s->planes = nsym <= 4 ? 2 : (nsym <= 32 ? 5 : 8);
 
-        DM_CUDA(cudaMalloc(&s->d_codes, o + 16));
-        DM_CUDA(cudaMalloc(&s->d_off, (n + 1) * sizeof(uint64_t)));
-        DM_CUDA(cudaMalloc(&s->d_len, std::max<size_t>(n, 1) * sizeof(uint32_t)));
-        DM_CUDA(cudaMalloc(&s->d_blk, (n + 1) * sizeof(uint64_t)));
-        DM_CUDA(cudaMalloc(&s->d_planes, std::max<uint64_t>(b, 1) * s->planes * sizeof(uint64_t)));
+        DM_CUDA(cudaMallocAsync(&s->d_codes, o + 16, st));
+        DM_CUDA(cudaMallocAsync(&s->d_off, (n + 1) * sizeof(uint64_t), st));
+        DM_CUDA(cudaMallocAsync(&s->d_len, std::max<size_t>(n, 1) * sizeof(uint32_t), st));
+        DM_CUDA(cudaMallocAsync(&s->d_blk, (n + 1) * sizeof(uint64_t), st));
+        DM_CUDA(cudaMallocAsync(&s->d_planes, std::max<uint64_t>(b, 1) * s->planes * sizeof(uint64_t), st));
         DM_CUDA(cudaMemsetAsync(s->d_codes, 0, o + 16, st));
         DM_CUDA(cudaMemcpyAsync(s->d_off, s->off.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st));
         if (n) DM_CUDA(cudaMemcpyAsync(s->d_len, s->len.data(), n * 4, cudaMemcpyHostToDevice, st));
@@ -183,11 +223,11 @@ dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets,
 }  // namespace dm
 
 dm_seqset::~dm_seqset() {
-    if (d_raw) cudaFree(d_raw);
-    if (d_raw_off) cudaFree(d_raw_off);
-    if (d_codes) cudaFree(d_codes);
-    if (d_off) cudaFree(d_off);
-    if (d_len) cudaFree(d_len);
-    if (d_blk) cudaFree(d_blk);
-    if (d_planes) cudaFree(d_planes);
+    if (d_raw) cudaFreeAsync(d_raw, ctx->stream);
+    if (d_raw_off) cudaFreeAsync(d_raw_off, ctx->stream);
+    if (d_codes) cudaFreeAsync(d_codes, ctx->stream);
+    if (d_off) cudaFreeAsync(d_off, ctx->stream);
+    if (d_len) cudaFreeAsync(d_len, ctx->stream);
+    if (d_blk) cudaFreeAsync(d_blk, ctx->stream);
+    if (d_planes) cudaFreeAsync(d_planes, ctx->stream);
 }
