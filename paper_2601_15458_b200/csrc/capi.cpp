@@ -50,6 +50,8 @@ int dm_ctx_create(int device, dm_ctx** out) {
         c->own_stream = c->stream;
         DM_CUDA(cudaEventCreate(&c->ev0));
         DM_CUDA(cudaEventCreate(&c->ev1));
+        dm::lev_warm();
+        dm::nw_warm();
         *out = c;
     });
 }
@@ -59,6 +61,7 @@ int dm_ctx_destroy(dm_ctx* ctx) {
         if (!ctx) return;
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
+        ctx->detach_buffers();  // scratch is freed synchronously once the stream is gone
         cudaEventDestroy(ctx->ev0);
         cudaEventDestroy(ctx->ev1);
         if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);

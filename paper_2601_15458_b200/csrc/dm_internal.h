@@ -31,23 +31,38 @@ struct cuda_error : std::runtime_error {
     } while (0)
 
 // Growable device scratch buffer (never shrinks; reused across calls).
+// Growable device scratch buffer (never shrinks; reused across calls).
+// Stream-ordered on the owning context's stream (*sp) so growth never
+// synchronises the device; the pool keeps freed blocks (dm_ctx_create).
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
+    cudaStream_t* sp = nullptr;
     void* get(size_t bytes) {
         if (bytes > cap) {
-            if (p) cudaFree(p);
+            if (p) {
+                if (sp) cudaFreeAsync(p, *sp);
+                else cudaFree(p);
+            }
             p = nullptr;
             size_t c = bytes + bytes / 4 + 256;
-            DM_CUDA(cudaMalloc(&p, c));
+            if (sp) DM_CUDA(cudaMallocAsync(&p, c, *sp));
+            else DM_CUDA(cudaMalloc(&p, c));
             cap = c;
         }
         return p;
     }
     template <class T>
     T* as(size_t count) { return static_cast<T*>(get(count * sizeof(T))); }
+    DevBuf() = default;
+    explicit DevBuf(cudaStream_t* s) : sp(s) {}
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() {
-        if (p) cudaFree(p);
+        if (p) {
+            if (sp) cudaFreeAsync(p, *sp);
+            else cudaFree(p);
+        }
     }
 };
 
@@ -86,6 +101,15 @@ struct dm_ctx {
     // scratch for the aligner / merge scheduler
     dm::DevBuf nw_in, nw_table, nw_jobs, nw_trace, nw_res, nw_gaps, rows_a, rows_b, colmap, tree_buf;
     uint64_t launches = 0;
+    dm_ctx() { attach(&stream); }
+    void detach_buffers() { attach(nullptr); }
+
+private:
+    void attach(cudaStream_t* s) {
+        for (dm::DevBuf* b : {&items, &out, &counter, &aux, &aux2, &aux3, &nw_in, &nw_table, &nw_jobs, &nw_trace,
+                              &nw_res, &nw_gaps, &rows_a, &rows_b, &colmap, &tree_buf})
+            b->sp = s;
+    }
 };
 
 // Device-resident sequence store.
@@ -153,6 +177,8 @@ dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets,
 void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_cap,
                 std::vector<dm_node>& nodes, std::vector<uint32_t>& order, dm_stats* st);
 double int32_peak(dm_ctx* ctx, int mode);
+void lev_warm();
+void nw_warm();
 dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node>& nodes,
                       const std::vector<uint32_t>& order, const NwScheme& sc, dm_stats* st);
 void insert_gap_columns(dm_ctx* ctx, const char* rows, uint64_t nrows, uint64_t width, const uint32_t* pos,

@@ -273,6 +273,15 @@ void dispatch_w(int w, const LevArgs& a, int sm, cudaStream_t st) {
     }
 }
 
+template <int NP, int W>
+void warm_np() {
+    if constexpr (W <= WMax<NP>::value) {
+        cudaFuncAttributes fa;
+        DM_CUDA(cudaFuncGetAttributes(&fa, lev_kernel<NP, W>));
+        warm_np<NP, W + 1>();
+    }
+}
+
 void launch_bucket(int np, int w, const LevArgs& a, int sm, cudaStream_t st) {
     if (np == 2) dispatch_w<2, 1>(w, a, sm, st);
     else if (np == 5) dispatch_w<5, 1>(w, a, sm, st);
@@ -434,6 +443,14 @@ void run_planned(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const ui
 }
 
 }  // namespace
+
+// Loads every kernel instance up front (lazy module loading would otherwise
+// charge the first batch that hits a new bucket).
+void lev_warm() {
+    warm_np<2, 1>();
+    warm_np<5, 1>();
+    warm_np<8, 1>();
+}
 
 void lev_run_host_items(dm_ctx* ctx, const dm_seqset* s, std::vector<LevItem>& items,
                         uint32_t* d_out, LevTotals* tot, bool time_kernels) {

@@ -102,10 +102,9 @@ __global__ void insert_rows_kernel(const SideDesc* __restrict__ sides, const uin
 void grow_rows(dm_ctx* ctx, DevBuf& buf, uint64_t& pitch, uint32_t n, uint64_t need) {
     if (need <= pitch) return;
     const uint64_t np = ((need + need / 4) + 63) & ~uint64_t(63);
-    DevBuf nb;
+    DevBuf nb(&ctx->stream);
     uint8_t* dst = (uint8_t*)nb.get((uint64_t)n * np);
     DM_CUDA(cudaMemcpy2DAsync(dst, np, buf.p, pitch, pitch, n, cudaMemcpyDeviceToDevice, ctx->stream));
-    DM_CUDA(cudaStreamSynchronize(ctx->stream));
     std::swap(buf.p, nb.p);
     std::swap(buf.cap, nb.cap);
     pitch = np;

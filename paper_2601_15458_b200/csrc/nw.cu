@@ -153,6 +153,17 @@ int group_of(uint32_t n) {
 
 }  // namespace
 
+void nw_warm() {
+    cudaFuncAttributes fa;
+    DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int32_t, 1>));
+    DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int32_t, 4>));
+    DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int32_t, 8>));
+    DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int64_t, 1>));
+    DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int64_t, 4>));
+    DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int64_t, 8>));
+    DM_CUDA(cudaFuncGetAttributes(&fa, nw_traceback_kernel));
+}
+
 NwScheme make_scheme(const int16_t* table, const uint8_t* has_symbol, int open_surcharge, int gap_extend) {
     NwScheme s;
     for (int c = 0; c < 128; ++c) {

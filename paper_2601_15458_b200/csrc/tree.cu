@@ -371,6 +371,11 @@ void download(dm_ctx* ctx, std::vector<T>& v, const T* d, size_t n) {
 struct TreeScratch {
     DevBuf order, tmp, dc, dl, dr, mat, matoff, kk, cand, candoff, nb, ne, res1, res2, res3, sub_begin, sub_k,
         sub_mat, sub_matoff, sub_recoff, sub_recs, err;
+    explicit TreeScratch(cudaStream_t* s) {
+        for (DevBuf* b : {&order, &tmp, &dc, &dl, &dr, &mat, &matoff, &kk, &cand, &candoff, &nb, &ne, &res1, &res2,
+                          &res3, &sub_begin, &sub_k, &sub_mat, &sub_matoff, &sub_recoff, &sub_recs, &err})
+            b->sp = s;
+    }
 };
 
 const char* kDedupMsg = "cluster contains identical sequences; input was not de-duplicated";
@@ -384,7 +389,7 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
     const uint64_t exact_cap = std::max<uint64_t>(2, exact_cap_in);
     const uint32_t T = (uint32_t)std::min<uint64_t>(exact_cap, kSubMax);
     cudaStream_t stream = ctx->stream;
-    TreeScratch sc;
+    TreeScratch sc(&ctx->stream);
     LevTotals tot;
     const bool timing = st != nullptr;
 
