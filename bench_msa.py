@@ -27,9 +27,23 @@ def main():
     ap.add_argument("--scale2", type=float, default=1.0)
     ap.add_argument("--scale4", type=float, default=0.1)
     ap.add_argument("--repeat", type=int, default=2)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--simulate-world", type=int, default=1,
+                    help="run the sharded path with k shards on one GPU (checks, not a speed number)")
     args = ap.parse_args()
     import paper_2601_15458_b200 as dm
-    ctx = dm.default_context(0)
+    from paper_2601_15458_b200 import dist as dmdist
+    rank, world, local = dmdist.env_rank()
+    if world > 1:  # torchrun: one process per GPU, NCCL inside libdmb200
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = dm.Context(local)
+    if world > 1:
+        dmdist.attach_from_torch(ctx)
+    elif args.simulate_world > 1:
+        dmdist.simulate_world(ctx, args.simulate_world)
     golden = {}
     gp = os.path.join(ROOT, "tests", "golden", "msa_configs.json")
     if os.path.exists(gp):
@@ -41,14 +55,22 @@ def main():
         sc = dm.ScoringScheme.protein() if cfg == 3 else dm.ScoringScheme.nucleotide()
         best = None
         for _ in range(args.repeat):
+            if world > 1:
+                tdist.barrier()
             t0 = time.perf_counter()
             ss = dm.SeqSet(seqs, ctx)
             m = dm.msa(ss, sc, seed=42)
             wall = time.perf_counter() - t0
+            if world > 1:  # the job ends when the slowest rank ends
+                t = torch.tensor([wall], dtype=torch.float64, device="cuda")
+                tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+                wall = float(t[0])
             if best is None or wall < best[0]:
                 best = (wall, m)
             del ss
         wall, m = best
+        if rank != 0:
+            continue
         st = m.stats
         key = f"cfg{cfg}@{scale}"
         match = None
@@ -63,8 +85,11 @@ def main():
                 "gcups_e2e": st["cells"] / wall / 1e9, "launches": st["launches"], "nw_calls": st["nw_calls"],
                 "reference_match": match,
                 "reference_cpu_s": (golden[key]["tree_s"] + golden[key]["align_s"]) if key in golden else None,
-                "reference_threads": golden[key]["threads"] if key in golden else None}
+                "reference_threads": golden[key]["threads"] if key in golden else None,
+                "n_gpus": world, "simulated_world": args.simulate_world}
         print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.destroy_process_group()
 
 
 if __name__ == "__main__":

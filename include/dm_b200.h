@@ -70,8 +70,18 @@ int dm_ctx_sync(dm_ctx* ctx);
 int dm_ctx_set_stream(dm_ctx* ctx, void* stream);
 /* INT32 lane-op peak of this device (mode 0 LOP3 (ALU), 1 IMAD (FMA), 2 LOP3+IMAD). */
 int dm_int32_peak(dm_ctx* ctx, int mode, double* lane_ops_per_s);
-/* Multi-GPU: this rank's share of sharded work (rank, world). The shards
- * exchange results with dm_ctx's NCCL communicator when one is attached. */
+/* Multi-GPU (one process per GPU): rank 0 makes an NCCL unique id, the caller
+ * broadcasts its 128 bytes (e.g. torch.distributed), every rank attaches.
+ * Afterwards dm_build_tree / dm_align_all / dm_msa split each distance
+ * batch and each merge level across the ranks (contiguous ranges) and
+ * exchange the results with ncclAllGather / ncclAllReduce; every rank ends
+ * with the full, identical tree and MSA. */
+int dm_nccl_unique_id(uint8_t* id128);
+int dm_ctx_attach_nccl(dm_ctx* ctx, const uint8_t* id128, int rank, int world);
+/* Run the sharded code path with `world` shards on this one GPU (tests). */
+int dm_ctx_simulate_world(dm_ctx* ctx, int world);
+/* Record (rank, world) without a communicator (independent shards, e.g. the
+ * cfg1 pair batches). */
 int dm_ctx_set_shard(dm_ctx* ctx, int rank, int world);
 
 /* ---- sequences -------------------------------------------------------- */

@@ -53,6 +53,9 @@ SIGNATURES = {
     "dm_ctx_sync": (C.c_int, [_P]),
     "dm_ctx_set_stream": (C.c_int, [_P, _P]),
     "dm_int32_peak": (C.c_int, [_P, C.c_int, C.POINTER(C.c_double)]),
+    "dm_nccl_unique_id": (C.c_int, [_u8p]),
+    "dm_ctx_attach_nccl": (C.c_int, [_P, _u8p, C.c_int, C.c_int]),
+    "dm_ctx_simulate_world": (C.c_int, [_P, C.c_int]),
     "dm_ctx_set_shard": (C.c_int, [_P, C.c_int, C.c_int]),
     "dm_seqset_create": (C.c_int, [_P, C.c_char_p, _u64p, C.c_uint32, C.POINTER(_P)]),
     "dm_seqset_destroy": (C.c_int, [_P]),

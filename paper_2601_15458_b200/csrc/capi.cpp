@@ -5,7 +5,10 @@
 #include <cstring>
 #include <string>
 
+#include <algorithm>
+
 #include "capi_guard.h"
+#include "comm.h"
 
 namespace dm {
 std::string& last_error() {
@@ -52,6 +55,7 @@ int dm_ctx_create(int device, dm_ctx** out) {
         DM_CUDA(cudaEventCreate(&c->ev1));
         dm::lev_warm();
         dm::nw_warm();
+        if (const char* sw = std::getenv("DM_SIM_WORLD")) c->sim_world = std::max(1, std::atoi(sw));
         *out = c;
     });
 }
@@ -62,6 +66,7 @@ int dm_ctx_destroy(dm_ctx* ctx) {
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
         ctx->detach_buffers();  // scratch is freed synchronously once the stream is gone
+        dm::comm_destroy(ctx);
         cudaEventDestroy(ctx->ev0);
         cudaEventDestroy(ctx->ev1);
         if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);

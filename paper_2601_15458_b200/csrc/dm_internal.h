@@ -94,9 +94,11 @@ struct dm_ctx {
     cudaStream_t stream = nullptr;      // stream every call is issued on
     cudaStream_t own_stream = nullptr;  // created by dm_ctx_create (null once replaced)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    int rank = 0, world = 1;
+    int rank = 0, world = 1;   // NCCL shard of this context (dm_ctx_attach_nccl)
+    int sim_world = 1;         // >1: run the sharded path on this one GPU (tests)
+    void* nccl = nullptr;      // ncclComm_t
     // scratch for the distance engine
-    dm::DevBuf items, out, counter, aux, aux2, aux3;
+    dm::DevBuf items, out, counter, aux, aux2, aux3, lev_all, lev_items;
     dm::PinnedBuf pin_items, pin_out;
     // scratch for the aligner / merge scheduler
     dm::DevBuf nw_in, nw_table, nw_jobs, nw_trace, nw_res, nw_gaps, rows_a, rows_b, colmap, tree_buf;
@@ -106,7 +108,8 @@ struct dm_ctx {
 
 private:
     void attach(cudaStream_t* s) {
-        for (dm::DevBuf* b : {&items, &out, &counter, &aux, &aux2, &aux3, &nw_in, &nw_table, &nw_jobs, &nw_trace,
+        for (dm::DevBuf* b : {&items, &out, &counter, &aux, &aux2, &aux3, &lev_all, &lev_items, &nw_in, &nw_table,
+                              &nw_jobs, &nw_trace,
                               &nw_res, &nw_gaps, &rows_a, &rows_b, &colmap, &tree_buf})
             b->sp = s;
     }

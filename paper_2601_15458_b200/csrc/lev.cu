@@ -32,6 +32,7 @@
 #include <cstdlib>
 
 #include "dm_internal.h"
+#include "comm.h"
 #include "lev_chains.h"
 
 namespace dm {
@@ -452,13 +453,63 @@ void lev_warm() {
     warm_np<8, 1>();
 }
 
+namespace {
+// all[r * maxc + k] holds job lo_r + k of shard r; route it to its slot.
+__global__ void scatter_shards(const uint32_t* __restrict__ all, const LevItem* __restrict__ items, uint64_t n,
+                               int w, uint64_t maxc, uint32_t* __restrict__ out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        int r = 0;
+        while (r + 1 < w && n * (uint64_t)(r + 1) / (uint64_t)w <= i) ++r;
+        const uint64_t lo = n * (uint64_t)r / (uint64_t)w;
+        out[items[i].slot] = all[(uint64_t)r * maxc + (i - lo)];
+    }
+}
+}  // namespace
+
 void lev_run_host_items(dm_ctx* ctx, const dm_seqset* s, std::vector<LevItem>& items,
                         uint32_t* d_out, LevTotals* tot, bool time_kernels) {
     if (items.empty()) return;
-    LevItem* d_items = ctx->aux3.as<LevItem>(items.size());
-    DM_CUDA(cudaMemcpyAsync(d_items, items.data(), items.size() * sizeof(LevItem),
-                            cudaMemcpyHostToDevice, ctx->stream));
-    run_planned(ctx, s, nullptr, nullptr, d_items, items.size(), d_out, tot, time_kernels);
+    const uint64_t n = items.size();
+    const int w = shard_world(ctx);
+    if (w == 1) {
+        LevItem* d_items = ctx->aux3.as<LevItem>(n);
+        DM_CUDA(cudaMemcpyAsync(d_items, items.data(), n * sizeof(LevItem), cudaMemcpyHostToDevice, ctx->stream));
+        run_planned(ctx, s, nullptr, nullptr, d_items, n, d_out, tot, time_kernels);
+        return;
+    }
+    // Sharded batch: each rank computes a contiguous range of jobs into its
+    // row of `all`, the rows are all-gathered, and every rank scatters the
+    // full result to the slots (decisions stay replicated).
+    uint64_t maxc = 0;
+    for (int r = 0; r < w; ++r) {
+        uint64_t lo, hi;
+        shard_range(n, r, w, &lo, &hi);
+        maxc = std::max(maxc, hi - lo);
+    }
+    uint32_t* d_all = ctx->lev_all.as<uint32_t>((uint64_t)w * maxc + 1);
+    LevItem* d_global = ctx->lev_items.as<LevItem>(n);
+    DM_CUDA(cudaMemcpyAsync(d_global, items.data(), n * sizeof(LevItem), cudaMemcpyHostToDevice, ctx->stream));
+    const bool real = ctx->world > 1;
+    std::vector<LevItem> sub;
+    for (int r = 0; r < w; ++r) {
+        if (real && r != ctx->rank) continue;
+        uint64_t lo, hi;
+        shard_range(n, r, w, &lo, &hi);
+        if (hi == lo) continue;
+        sub.assign(items.begin() + lo, items.begin() + hi);
+        for (uint64_t k = 0; k < sub.size(); ++k) sub[k].slot = (uint32_t)k;
+        LevItem* d_items = ctx->aux3.as<LevItem>(sub.size());
+        DM_CUDA(cudaMemcpyAsync(d_items, sub.data(), sub.size() * sizeof(LevItem), cudaMemcpyHostToDevice,
+                                ctx->stream));
+        run_planned(ctx, s, nullptr, nullptr, d_items, sub.size(), d_all + (uint64_t)r * maxc, tot, time_kernels);
+        if (!real) DM_CUDA(cudaStreamSynchronize(ctx->stream));  // host `sub` reused
+    }
+    if (real) comm_allgather(ctx, d_all + (uint64_t)ctx->rank * maxc, d_all, maxc * sizeof(uint32_t));
+    const int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)ctx->sm_count * 8);
+    scatter_shards<<<std::max(grid, 1), 256, 0, ctx->stream>>>(d_all, d_global, n, w, maxc, d_out);
+    DM_CUDA(cudaGetLastError());
+    ctx->launches += 1;
 }
 
 void lev_run_device_pairs(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia,

@@ -203,7 +203,7 @@ dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node
             }
             NwOut no;
             const auto h0 = std::chrono::steady_clock::now();
-            nw_run(ctx, (const uint8_t*)rowsbuf.p, jobs, sc, no, st != nullptr || trace);
+            nw_run_sharded(ctx, (const uint8_t*)rowsbuf.p, jobs, sc, no, st != nullptr || trace);
             fwd_ms += no.fwd_ms;
             tb_ms += no.tb_ms;
             cells += no.cells;

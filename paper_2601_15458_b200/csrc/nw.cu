@@ -33,6 +33,7 @@
 #include "dm_internal.h"
 #include "nw.h"
 #include "nw_fwd.cuh"
+#include "comm.h"
 
 namespace dm {
 namespace {
@@ -187,29 +188,42 @@ NwScheme make_scheme(const int16_t* table, const uint8_t* has_symbol, int open_s
     return s;
 }
 
-void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const NwScheme& sc, NwOut& out,
-            bool time_kernels) {
-    out.fwd_ms = out.tb_ms = 0.f;
-    out.cells = 0;
-    out.launches = 0;
-    const size_t nj = jobs.size();
-    // outputs: results + gap lists
-    uint64_t gtot = 0, ttot = 0;
-    uint32_t mmax = 0, nmmax = 0;
-    for (auto& jb : jobs) {
+namespace {
+// Result slots and gap-list offsets of a batch (one layout for all shards).
+uint64_t assign_layout(std::vector<NwJob>& jobs) {
+    uint64_t gtot = 0;
+    for (size_t k = 0; k < jobs.size(); ++k) {
+        NwJob& jb = jobs[k];
         if (jb.n == 0 || jb.m == 0) throw invalid_argument("nw_align requires non-empty inputs");
+        jb.slot = (uint32_t)k;
         jb.ga_off = gtot;
         gtot += jb.m;
         jb.gb_off = gtot;
         gtot += jb.n;
-        mmax = std::max(mmax, jb.m);
+    }
+    return gtot;
+}
+}  // namespace
+
+void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const NwScheme& sc, NwOut& out,
+            bool time_kernels, bool layout_given) {
+    out.fwd_ms = out.tb_ms = 0.f;
+    out.cells = 0;
+    out.launches = 0;
+    const size_t nj = jobs.size();
+    if (!layout_given) {
+        const uint64_t gtot = assign_layout(jobs);
+        out.d_res = ctx->nw_res.as<NwRes>(std::max<size_t>(nj, 1));
+        out.d_gaps = ctx->nw_gaps.as<uint32_t>(std::max<uint64_t>(gtot, 1));
+        out.gaps_total = gtot;
+    }
+    uint64_t ttot = 0;
+    uint32_t nmmax = 0;
+    for (const auto& jb : jobs) {
         nmmax = std::max(nmmax, jb.n + jb.m);
         out.cells += (uint64_t)jb.n * jb.m;
         ttot += (uint64_t)jb.m * ((jb.n + 15) & ~15u);
     }
-    out.d_res = ctx->nw_res.as<NwRes>(std::max<size_t>(nj, 1));
-    out.d_gaps = ctx->nw_gaps.as<uint32_t>(std::max<uint64_t>(gtot, 1));
-    out.gaps_total = gtot;
     if (nj == 0) return;
     const int64_t bound = ((int64_t)nmmax + 2) * (sc.maxabs + std::llabs(sc.open) + std::llabs(sc.extend)) * 4;
     const bool wide = bound >= (1ll << 28);
@@ -223,7 +237,6 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
     // Larger alignments first (better tail balance), grouped by warps per
     // alignment; chunked by a trace-memory budget.
     std::vector<NwJob> sj(jobs);
-    for (size_t k = 0; k < nj; ++k) sj[k].slot = (uint32_t)k;
     std::stable_sort(sj.begin(), sj.end(), [](const NwJob& x, const NwJob& y) {
         const int gx = group_of(x.n), gy = group_of(y.n);
         if (gx != gy) return gx > gy;
@@ -287,6 +300,45 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
         ctx->launches += 1;
         if (c1 < nj) DM_CUDA(cudaStreamSynchronize(ctx->stream));  // trace buffer reused by the next chunk
         c0 = c1;
+    }
+}
+
+void nw_run_sharded(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const NwScheme& sc,
+                    NwOut& out, bool time_kernels) {
+    const int w = shard_world(ctx);
+    if (w == 1 || jobs.size() < 2) {
+        nw_run(ctx, d_chars, jobs, sc, out, time_kernels);
+        return;
+    }
+    const size_t nj = jobs.size();
+    const uint64_t gtot = assign_layout(jobs);
+    out = NwOut{};
+    out.d_res = ctx->nw_res.as<NwRes>(nj);
+    out.d_gaps = ctx->nw_gaps.as<uint32_t>(std::max<uint64_t>(gtot, 1));
+    out.gaps_total = gtot;
+    DM_CUDA(cudaMemsetAsync(out.d_res, 0, nj * sizeof(NwRes), ctx->stream));
+    DM_CUDA(cudaMemsetAsync(out.d_gaps, 0, std::max<uint64_t>(gtot, 1) * 4, ctx->stream));
+    const bool real = ctx->world > 1;
+    for (int r = 0; r < w; ++r) {
+        if (real && r != ctx->rank) continue;
+        uint64_t lo, hi;
+        shard_range(nj, r, w, &lo, &hi);
+        if (hi == lo) continue;
+        std::vector<NwJob> sub(jobs.begin() + lo, jobs.begin() + hi);
+        NwOut part;
+        part.d_res = out.d_res;
+        part.d_gaps = out.d_gaps;
+        part.gaps_total = gtot;
+        nw_run(ctx, d_chars, sub, sc, part, time_kernels, /*layout_given=*/true);
+        out.fwd_ms += part.fwd_ms;
+        out.tb_ms += part.tb_ms;
+        out.cells += part.cells;
+        out.launches += part.launches;
+    }
+    if (real) {
+        static_assert(sizeof(NwRes) % 8 == 0, "NwRes is reduced as int64 words");
+        comm_allreduce_sum_i64(ctx, out.d_res, nj * sizeof(NwRes) / 8);
+        comm_allreduce_sum_u32(ctx, out.d_gaps, gtot);
     }
 }
 

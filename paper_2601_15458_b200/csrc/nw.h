@@ -51,7 +51,14 @@ struct NwOut {
 
 // Runs forward + traceback over `jobs` (host array; t_off/ga_off/gb_off are
 // assigned here). `d_chars` is device memory holding every a and b.
+// layout_given: slots / gap offsets are already set and out.d_res / d_gaps
+// point at the (shared) result buffers — used by nw_run_sharded.
 void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const NwScheme& sc,
-            NwOut& out, bool time_kernels);
+            NwOut& out, bool time_kernels, bool layout_given = false);
+// Same results, with the jobs split across the context's shards (NCCL ranks
+// or the simulated world): each rank aligns its range into zeroed shared
+// buffers, which are then all-reduced (sum) so every rank holds all results.
+void nw_run_sharded(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const NwScheme& sc,
+                    NwOut& out, bool time_kernels);
 
 }  // namespace dm
