@@ -102,6 +102,12 @@ int dm_lev_pairs(dm_ctx* ctx, const dm_seqset* s, const uint32_t* ia, const uint
 /* Same with DEVICE arrays (ia, ib, out resident in HBM); no host copies. */
 int dm_lev_pairs_device(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia,
                         const uint32_t* d_ib, uint64_t n, uint32_t* d_out, dm_stats* st);
+/* End-to-end batch from HOST memory: pair i = (sequence 2i, sequence 2i+1)
+ * of `data` / `offsets` (2*npairs+1 entries). Uploads and computes in
+ * overlapped chunks (copy stream + compute stream); pinned `data` lets the
+ * transfer run fully asynchronously. out: host uint32[npairs]. */
+int dm_lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint64_t npairs,
+                        uint32_t* out, dm_stats* st);
 /* distance_scan: out[i] = levenshtein(seq from, seq members[i]). */
 int dm_lev_one_to_many(dm_ctx* ctx, const dm_seqset* s, uint32_t from, const uint32_t* members,
                        uint64_t n, uint32_t* out, dm_stats* st);

@@ -142,6 +142,21 @@ def lev_pairs(seqset: SeqSet, ia, ib, stats: bool = False):
     return (out, s.as_dict()) if stats else out
 
 
+def lev_pairs_packed(data, offsets, ctx: Context | None = None, stats: bool = False):
+    """End-to-end batch from host memory: pair i = (sequence 2i, 2i+1) of
+    (data, offsets); transfers overlap the kernels (dm_lev_pairs_packed).
+    `data` may be bytes or an object exposing a host pointer (e.g. a pinned
+    torch uint8 tensor, via .data_ptr())."""
+    ctx = ctx or default_context()
+    offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+    npairs = (len(offsets) - 1) // 2
+    out = np.empty(npairs, dtype=np.uint32)
+    ptr = C.c_void_p(data.data_ptr()) if hasattr(data, "data_ptr") else C.cast(C.c_char_p(data), C.c_void_p)
+    s = dm_stats()
+    check(lib().dm_lev_pairs_packed(ctx.handle, ptr, _ptr(offsets, C.c_uint64), npairs, _ptr(out), C.byref(s)))
+    return (out, s.as_dict()) if stats else out
+
+
 def lev_one_to_many(seqset: SeqSet, origin: int, members, stats: bool = False):
     """distance_scan (cluster_tree.cpp:31-41): distances from `origin` to each member."""
     members = _u32(members)

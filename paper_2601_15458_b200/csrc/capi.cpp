@@ -65,11 +65,30 @@ int dm_ctx_destroy(dm_ctx* ctx) {
         if (!ctx) return;
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
+        for (dm_ctx*& p : ctx->prep) {  // planner contexts of the streamed path
+            if (!p) continue;
+            cudaStreamSynchronize(p->stream);
+            p->detach_buffers();
+            cudaEventDestroy(p->ev0);
+            cudaEventDestroy(p->ev1);
+            cudaStreamDestroy(p->own_stream);
+            delete p;
+            p = nullptr;
+        }
+        for (int k = 0; k < dm_ctx::kLevSide; ++k) {
+            if (ctx->lev_side[k]) {
+                cudaStreamSynchronize(ctx->lev_side[k]);
+                cudaStreamDestroy(ctx->lev_side[k]);
+            }
+            if (ctx->lev_join[k]) cudaEventDestroy(ctx->lev_join[k]);
+        }
+        if (ctx->lev_fork) cudaEventDestroy(ctx->lev_fork);
         ctx->detach_buffers();  // scratch is freed synchronously once the stream is gone
         dm::comm_destroy(ctx);
         cudaEventDestroy(ctx->ev0);
         cudaEventDestroy(ctx->ev1);
         if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+        if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
         delete ctx;
     });
 }

@@ -99,6 +99,12 @@ struct dm_ctx {
     void* nccl = nullptr;      // ncclComm_t
     // scratch for the distance engine
     dm::DevBuf items, out, counter, aux, aux2, aux3, lev_all, lev_items;
+    cudaStream_t copy_stream = nullptr;  // host->device staging of streamed batches
+    dm::DevBuf stage0, stage1, stage2, stream_pairs, stream_out, stream_offs;
+    dm_ctx* prep[3] = {};  // planner contexts of the streamed path (own stream + scratch)
+    static constexpr int kLevSide = 4;  // side streams the distance buckets fan out on
+    cudaStream_t lev_side[kLevSide] = {};
+    cudaEvent_t lev_fork = nullptr, lev_join[kLevSide] = {};
     dm::PinnedBuf pin_items, pin_out;
     // scratch for the aligner / merge scheduler
     dm::DevBuf nw_in, nw_table, nw_jobs, nw_trace, nw_res, nw_gaps, rows_a, rows_b, colmap, tree_buf;
@@ -108,7 +114,8 @@ struct dm_ctx {
 
 private:
     void attach(cudaStream_t* s) {
-        for (dm::DevBuf* b : {&items, &out, &counter, &aux, &aux2, &aux3, &lev_all, &lev_items, &nw_in, &nw_table,
+        for (dm::DevBuf* b : {&items, &out, &counter, &aux, &aux2, &aux3, &lev_all, &lev_items, &stage0, &stage1, &stage2,
+                              &stream_pairs, &stream_out, &stream_offs, &nw_in, &nw_table,
                               &nw_jobs, &nw_trace,
                               &nw_res, &nw_gaps, &rows_a, &rows_b, &colmap, &tree_buf})
             b->sp = s;
@@ -130,6 +137,7 @@ struct dm_seqset {
     std::vector<uint64_t> raw_off; // offset of sequence i in d_raw (as given by the caller)
     // device
     uint8_t* d_raw = nullptr;      // raw residue bytes (what NW scores and the MSA prints)
+    bool owns_raw = true;
     uint64_t* d_raw_off = nullptr;
     uint8_t* d_codes = nullptr;    // dense codes 0..nsym-1, 16-B aligned per sequence
     uint64_t* d_off = nullptr;
@@ -169,12 +177,29 @@ struct LevTotals {
 // by the planner). d_out is indexed by item.slot.
 void lev_run_host_items(dm_ctx* ctx, const dm_seqset* s, std::vector<LevItem>& items,
                         uint32_t* d_out, LevTotals* tot, bool time_kernels);
+// Pairs (2i, 2i+1) of a packed HOST buffer, streamed in chunks (stream.cu).
+void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint64_t npairs, uint32_t* out,
+                      LevTotals* tot, bool timing);
+// Streamed path: plan on `prep` (its stream and scratch; host-synchronous),
+// then launch the distance kernels on ctx->stream after `planned`.
+void lev_plan_then_launch(dm_ctx* prep, dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia,
+                          const uint32_t* d_ib, uint64_t n, uint32_t* d_out, cudaEvent_t planned,
+                          LevTotals* tot);
 // Pairs given as device arrays (bench path): builds items on the device.
 void lev_run_device_pairs(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia,
                           const uint32_t* d_ib, uint64_t n, uint32_t* d_out, LevTotals* tot,
                           bool time_kernels);
 
-dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint32_t n);
+// d_raw_given: the residues already sit on the device at that address
+// (offsets relative to it after subtracting offsets[0]); not owned.
+dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint32_t n,
+                         const uint8_t* d_raw_given = nullptr);
+// Sequence set over residues already on the device (d_raw) whose offsets are
+// d_offs[first..first+n] (device, absolute) / h_offs[0..n] (host, same values):
+// no host->device copies, so it never queues behind a bulk upload.
+// Host mirrors (len/off/blk_off/raw_off) are left empty.
+dm_seqset* seqset_create_device(dm_ctx* ctx, const uint8_t* d_raw, const uint64_t* d_offs,
+                                const uint64_t* h_offs, uint32_t n);
 
 // Guide tree (tree.cu / tree_host.cpp).
 void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_cap,

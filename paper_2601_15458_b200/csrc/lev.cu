@@ -290,6 +290,7 @@ void launch_bucket(int np, int w, const LevArgs& a, int sm, cudaStream_t st) {
 }
 
 constexpr int kBuckets = 6 * 32;  // (log2 G) * 32 + W
+constexpr int kLevSide = dm_ctx::kLevSide;
 
 // Orient each job (shorter string = pattern), pick (G, R) and build the
 // radix key (bucket << 32 | ~n) so one sort groups buckets and balances warps.
@@ -353,10 +354,18 @@ __global__ void gather_items(const LevItem* __restrict__ in, const uint32_t* __r
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = in[idx[i]];
 }
 
-void run_planned(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const uint32_t* d_ib,
-                 const LevItem* d_in_items, uint64_t n, uint32_t* d_out, LevTotals* tot,
-                 bool time_kernels) {
-    if (n == 0) return;
+// A planned batch: bucket-sorted items plus the host copy of the histogram.
+struct LevPlan {
+    LevItem* items = nullptr;
+    uint32_t* counters = nullptr;
+    unsigned int h[kBuckets];
+    unsigned long long hc[2];
+};
+
+// Planner phase on `ctx`'s stream (scratch from ctx): orient, bucket, sort,
+// read the histogram back (the one host sync of a batch).
+void plan_batch(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const uint32_t* d_ib,
+                const LevItem* d_in_items, uint64_t n, LevPlan& P) {
     if (n > 0xffffffffull) throw invalid_argument("too many distance jobs in one batch");
     cudaStream_t st = ctx->stream;
     const int np = s->planes;
@@ -398,22 +407,49 @@ void run_planned(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const ui
     DM_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_b, k0, k1, i0, i1, (int)n, 0, 40, st));
     gather_items<<<grid, 256, 0, st>>>(it0, i1, n, it1);
     DM_CUDA(cudaGetLastError());
-    unsigned int h[kBuckets];
-    unsigned long long hc[2];
-    DM_CUDA(cudaMemcpyAsync(h, hist, sizeof(h), cudaMemcpyDeviceToHost, st));
-    DM_CUDA(cudaMemcpyAsync(hc, cells, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    DM_CUDA(cudaMemcpyAsync(P.h, hist, sizeof(P.h), cudaMemcpyDeviceToHost, st));
+    DM_CUDA(cudaMemcpyAsync(P.hc, cells, sizeof(P.hc), cudaMemcpyDeviceToHost, st));
     DM_CUDA(cudaStreamSynchronize(st));
-    if (h[kBuckets - 1])
+    if (P.h[kBuckets - 1])
         throw invalid_argument("sequence too long for the distance engine (max " +
                                std::to_string(32 * wmax * 32) + " residues for this alphabet)");
-    if (time_kernels) DM_CUDA(cudaEventRecord(ctx->ev0, st));
+    P.items = it1;
+    P.counters = counters;
+    ctx->launches += 2;
+}
+
+// Kernel phase: one persistent launch per non-empty bucket. A bucket's launch
+// drains with a tail (its last warp tasks run while SMs empty out), so the
+// buckets go out on kLevSide side streams forked from `st`, largest words per
+// lane first: the next bucket's blocks take the SMs the previous one frees.
+int launch_plan(dm_ctx* ctx, const LevPlan& P, const dm_seqset* s, uint32_t* d_out, cudaStream_t st) {
+    uint64_t starts[kBuckets];
+    int order[kBuckets], nb = 0;
     uint64_t start = 0;
-    int launches = 0;
     for (int b = 0; b < kBuckets; ++b) {
-        if (!h[b]) continue;
+        starts[b] = start;
+        start += P.h[b];
+        if (P.h[b]) order[nb++] = b;
+    }
+    // largest per-task work first: lanes per pair x words per lane
+    std::stable_sort(order, order + nb, [](int x, int y) { return ((x % 32) << (x / 32)) > ((y % 32) << (y / 32)); });
+    const bool fork = nb > 1;
+    if (fork) {
+        if (!ctx->lev_fork) {
+            DM_CUDA(cudaEventCreateWithFlags(&ctx->lev_fork, cudaEventDisableTiming));
+            for (int k = 0; k < kLevSide; ++k) {
+                DM_CUDA(cudaStreamCreateWithFlags(&ctx->lev_side[k], cudaStreamNonBlocking));
+                DM_CUDA(cudaEventCreateWithFlags(&ctx->lev_join[k], cudaEventDisableTiming));
+            }
+        }
+        DM_CUDA(cudaEventRecord(ctx->lev_fork, st));
+        for (int k = 0; k < std::min(nb, kLevSide); ++k) DM_CUDA(cudaStreamWaitEvent(ctx->lev_side[k], ctx->lev_fork, 0));
+    }
+    for (int i = 0; i < nb; ++i) {
+        const int b = order[i];
         LevArgs a;
-        a.items = it1 + start;
-        a.nitems = h[b];
+        a.items = P.items + starts[b];
+        a.nitems = P.h[b];
         a.lgG = b / 32;
         a.codes = s->d_codes;
         a.off = s->d_off;
@@ -421,18 +457,33 @@ void run_planned(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const ui
         a.blk = s->d_blk;
         a.planes = s->d_planes;
         a.out = d_out;
-        a.counter = counters + b;
+        a.counter = P.counters + b;
         a.one = 1u;
-        launch_bucket(np, b % 32, a, ctx->sm_count, st);
+        launch_bucket(s->planes, b % 32, a, ctx->sm_count, fork ? ctx->lev_side[i % kLevSide] : st);
         DM_CUDA(cudaGetLastError());
-        start += h[b];
-        ++launches;
     }
+    if (fork)
+        for (int k = 0; k < std::min(nb, kLevSide); ++k) {
+            DM_CUDA(cudaEventRecord(ctx->lev_join[k], ctx->lev_side[k]));
+            DM_CUDA(cudaStreamWaitEvent(st, ctx->lev_join[k], 0));
+        }
+    return nb;
+}
+
+void run_planned(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const uint32_t* d_ib,
+                 const LevItem* d_in_items, uint64_t n, uint32_t* d_out, LevTotals* tot,
+                 bool time_kernels) {
+    if (n == 0) return;
+    LevPlan P;
+    plan_batch(ctx, s, d_ia, d_ib, d_in_items, n, P);
+    cudaStream_t st = ctx->stream;
+    if (time_kernels) DM_CUDA(cudaEventRecord(ctx->ev0, st));
+    const int launches = launch_plan(ctx, P, s, d_out, st);
     if (time_kernels) DM_CUDA(cudaEventRecord(ctx->ev1, st));
-    ctx->launches += launches + 2;
+    ctx->launches += launches;
     if (tot) {
-        tot->cells += hc[0];
-        tot->cells_exec += hc[1];
+        tot->cells += P.hc[0];
+        tot->cells_exec += P.hc[1];
         tot->launches += launches + 2;
         if (time_kernels) {
             DM_CUDA(cudaEventSynchronize(ctx->ev1));
@@ -516,6 +567,23 @@ void lev_run_device_pairs(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia,
                           const uint32_t* d_ib, uint64_t n, uint32_t* d_out, LevTotals* tot,
                           bool time_kernels) {
     run_planned(ctx, s, d_ia, d_ib, nullptr, n, d_out, tot, time_kernels);
+}
+
+void lev_plan_then_launch(dm_ctx* prep, dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia,
+                          const uint32_t* d_ib, uint64_t n, uint32_t* d_out, cudaEvent_t planned,
+                          LevTotals* tot) {
+    if (n == 0) return;
+    LevPlan P;
+    plan_batch(prep, s, d_ia, d_ib, nullptr, n, P);
+    DM_CUDA(cudaEventRecord(planned, prep->stream));
+    DM_CUDA(cudaStreamWaitEvent(ctx->stream, planned, 0));
+    const int launches = launch_plan(ctx, P, s, d_out, ctx->stream);
+    ctx->launches += launches;
+    if (tot) {
+        tot->cells += P.hc[0];
+        tot->cells_exec += P.hc[1];
+        tot->launches += launches + 2;
+    }
 }
 
 }  // namespace dm

@@ -14,6 +14,8 @@
 #include <algorithm>
 #include <cstring>
 
+#include <cub/cub.cuh>
+
 #include "dm_internal.h"
 
 namespace dm {
@@ -122,9 +124,124 @@ __global__ void planes_kernel(const uint8_t* __restrict__ codes, const uint64_t*
     }
 }
 
+// Per-sequence metadata from absolute device offsets (streamed batches):
+// relative raw offsets, lengths and the padded sizes the two scans turn into
+// code offsets (16-B aligned, >= 1 pad byte) and first plane block.
+__global__ void meta_kernel(const uint64_t* __restrict__ offs, uint32_t n, uint64_t* __restrict__ raw_off,
+                            uint32_t* __restrict__ len, uint64_t* __restrict__ code_sz,
+                            uint64_t* __restrict__ blk_sz) {
+    const uint64_t base = offs[0];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x) {
+        raw_off[i] = offs[i] - base;
+        if (i < n) {
+            const uint64_t L = offs[i + 1] - offs[i];
+            len[i] = (uint32_t)L;
+            code_sz[i] = (L + 16) & ~uint64_t(15);
+            blk_sz[i] = (L + 63) / 64;
+        } else {
+            code_sz[i] = 0;
+            blk_sz[i] = 0;
+        }
+    }
+}
+
+// Dense code map from the census mask: code(c) = #present bytes below c.
+__global__ void lut_kernel(const unsigned int* __restrict__ present, uint8_t* __restrict__ lut) {
+    const int c = threadIdx.x;
+    int below = 0;
+    for (int w = 0; w < (c >> 5); ++w) below += __popc(present[w]);
+    below += __popc(present[c >> 5] & ((1u << (c & 31)) - 1u));
+    lut[c] = (present[c >> 5] >> (c & 31)) & 1u ? (uint8_t)below : 0;
+}
+
 }  // namespace
 
-dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint32_t n) {
+dm_seqset* seqset_create_device(dm_ctx* ctx, const uint8_t* d_raw, const uint64_t* d_offs,
+                                const uint64_t* h_offs, uint32_t n) {
+    auto* s = new dm_seqset;
+    s->ctx = ctx;
+    s->n = n;
+    s->owns_raw = false;
+    s->d_raw = const_cast<uint8_t*>(d_raw);
+    try {
+        uint64_t o = 0, b = 0;
+        for (uint32_t i = 0; i < n; ++i) {
+            const uint64_t L = h_offs[i + 1] - h_offs[i];
+            if (L > 0xffffffffull) throw invalid_argument("sequence longer than 2^32-1 residues");
+            o += (L + 16) & ~uint64_t(15);
+            b += (L + 63) / 64;
+        }
+        s->total_blocks = b;
+        const uint64_t nbytes = h_offs[n] - h_offs[0];
+        cudaStream_t st = ctx->stream;
+        DM_CUDA(cudaMallocAsync(&s->d_raw_off, (n + 1) * sizeof(uint64_t), st));
+        DM_CUDA(cudaMallocAsync(&s->d_off, (n + 1) * sizeof(uint64_t), st));
+        DM_CUDA(cudaMallocAsync(&s->d_len, std::max<size_t>(n, 1) * sizeof(uint32_t), st));
+        DM_CUDA(cudaMallocAsync(&s->d_blk, (n + 1) * sizeof(uint64_t), st));
+        size_t cub_b = 0;
+        DM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, cub_b, (uint64_t*)nullptr, (uint64_t*)nullptr, (int)n + 1, st));
+        const size_t sz_b = ((size_t)(n + 1) * 8 + 255) & ~size_t(255);
+        char* scratch = (char*)ctx->aux3.get(2 * sz_b + cub_b + 256);
+        uint64_t* code_sz = (uint64_t*)scratch;
+        uint64_t* blk_sz = (uint64_t*)(scratch + sz_b);
+        void* cub_tmp = scratch + 2 * sz_b;
+        const int mgrid = (int)std::min<uint64_t>((n + 256) / 256, (uint64_t)ctx->sm_count * 8);
+        meta_kernel<<<std::max(mgrid, 1), 256, 0, st>>>(d_offs, n, s->d_raw_off, s->d_len, code_sz, blk_sz);
+        DM_CUDA(cudaGetLastError());
+        DM_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_b, code_sz, s->d_off, (int)n + 1, st));
+        DM_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_b, blk_sz, s->d_blk, (int)n + 1, st));
+
+        unsigned int* d_present = ctx->aux.as<unsigned int>(8);
+        DM_CUDA(cudaMemsetAsync(d_present, 0, 32, st));
+        if (nbytes) {
+            const int grid = (int)std::min<uint64_t>((nbytes + 4095) / 4096, (uint64_t)ctx->sm_count * 16);
+            census_kernel<<<std::max(grid, 1), 256, 0, st>>>(d_raw, nbytes,
+                                                             reinterpret_cast<unsigned long long*>(d_present));
+            DM_CUDA(cudaGetLastError());
+        }
+        uint8_t* d_lut = (uint8_t*)ctx->aux2.get(256);
+        lut_kernel<<<1, 256, 0, st>>>(d_present, d_lut);
+        DM_CUDA(cudaGetLastError());
+        unsigned int present[8];
+        DM_CUDA(cudaMemcpyAsync(present, d_present, 32, cudaMemcpyDeviceToHost, st));
+        DM_CUDA(cudaStreamSynchronize(st));
+        int nsym = 0;
+        for (int c = 0; c < 256; ++c)
+            if (present[c >> 5] & (1u << (c & 31))) {
+                s->code_of[c] = (uint8_t)nsym++;
+                s->present[c] = true;
+            }
+        s->nsym = nsym;
+        s->planes = nsym <= 4 ? 2 : (nsym <= 32 ? 5 : 8);
+
+        DM_CUDA(cudaMallocAsync(&s->d_codes, o + 16, st));
+        DM_CUDA(cudaMallocAsync(&s->d_planes, std::max<uint64_t>(b, 1) * s->planes * sizeof(uint64_t), st));
+        DM_CUDA(cudaMemsetAsync(s->d_codes, 0, o + 16, st));
+        if (n) {
+            const int grid = (int)std::min<uint64_t>((n + 7) / 8, (uint64_t)ctx->sm_count * 16);
+            recode_kernel<<<grid, 256, 0, st>>>(d_raw, s->d_raw_off, s->d_off, n, d_lut, s->d_codes);
+            DM_CUDA(cudaGetLastError());
+        }
+        if (b) {
+            const int grid = (int)std::min<uint64_t>((b + 255) / 256, (uint64_t)ctx->sm_count * 16);
+            if (s->planes == 2)
+                planes_kernel<2><<<grid, 256, 0, st>>>(s->d_codes, s->d_off, s->d_len, s->d_blk, n, s->d_planes);
+            else if (s->planes == 5)
+                planes_kernel<5><<<grid, 256, 0, st>>>(s->d_codes, s->d_off, s->d_len, s->d_blk, n, s->d_planes);
+            else
+                planes_kernel<8><<<grid, 256, 0, st>>>(s->d_codes, s->d_off, s->d_len, s->d_blk, n, s->d_planes);
+            DM_CUDA(cudaGetLastError());
+        }
+        ctx->launches += 7;
+    } catch (...) {
+        delete s;
+        throw;
+    }
+    return s;
+}
+
+dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint32_t n,
+                         const uint8_t* d_raw_given) {
     auto* s = new dm_seqset;
     s->ctx = ctx;
     s->n = n;
@@ -153,13 +270,18 @@ dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets,
 
         uint8_t* d_raw = nullptr;
         uint64_t* d_raw_off = nullptr;
-        DM_CUDA(cudaMallocAsync(&d_raw, nbytes + 16, st));
+        if (d_raw_given) {  // bytes already on the device (streamed batches); not owned
+            d_raw = const_cast<uint8_t*>(d_raw_given);
+            s->owns_raw = false;
+        } else {
+            DM_CUDA(cudaMallocAsync(&d_raw, nbytes + 16, st));
+        }
         DM_CUDA(cudaMallocAsync(&d_raw_off, (n + 1) * sizeof(uint64_t), st));
         s->d_raw = d_raw;
         s->d_raw_off = d_raw_off;
         std::vector<uint64_t> rel(n + 1);
         for (uint32_t i = 0; i <= n; ++i) rel[i] = offsets[i] - base;
-        if (nbytes) DM_CUDA(cudaMemcpyAsync(d_raw, data + base, nbytes, cudaMemcpyHostToDevice, st));
+        if (nbytes && !d_raw_given) DM_CUDA(cudaMemcpyAsync(d_raw, data + base, nbytes, cudaMemcpyHostToDevice, st));
         DM_CUDA(cudaMemcpyAsync(d_raw_off, rel.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st));
         s->raw_off = rel;
 
@@ -223,7 +345,7 @@ dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets,
 }  // namespace dm
 
 dm_seqset::~dm_seqset() {
-    if (d_raw) cudaFreeAsync(d_raw, ctx->stream);
+    if (d_raw && owns_raw) cudaFreeAsync(d_raw, ctx->stream);
     if (d_raw_off) cudaFreeAsync(d_raw_off, ctx->stream);
     if (d_codes) cudaFreeAsync(d_codes, ctx->stream);
     if (d_off) cudaFreeAsync(d_off, ctx->stream);

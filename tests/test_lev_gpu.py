@@ -131,3 +131,42 @@ def test_cfg1_full_properties(dm, ctx, orc):
         a = data[offs[2 * i]:offs[2 * i + 1]]
         b = data[offs[2 * i + 1]:offs[2 * i + 2]]
         assert d[i] == orc.levenshtein(a, b)
+
+
+def test_packed_streaming_matches(dm, ctx, orc, monkeypatch):
+    """dm_lev_pairs_packed (host buffer, overlapped chunks) == resident batch."""
+    monkeypatch.setenv("DM_STREAM_CHUNK_BYTES", "200000")  # force ~25 chunks
+    data, offs = dm.synth(1, scale=0.004)  # 4000 pairs
+    got = dm.lev_pairs_packed(data, offs, ctx)
+    ss = dm.SeqSet(data=data, offsets=offs, ctx=ctx)
+    n = (len(offs) - 1) // 2
+    ia = np.arange(n) * 2
+    assert np.array_equal(got, dm.lev_pairs(ss, ia, ia + 1))
+    for i in (0, 1, n // 2, n - 1):
+        assert got[i] == orc.levenshtein(data[offs[2 * i]:offs[2 * i + 1]], data[offs[2 * i + 1]:offs[2 * i + 2]])
+    import torch
+    pinned = torch.frombuffer(bytearray(data), dtype=torch.uint8).pin_memory()
+    assert np.array_equal(dm.lev_pairs_packed(pinned, offs, ctx), got)
+
+
+@pytest.mark.parametrize("chunk", ["1", "3000", "50000"])
+def test_packed_streaming_mixed_chunks(dm, ctx, orc, monkeypatch, chunk):
+    """Chunks with different alphabets (2/5/8 bit-planes), empty sequences and
+    one-pair chunks; each chunk is recoded on its own."""
+    monkeypatch.setenv("DM_STREAM_CHUNK_BYTES", chunk)
+    rng = random.Random(int(chunk))
+    alphabets = ["ACGT", "ARNDCQEGHILKMFPSTWYV", "".join(chr(c) for c in range(33, 127))]
+    seqs = []
+    for k in range(300):
+        alpha = alphabets[(k // 40) % 3]
+        for _ in range(2):
+            n = 0 if rng.random() < 0.05 else rng.randint(1, 700)
+            seqs.append(rand_str(rng, n, alpha))
+    data = "".join(seqs).encode()
+    offs = np.zeros(len(seqs) + 1, dtype=np.uint64)
+    offs[1:] = np.cumsum([len(x) for x in seqs])
+    got = dm.lev_pairs_packed(data, offs, ctx)
+    want = [orc.levenshtein(seqs[2 * i], seqs[2 * i + 1]) for i in range(300)]
+    assert list(got) == want
+    # a second call on the same context reuses the planner slots
+    assert list(dm.lev_pairs_packed(data, offs, ctx)) == want
