@@ -100,10 +100,12 @@ struct dm_ctx {
     // scratch for the distance engine
     dm::DevBuf items, out, counter, aux, aux2, aux3, lev_all, lev_items;
     cudaStream_t copy_stream = nullptr;  // host->device staging of streamed batches
-    dm::DevBuf stage0, stage1, stage2, stream_pairs, stream_out, stream_offs;
-    dm_ctx* prep[3] = {};  // planner contexts of the streamed path (own stream + scratch)
-    static constexpr int kLevSide = 4;  // side streams the distance buckets fan out on
+    static constexpr int kStreamSlots = 4;  // chunks of a streamed batch in flight
+    dm::DevBuf stage[kStreamSlots], stream_pairs, stream_out, stream_offs;
+    dm_ctx* prep[kStreamSlots] = {};  // planner contexts of the streamed path (own stream + scratch)
+    static constexpr int kLevSide = 8;  // side streams the distance buckets fan out on
     cudaStream_t lev_side[kLevSide] = {};
+    int lev_rr = 0;
     cudaEvent_t lev_fork = nullptr, lev_join[kLevSide] = {};
     dm::PinnedBuf pin_items, pin_out;
     // scratch for the aligner / merge scheduler
@@ -114,11 +116,12 @@ struct dm_ctx {
 
 private:
     void attach(cudaStream_t* s) {
-        for (dm::DevBuf* b : {&items, &out, &counter, &aux, &aux2, &aux3, &lev_all, &lev_items, &stage0, &stage1, &stage2,
+        for (dm::DevBuf* b : {&items, &out, &counter, &aux, &aux2, &aux3, &lev_all, &lev_items,
                               &stream_pairs, &stream_out, &stream_offs, &nw_in, &nw_table,
                               &nw_jobs, &nw_trace,
                               &nw_res, &nw_gaps, &rows_a, &rows_b, &colmap, &tree_buf})
             b->sp = s;
+        for (dm::DevBuf& b : stage) b.sp = s;
     }
 };
 

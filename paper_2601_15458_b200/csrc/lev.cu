@@ -63,7 +63,8 @@ struct LevArgs {
     const uint64_t* planes;
     uint32_t* out;
     uint32_t* counter;
-    uint32_t one;  // == 1; opaque to ptxas so the carry chains stay on the FMA pipe
+    uint32_t one;        // == 1; opaque to ptxas so the carry chains stay on the FMA pipe
+    uint32_t max_pulls;  // task pulls per warp before its block retires (see launch_one)
 };
 
 // One lane = W consecutive 32-bit words of the pattern, handled as ONE
@@ -121,7 +122,7 @@ __global__ void __launch_bounds__(256, NP == 2 ? 3 : 1) lev_kernel(const LevArgs
     const int grp = lane >> lgG;
     const uint32_t gpw = 32u >> lgG;
 
-    for (;;) {
+    for (uint32_t pull = 0; pull < a.max_pulls; ++pull) {
         uint32_t base = 0;
         if (lane == 0) base = atomicAdd(a.counter, gpw);
         base = __shfl_sync(FULL, base, 0);
@@ -255,10 +256,19 @@ void launch_one(const LevArgs& a, int sm_count, cudaStream_t st) {
         DM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lev_kernel<NP, W>, 256, smem));
         occ = std::max(occ, 1);
     }
-    const uint64_t lanes = (uint64_t)a.nitems << a.lgG;
-    const uint64_t want = (lanes + 255) / 256;
-    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)occ * sm_count));
-    lev_kernel<NP, W><<<grid, 256, smem, st>>>(a);
+    // Warps pull tasks (32/G jobs) from the counter; each retires after
+    // max_pulls tasks, and the grid is sized for ~kWaves waves of resident
+    // blocks, so blocks turn over during a launch: kernels on other streams
+    // (the planners of streamed batches) get SM slots within a fraction of
+    // a bucket instead of after it. grid * 8 warps * max_pulls >= tasks.
+    constexpr uint64_t kWaves = 4;
+    const uint64_t tasks = ((uint64_t)a.nitems + (32u >> a.lgG) - 1) / (32u >> a.lgG);
+    const uint64_t resident = (uint64_t)occ * sm_count;
+    const uint64_t want = (tasks + 7) / 8;  // blocks if every warp pulled once
+    const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(want, resident * kWaves));
+    LevArgs b = a;
+    b.max_pulls = (uint32_t)((tasks + grid * 8 - 1) / (grid * 8));
+    lev_kernel<NP, W><<<(unsigned)grid, 256, smem, st>>>(b);
 }
 
 template <int NP, int W>
@@ -420,9 +430,12 @@ void plan_batch(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const uin
 
 // Kernel phase: one persistent launch per non-empty bucket. A bucket's launch
 // drains with a tail (its last warp tasks run while SMs empty out), so the
-// buckets go out on kLevSide side streams forked from `st`, largest words per
-// lane first: the next bucket's blocks take the SMs the previous one frees.
-int launch_plan(dm_ctx* ctx, const LevPlan& P, const dm_seqset* s, uint32_t* d_out, cudaStream_t st) {
+// buckets go out on side streams, largest per-task work first: the next
+// bucket's blocks take the SMs the previous one frees. `after` (optional) is
+// the event the launches must follow; by default they follow `st`. `st`
+// waits for all of them on return.
+int launch_plan(dm_ctx* ctx, const LevPlan& P, const dm_seqset* s, uint32_t* d_out, cudaStream_t st,
+                cudaEvent_t after = nullptr) {
     uint64_t starts[kBuckets];
     int order[kBuckets], nb = 0;
     uint64_t start = 0;
@@ -433,7 +446,8 @@ int launch_plan(dm_ctx* ctx, const LevPlan& P, const dm_seqset* s, uint32_t* d_o
     }
     // largest per-task work first: lanes per pair x words per lane
     std::stable_sort(order, order + nb, [](int x, int y) { return ((x % 32) << (x / 32)) > ((y % 32) << (y / 32)); });
-    const bool fork = nb > 1;
+    const bool fork = nb > 1 || after != nullptr;
+    int used[kLevSide], nused = 0;
     if (fork) {
         if (!ctx->lev_fork) {
             DM_CUDA(cudaEventCreateWithFlags(&ctx->lev_fork, cudaEventDisableTiming));
@@ -442,8 +456,18 @@ int launch_plan(dm_ctx* ctx, const LevPlan& P, const dm_seqset* s, uint32_t* d_o
                 DM_CUDA(cudaEventCreateWithFlags(&ctx->lev_join[k], cudaEventDisableTiming));
             }
         }
-        DM_CUDA(cudaEventRecord(ctx->lev_fork, st));
-        for (int k = 0; k < std::min(nb, kLevSide); ++k) DM_CUDA(cudaStreamWaitEvent(ctx->lev_side[k], ctx->lev_fork, 0));
+        if (!after) {
+            DM_CUDA(cudaEventRecord(ctx->lev_fork, st));
+            after = ctx->lev_fork;
+        }
+        // rotate through the side streams across calls, so back-to-back
+        // batches (streamed chunks) do not queue behind each other's tails
+        for (int i = 0; i < std::min(nb, kLevSide); ++i) {
+            used[nused] = (ctx->lev_rr + i) % kLevSide;
+            DM_CUDA(cudaStreamWaitEvent(ctx->lev_side[used[nused]], after, 0));
+            ++nused;
+        }
+        ctx->lev_rr = (ctx->lev_rr + nused) % kLevSide;
     }
     for (int i = 0; i < nb; ++i) {
         const int b = order[i];
@@ -459,14 +483,13 @@ int launch_plan(dm_ctx* ctx, const LevPlan& P, const dm_seqset* s, uint32_t* d_o
         a.out = d_out;
         a.counter = P.counters + b;
         a.one = 1u;
-        launch_bucket(s->planes, b % 32, a, ctx->sm_count, fork ? ctx->lev_side[i % kLevSide] : st);
+        launch_bucket(s->planes, b % 32, a, ctx->sm_count, fork ? ctx->lev_side[used[i % nused]] : st);
         DM_CUDA(cudaGetLastError());
     }
-    if (fork)
-        for (int k = 0; k < std::min(nb, kLevSide); ++k) {
-            DM_CUDA(cudaEventRecord(ctx->lev_join[k], ctx->lev_side[k]));
-            DM_CUDA(cudaStreamWaitEvent(st, ctx->lev_join[k], 0));
-        }
+    for (int i = 0; i < nused; ++i) {
+        DM_CUDA(cudaEventRecord(ctx->lev_join[used[i]], ctx->lev_side[used[i]]));
+        DM_CUDA(cudaStreamWaitEvent(st, ctx->lev_join[used[i]], 0));
+    }
     return nb;
 }
 
@@ -576,8 +599,9 @@ void lev_plan_then_launch(dm_ctx* prep, dm_ctx* ctx, const dm_seqset* s, const u
     LevPlan P;
     plan_batch(prep, s, d_ia, d_ib, nullptr, n, P);
     DM_CUDA(cudaEventRecord(planned, prep->stream));
-    DM_CUDA(cudaStreamWaitEvent(ctx->stream, planned, 0));
-    const int launches = launch_plan(ctx, P, s, d_out, ctx->stream);
+    // the kernels follow the planner directly, not ctx->stream: this batch's
+    // buckets start while the previous batch's tails still drain
+    const int launches = launch_plan(ctx, P, s, d_out, ctx->stream, planned);
     ctx->launches += launches;
     if (tot) {
         tot->cells += P.hc[0];

@@ -1,7 +1,7 @@
 // Streamed pair batches from host memory (the end-to-end path of the
 // distance engine): pair i = (sequence 2i, sequence 2i+1) of a packed host
 // buffer. The batch is cut into chunks that move through three streams:
-//   copy stream     upload of chunk c+2 (the offsets go up once, first)
+//   copy stream     uploads of chunks c+1..c+3 (offsets, then residues)
 //   planner stream  census/recode/bit-planes + pair planning of chunk c+1
 //                   (one planner context per staging slot: own scratch)
 //   ctx->stream     distance kernels of chunk c
@@ -39,7 +39,11 @@ dm_ctx* prep_context(dm_ctx* ctx, int k) {
         auto* p = new dm_ctx;
         p->device = ctx->device;
         p->sm_count = ctx->sm_count;
-        if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        // planners run at high priority: their blocks take the first SM slots
+        // the distance kernels free (the host waits on them)
+        int least = 0, greatest = 0;
+        DM_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        if (cudaStreamCreateWithPriority(&p->stream, cudaStreamNonBlocking, greatest) != cudaSuccess) {
             delete p;
             throw cuda_error("cannot create a planner stream");
         }
@@ -51,7 +55,7 @@ dm_ctx* prep_context(dm_ctx* ctx, int k) {
     return ctx->prep[k];
 }
 
-constexpr int NB = 3;  // chunks in flight: copying, planning, computing
+constexpr int NB = dm_ctx::kStreamSlots;  // chunks in flight: uploading (NB-1), planning/computing
 
 struct ChunkEvents {
     cudaEvent_t copied[NB] = {}, recoded[NB] = {}, planned[NB] = {}, done[NB] = {}, ready = nullptr;
@@ -78,26 +82,43 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
     if (2 * npairs > 0xffffffffull) throw invalid_argument("too many sequences in one streamed batch");
     for (uint64_t i = 0; i < 2 * npairs; ++i)
         if (offsets[i + 1] < offsets[i]) throw invalid_argument("sequence offsets must be non-decreasing");
-    const uint64_t total = offsets[2 * npairs] - offsets[0];
-    uint64_t target = 256ull << 20;  // residue bytes per chunk
-    const char* env = std::getenv("DM_STREAM_CHUNK_BYTES");
-    if (env) target = std::max<uint64_t>(1, std::strtoull(env, nullptr, 10));
-    const uint64_t avg = std::max<uint64_t>(1, total / npairs);
-    const uint64_t per = std::max<uint64_t>(env ? 1 : 4096, target / avg);
-    const uint64_t nchunks = (npairs + per - 1) / per;
+    // Chunk boundaries (pair indices). Sizes ramp up from `small` to `big`
+    // residue bytes so the first kernels start after a short upload, and
+    // halve again over the tail so little compute is left once the last
+    // upload lands.
+    uint64_t big = 256ull << 20, small = 32ull << 20;
+    if (const char* env = std::getenv("DM_STREAM_CHUNK_BYTES"))
+        big = small = std::max<uint64_t>(1, std::strtoull(env, nullptr, 10));
+    std::vector<uint64_t> cb{0};
+    for (uint64_t lo = 0, k = 0; lo < npairs; ++k) {
+        const uint64_t rem = offsets[2 * npairs] - offsets[2 * lo];
+        uint64_t t = std::min(big, small << std::min<uint64_t>(k, 20));
+        if (rem < 2 * t) t = std::max(small, rem / 2);
+        // smallest hi > lo with offsets[2hi] - offsets[2lo] >= t
+        uint64_t a = lo + 1, z = npairs;
+        while (a < z) {
+            const uint64_t mid = (a + z) / 2;
+            if (offsets[2 * mid] - offsets[2 * lo] >= t) z = mid; else a = mid + 1;
+        }
+        lo = a;
+        cb.push_back(lo);
+    }
+    const uint64_t nchunks = cb.size() - 1;
+    uint64_t per = 1, maxbytes = 0;
+    for (uint64_t c = 0; c < nchunks; ++c) {
+        per = std::max(per, cb[c + 1] - cb[c]);
+        maxbytes = std::max(maxbytes, offsets[2 * cb[c + 1]] - offsets[2 * cb[c]]);
+    }
+    const uint64_t oslot = 2 * per + 1;  // offsets per staging slot
     if (!ctx->copy_stream) DM_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
     dm_ctx* prep[NB];
     for (int b = 0; b < NB; ++b) prep[b] = prep_context(ctx, b);
-    uint64_t maxbytes = 0;
-    for (uint64_t c = 0; c < nchunks; ++c) {
-        const uint64_t lo = c * per, hi = std::min(npairs, lo + per);
-        maxbytes = std::max(maxbytes, offsets[2 * hi] - offsets[2 * lo]);
-    }
     ChunkEvents ev;
     dm_seqset* live[NB] = {};
     const bool trace = std::getenv("DM_TRACE") != nullptr;
     const auto t_start = std::chrono::steady_clock::now();
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tl;
+    std::vector<std::pair<cudaEvent_t, uint64_t>> tc;
     cudaEvent_t tl0 = nullptr;
     if (trace) {
         cudaEventCreate(&tl0);
@@ -117,9 +138,10 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
     };
     try {
         // every buffer the side streams touch is (re)allocated on ctx->stream first
-        uint8_t* stage[NB] = {(uint8_t*)ctx->stage0.get(maxbytes + 16), (uint8_t*)ctx->stage1.get(maxbytes + 16),
-                              (uint8_t*)ctx->stage2.get(maxbytes + 16)};
-        uint64_t* d_offs = ctx->stream_offs.as<uint64_t>(2 * npairs + 1);
+        uint8_t* stage[NB];
+        for (int b = 0; b < NB; ++b) stage[b] = (uint8_t*)ctx->stage[b].get(maxbytes + 16);
+        uint64_t* d_offs = ctx->stream_offs.as<uint64_t>(NB * oslot);
+        uint64_t* h_offs = ctx->pin_items.as<uint64_t>(NB * oslot);
         uint32_t* d_ab = ctx->stream_pairs.as<uint32_t>(2 * per + 2);
         uint32_t* d_res = ctx->stream_out.as<uint32_t>(npairs);
         uint32_t* h_res = ctx->pin_out.as<uint32_t>(npairs);
@@ -128,33 +150,43 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
         DM_CUDA(cudaGetLastError());
         DM_CUDA(cudaEventRecord(ev.ready, ctx->stream));
         DM_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ev.ready, 0));
-        DM_CUDA(cudaMemcpyAsync(d_offs, offsets, (2 * npairs + 1) * 8, cudaMemcpyHostToDevice, ctx->copy_stream));
         auto issue_copy = [&](uint64_t c) {
             const int b = (int)(c % NB);
-            const uint64_t lo = c * per, hi = std::min(npairs, lo + per);
+            const uint64_t lo = cb[c], hi = cb[c + 1];
+            // chunk offsets go up from a pinned slot (a pageable copy would block
+            // the host behind the bulk upload already queued)
+            if (c >= NB) DM_CUDA(cudaEventSynchronize(ev.copied[b]));  // slot's last upload done
+            std::memcpy(h_offs + b * oslot, offsets + 2 * lo, (2 * (hi - lo) + 1) * 8);
             if (c >= NB) DM_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ev.recoded[b], 0));
+            DM_CUDA(cudaMemcpyAsync(d_offs + b * oslot, h_offs + b * oslot, (2 * (hi - lo) + 1) * 8,
+                                    cudaMemcpyHostToDevice, ctx->copy_stream));
             const uint64_t a0 = offsets[2 * lo], a1 = offsets[2 * hi];
             if (a1 > a0)
                 DM_CUDA(cudaMemcpyAsync(stage[b], data + a0, a1 - a0, cudaMemcpyHostToDevice, ctx->copy_stream));
             DM_CUDA(cudaEventRecord(ev.copied[b], ctx->copy_stream));
+            if (trace) {
+                cudaEvent_t e;
+                cudaEventCreate(&e);
+                cudaEventRecord(e, ctx->copy_stream);
+                tc.push_back({e, a1 - a0});
+            }
         };
-        issue_copy(0);
-        if (nchunks > 1) issue_copy(1);
+        for (uint64_t c = 0; c + 1 < NB && c < nchunks; ++c) issue_copy(c);
         for (uint64_t c = 0; c < nchunks; ++c) {
             const int b = (int)(c % NB);
             dm_ctx* P = prep[b];
-            const uint64_t lo = c * per, hi = std::min(npairs, lo + per), cnt = hi - lo;
+            const uint64_t lo = cb[c], hi = cb[c + 1], cnt = hi - lo;
             DM_CUDA(cudaStreamWaitEvent(P->stream, ev.copied[b], 0));
             if (c >= NB) DM_CUDA(cudaStreamWaitEvent(P->stream, ev.done[b], 0));  // chunk c-NB's kernels
             delete live[b];  // stream-ordered frees behind that wait
             live[b] = nullptr;
             // census + recode + bit-planes on the planner stream (one host sync)
             const double t0 = trace ? now_ms() : 0.0;
-            live[b] = seqset_create_device(P, stage[b], d_offs + 2 * lo, offsets + 2 * lo, (uint32_t)(2 * cnt));
+            live[b] = seqset_create_device(P, stage[b], d_offs + b * oslot, offsets + 2 * lo, (uint32_t)(2 * cnt));
             DM_CUDA(cudaEventRecord(ev.recoded[b], P->stream));  // staging b free again
             const double t1 = trace ? now_ms() : 0.0;
-            // keep two chunk uploads queued so the copy engine never idles
-            if (c + 2 < nchunks) issue_copy(c + 2);
+            // keep NB-1 chunk uploads queued so the copy engine never idles
+            if (c + NB - 1 < nchunks) issue_copy(c + NB - 1);
             // plan on the planner stream (second host sync), kernels on ctx->stream
             lev_plan_then_launch(P, ctx, live[b], d_ab, d_ab + per, cnt, d_res + lo, ev.planned[b], tot);
             DM_CUDA(cudaEventRecord(ev.done[b], ctx->stream));
@@ -181,6 +213,12 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
                 std::fprintf(stderr, "[stream] gpu: chunk %zu planned %.2f ms, kernels done %.2f ms\n", i, pa, ka);
                 cudaEventDestroy(tl[i].first);
                 cudaEventDestroy(tl[i].second);
+            }
+            for (size_t i = 0; i < tc.size(); ++i) {
+                float ca = 0;
+                cudaEventElapsedTime(&ca, tl0, tc[i].first);
+                std::fprintf(stderr, "[stream] gpu: chunk %zu uploaded %.2f ms (%.1f MB)\n", i, ca, tc[i].second / 1e6);
+                cudaEventDestroy(tc[i].first);
             }
             cudaEventDestroy(tl0);
         }
