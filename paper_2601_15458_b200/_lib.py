@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdmb200.so")
+# DM_LIB_PATH: load a differently-built copy (tuning experiments only)
+LIB_PATH = os.environ.get("DM_LIB_PATH") or os.path.join(_HERE, "libdmb200.so")
 
 DM_OK, DM_EINVAL, DM_ERUNTIME, DM_ECUDA, DM_ENOMEM = 0, 1, 2, 3, 4
 

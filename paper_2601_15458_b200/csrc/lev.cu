@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "dm_internal.h"
 #include "comm.h"
@@ -169,20 +170,25 @@ __global__ void __launch_bounds__(256, NP == 2 ? 3 : 1) lev_kernel(const LevArgs
         uint32_t steps = valid ? n + (uint32_t)G - 1u : 0u;
         steps = __reduce_max_sync(FULL, steps);
         const uint8_t* tp = a.codes + a.off[item.txt];
+        const bool lead = g == 0 && valid;  // lane reading the text
+        const uint32_t leadmask = g == 0 ? 0xffffffffu : 0u;
         uint32_t word = 0;
-        for (uint32_t s = 0; s < steps; ++s) {
+        // One text column through the lane pipeline. CHK: some lane of the
+        // warp may be outside its text (pipeline fill/drain, shorter texts of
+        // other groups, the final column); the steady state skips the checks.
+        auto column = [&](uint32_t s, auto chk, uint32_t own) {
+            constexpr bool CHK = decltype(chk)::value;
             // word = code << 2 | h_minus << 1 | h_plus; lane 0 synthesises its
-            // own (text code, h_in = +1).
+            // own (text code `own`, h_in = +1). Branch-free select on a mask.
             const uint32_t recv = __shfl_up_sync(FULL, word, 1, G);
-            const uint32_t own = (g == 0 && s < n) ? (uint32_t)tp[s] : 0u;
-            const uint32_t r = (g == 0) ? imad(own, four, a.one) : recv;
+            const uint32_t r = lop3<0xCA>(leadmask, imad(own, four, a.one), recv);  // lead ? own word : recv
             const uint32_t c = r >> 2;
             uint32_t hm = (r >> 1) & 1u;
             uint32_t hp = r & 1u;
             const uint32_t j = s - (uint32_t)g;
-            if (j < n) {
+            if (!CHK || j < n) {
                 // t_k = bit_k(c) - 1 (0 or all-ones), s_k = 2 t_k + 1 (+1 / -1)
-                uint32_t ts[NP], ss[NP];
+                [[maybe_unused]] uint32_t ts[NP], ss[NP];
                 if constexpr (!TAB) {
 #pragma unroll
                     for (int k = 0; k < NP; ++k) {
@@ -196,7 +202,7 @@ __global__ void __launch_bounds__(256, NP == 2 ? 3 : 1) lev_kernel(const LevArgs
                 //   Ph = Mv | ~(Xh | Pv) = Mv | ~(S | Pv | Xv (| h_minus))
                 // (on Pv bits S^Pv = ~S; off Pv bits Xh = S | E; Mv bits force Ph).
                 // LUT constants: lop3(a, b, c) truth table over (0xF0, 0xCC, 0xAA).
-                uint32_t X[W], S[W], Ph[W], Mh[W], Xv[W], T[W];
+                uint32_t X[W], S[W], Ph[W], Mh[W], Xv[W], T0 = 0;
 #pragma unroll
                 for (int w = 0; w < W; ++w) {
                     uint32_t e;
@@ -210,13 +216,15 @@ __global__ void __launch_bounds__(256, NP == 2 ? 3 : 1) lev_kernel(const LevArgs
                     Xv[w] = e | Mv[w];
                     // row 0 of the lane: h_in = -1 enters as a carry
                     X[w] = w == 0 ? lop3<0xA8>(e, hm, Pv[w]) : (e & Pv[w]);  // (e | hm) & Pv
-                    T[w] = w == 0 ? lop3<0xFE>(Pv[w], Xv[w], hm) : (Pv[w] | Xv[w]);
+                    if (w == 0) T0 = lop3<0xFE>(Pv[w], Xv[w], hm);
                 }
                 Chain<W>::add(S, X, Pv);
 #pragma unroll
                 for (int w = 0; w < W; ++w) {
                     Mh[w] = lop3<0xBA>(Pv[w], S[w], X[w]);  // (Pv & ~S) | X
-                    Ph[w] = lop3<0xF1>(Mv[w], S[w], T[w]);  // Mv | ~(S | T)
+                    // Ph = Mv | ~(S | Pv | Xv): Mv is a subset of Xv, so the two
+                    // terms are disjoint and the OR is an add -> FMA pipe
+                    Ph[w] = w == 0 ? lop3<0xF1>(Mv[w], S[w], T0) : imad(lop3<0x01>(S[w], Pv[w], Xv[w]), a.one, Mv[w]);
                 }
                 const uint32_t hpo = shl1<W>(Ph, hp, two, a.one);
                 const uint32_t hmo = shl1<W>(Mh, hm, two, a.one);
@@ -227,7 +235,7 @@ __global__ void __launch_bounds__(256, NP == 2 ? 3 : 1) lev_kernel(const LevArgs
                 }
                 hp = hpo;
                 hm = hmo;
-                if (j == n - 1) {
+                if (CHK && j == n - 1) {
                     int acc = 0;
 #pragma unroll
                     for (int w = 0; w < W; ++w) {
@@ -240,7 +248,25 @@ __global__ void __launch_bounds__(256, NP == 2 ? 3 : 1) lev_kernel(const LevArgs
                 }
             }
             word = imad(c, four, imad(hm, two, hp));
+        };
+        // steady state [s0, s1): every valid lane has 0 <= j < n - 1
+        uint32_t nmin = __reduce_min_sync(FULL, valid ? n : 0xffffffffu);
+        const uint32_t s1 = nmin == 0xffffffffu || nmin == 0 ? 0u : nmin - 1u;
+        const uint32_t s0 = min((uint32_t)G - 1u, s1);
+        auto code_at = [&](uint32_t s) -> uint32_t { return (lead && s < n) ? (uint32_t)__ldg(tp + s) : 0u; };
+        uint32_t s = 0;
+        for (; s < s0; ++s) column(s, std::true_type{}, code_at(s));
+        // steady state, four columns per text load (16-B aligned code runs)
+        for (; s < s1 && (s & 3u); ++s) column(s, std::false_type{}, code_at(s));
+        for (; s + 4 <= s1; s += 4) {
+            const uint32_t t4 = lead ? __ldg(reinterpret_cast<const uint32_t*>(tp + s)) : 0u;
+            column(s, std::false_type{}, t4 & 0xffu);
+            column(s + 1, std::false_type{}, __byte_perm(t4, 0u, 0x4441u));
+            column(s + 2, std::false_type{}, __byte_perm(t4, 0u, 0x4442u));
+            column(s + 3, std::false_type{}, t4 >> 24);
         }
+        for (; s < s1; ++s) column(s, std::false_type{}, code_at(s));
+        for (; s < steps; ++s) column(s, std::true_type{}, code_at(s));
         for (int o = G >> 1; o > 0; o >>= 1) partial += __shfl_down_sync(FULL, partial, o, G);
         if (valid && g == 0) a.out[item.slot] = n + (uint32_t)partial;
     }
