@@ -9,9 +9,14 @@ A step = one pass of the distance engine over the whole pair batch.
   value  GCUPS (cells = sum |a|*|b|, untrimmed) with the sequences and pair
          lists already resident in HBM; device time (CUDA events on the
          launching stream), max over ranks, aggregated over all ranks.
-  e2e    same metric through the C ABI with HOST buffers: every step uploads
-         the step's sequences from pinned host memory (dm_seqset_create),
-         runs dm_lev_pairs (pair lists H2D, distances D2H) and frees them.
+  e2e    same metric through the C ABI with HOST buffers: every step hands
+         the packed pairs in pinned host memory to dm_lev_pairs_packed, which
+         uploads them in chunks overlapped with the kernels and returns the
+         distances in host memory (wall clock around the call).
+  nw     the NW micro-benchmark of SURVEY.md §8(d): the first 65,536 cfg1
+         pairs through dm_nw_batch (nucleotide scheme, affine -10/-1, full
+         traceback), bit-checked against the C restatement on a sample;
+         roofline c_nw = 13 INT32 ops/cell.
 
 --impl reference times the compiled reference (oracle/_ref, the unmodified
 divmsa C++ sources) on the box's host cores: divmsa::parallel_for +
@@ -36,6 +41,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 C_LEV = 10.0 / 32.0  # canonical INT32 ops per Levenshtein cell
+C_NW = 13.0          # canonical INT32 ops per Gotoh cell
 
 
 def dist_env():
@@ -126,6 +132,90 @@ def cpu_baseline(data, offs, n_pairs, budget_s=12.0, threads=None):
                       f"divmsa::parallel_for(grain 64)+levenshtein on {threads} host threads"}
 
 
+def nw_micro(dm, ctx, data, offs, p_int32, npairs=65536, reps=3, cpu=True):
+    """SURVEY.md §8(d) NW micro-benchmark: first `npairs` cfg1 pairs, nw_align each."""
+    import ctypes as C
+    from paper_2601_15458_b200._lib import check, lib
+    npairs = min(npairs, (len(offs) - 1) // 2)
+    offs = np.asarray(offs, dtype=np.int64)
+    buf = np.frombuffer(data, dtype=np.uint8)
+
+    def pack(idx):
+        lens = offs[idx + 1] - offs[idx]
+        o = np.zeros(len(idx) + 1, dtype=np.uint64)
+        o[1:] = np.cumsum(lens)
+        out = np.concatenate([buf[offs[i]:offs[i + 1]] for i in idx])
+        return out.tobytes(), o
+
+    ia = np.arange(npairs) * 2
+    A, ao = pack(ia)
+    B, bo = pack(ia + 1)
+    sc = dm.ScoringScheme.nucleotide()
+    u64p = C.POINTER(C.c_uint64)
+
+    def run():
+        h = C.c_void_p()
+        s = dm.dm_stats()
+        t0 = time.perf_counter()
+        check(lib().dm_nw_batch(ctx.handle, A, ao.ctypes.data_as(u64p), B, bo.ctypes.data_as(u64p), npairs,
+                                sc.table.ctypes.data_as(C.POINTER(C.c_int16)),
+                                sc.has_symbol.ctypes.data_as(C.POINTER(C.c_uint8)), sc.open_surcharge(),
+                                sc.gap_extend(), C.byref(h), C.byref(s)))
+        wall = time.perf_counter() - t0
+        return h, s, wall
+
+    h, s, _ = run()
+    lib().dm_pw_free(h)
+    fwd = tot = wall = 0.0
+    for _ in range(reps):
+        h, s, w = run()
+        fwd += s.align_ms
+        tot += s.kernel_ms
+        wall += w
+        last = h if _ == reps - 1 else None
+        if last is None:
+            lib().dm_pw_free(h)
+    cells = float(s.cells)
+    # bit-check a sample of the timed results against the C restatement
+    import oracle
+    orc = oracle.restatement()
+    table = orc.table("nt")
+    for k in (0, 1, npairs // 2, npairs - 1):
+        a = data[int(offs[2 * k]):int(offs[2 * k + 1])]
+        b = data[int(offs[2 * k + 1]):int(offs[2 * k + 2])]
+        want = orc.nw_align(a, b, table, -10, -1)
+        if lib().dm_pw_score(last, k) != want["score"] or lib().dm_pw_len(last, k) != len(want["aligned_a"]):
+            raise SystemExit(f"bench: nw mismatch at pair {k}")
+    lib().dm_pw_free(last)
+    fwd_gcups = cells / (fwd / reps * 1e-3) / 1e9
+    res = {"workload": f"first {npairs} cfg1 pairs through nw_align (nucleotide, affine -10/-1, traceback)",
+           "pairs": npairs, "cells": int(cells), "cells_executed": int(s.cells_executed),
+           "kernel_gcups": cells / (tot / reps * 1e-3) / 1e9, "forward_gcups": fwd_gcups,
+           "e2e_gcups": cells / (wall / reps) / 1e9,
+           "roofline": {"bound": "int32", "achieved": fwd_gcups, "peak": p_int32 / C_NW / 1e9, "unit": "GCUPS",
+                        "frac": fwd_gcups / (p_int32 / C_NW / 1e9),
+                        "kernel": "nw_fwd_kernel<int32,NWW> (score + trace)",
+                        "peak_source": f"measured INT32 lane-op/s {p_int32:.3e} / c_nw=13 ops per cell"}}
+    if cpu:
+        import oracle as _o
+        from concurrent.futures import ThreadPoolExecutor
+        ref = _o.reference()
+        threads = os.cpu_count() or 1
+        k = max(threads, int(3.0 * 0.09e9 * threads / (cells / npairs)))
+        k = min(k, npairs)
+        pairs = [(data[int(offs[2 * i]):int(offs[2 * i + 1])], data[int(offs[2 * i + 1]):int(offs[2 * i + 2])])
+                 for i in range(k)]
+        c = float(sum(len(x) * len(y) for x, y in pairs))
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda p: ref.nw_align(p[0], p[1]), pairs))
+        dt = time.perf_counter() - t0
+        res["cpu_baseline"] = {"value": c / dt / 1e9, "unit": "GCUPS", "cores": threads, "kind": "reference",
+                               "sample": f"first {k} of the {npairs} pairs ({c:.3e} cells, {dt:.1f} s), "
+                                         f"divmsa::nw_align on {threads} host threads"}
+    return res
+
+
 def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
@@ -174,6 +264,7 @@ def main():
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--ref-step-s", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-nw", action="store_true", help="skip the NW micro-benchmark")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -301,6 +392,9 @@ def main():
                 "kernel": "lev_kernel<NP=2,R> (all buckets)",
                 "cells_executed_per_step": int(st.cells_executed)}
 
+    nw = nw_micro(dm, ctx, data, offs, p_int32, cpu=(rank == 0 and world == 1 and not args.no_cpu_baseline)) \
+        if not args.no_nw else None
+
     line = {"metric": "levenshtein_gcups", "value": value, "unit": "GCUPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
@@ -310,6 +404,8 @@ def main():
                        "l2": "inputs (%.1f GB/GPU) larger than L2" % (len(data) / 1e9),
                        "parallelism": f"dp{world} (independent pair batches)"},
             "gpu_launches": int(launches), "clocks": clk, "e2e": e2e, "roofline": roofline}
+    if nw is not None:
+        line["nw"] = nw
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(data, offs, n_pairs, args.cpu_budget_s)
     if rank == 0:

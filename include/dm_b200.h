@@ -54,7 +54,7 @@ typedef struct {
     uint64_t cells;          /* oracle-equivalent cells: sum |a|*|b| (untrimmed) */
     uint64_t cells_executed; /* cells the kernels actually computed (padding incl.) */
     uint64_t launches;       /* kernels launched */
-    double tree_ms, align_ms;
+    double tree_ms, align_ms; /* dm_msa: phase times; dm_nw_*: align_ms = forward-pass kernel time */
     uint64_t lev_calls, nw_calls;
 } dm_stats;
 

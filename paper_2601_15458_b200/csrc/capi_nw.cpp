@@ -86,8 +86,9 @@ void run_batch(dm_ctx* ctx, const char* A, const uint64_t* a_off, const char* B,
     if (st) {
         std::memset(st, 0, sizeof(*st));
         st->kernel_ms = no.fwd_ms + no.tb_ms;
+        st->align_ms = no.fwd_ms;
         st->cells = no.cells;
-        st->cells_executed = no.cells;
+        st->cells_executed = no.cells_exec;
         st->launches = no.launches;
         st->nw_calls = njobs;
     }

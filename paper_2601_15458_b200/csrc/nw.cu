@@ -209,6 +209,7 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
             bool time_kernels, bool layout_given) {
     out.fwd_ms = out.tb_ms = 0.f;
     out.cells = 0;
+    out.cells_exec = 0;
     out.launches = 0;
     const size_t nj = jobs.size();
     if (!layout_given) {
@@ -222,6 +223,7 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
     for (const auto& jb : jobs) {
         nmmax = std::max(nmmax, jb.n + jb.m);
         out.cells += (uint64_t)jb.n * jb.m;
+        out.cells_exec += (uint64_t)((jb.n + nwk::BAND - 1) / nwk::BAND) * nwk::BAND * jb.m;
         ttot += (uint64_t)jb.m * ((jb.n + 15) & ~15u);
     }
     if (nj == 0) return;
@@ -333,6 +335,7 @@ void nw_run_sharded(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& job
         out.fwd_ms += part.fwd_ms;
         out.tb_ms += part.tb_ms;
         out.cells += part.cells;
+        out.cells_exec += part.cells_exec;
         out.launches += part.launches;
     }
     if (real) {

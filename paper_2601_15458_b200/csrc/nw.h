@@ -46,6 +46,7 @@ struct NwOut {
     uint64_t gaps_total = 0;
     float fwd_ms = 0.f, tb_ms = 0.f;
     uint64_t cells = 0;
+    uint64_t cells_exec = 0;  // rows padded to whole bands
     uint64_t launches = 0;
 };
 

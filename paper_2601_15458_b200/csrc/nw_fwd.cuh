@@ -15,6 +15,8 @@
 // single-band alignments.
 #pragma once
 
+#include <type_traits>
+
 namespace dm {
 namespace nwk {
 
@@ -60,6 +62,23 @@ __device__ __forceinline__ uint32_t gather_lo(uint32_t a, uint32_t b, uint32_t c
     return __byte_perm(ab, cd, 0x5410);
 }
 
+template <int LUT>
+__device__ __forceinline__ uint32_t lop3(uint32_t x, uint32_t y, uint32_t z) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(x), "r"(y), "r"(z), "n"(LUT));
+    return d;
+}
+
+// (x & ~3) | tag as ONE LOP3: `keep` (= ~3) and `tag` live in registers
+// (opaque to ptxas, which would otherwise split the immediates over two ops)
+__device__ __forceinline__ int32_t retag(int32_t x, uint32_t keep, uint32_t tag) {
+    return (int32_t)lop3<0xEA>((uint32_t)x, keep, tag);
+}
+__device__ __forceinline__ int64_t retag(int64_t x, uint32_t, uint32_t tag) { return (x & ~(int64_t)3) | (int64_t)tag; }
+
+// bits of x where mask is set, bits of y elsewhere (one LOP3)
+__device__ __forceinline__ uint32_t bitsel(uint32_t x, uint32_t y, uint32_t mask) { return lop3<0xE4>(x, y, mask); }
+
 struct FwdArgs {
     const uint8_t* chars;
     const NwJob* jobs;
@@ -93,6 +112,8 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
     const V NEG = neg_inf<V>();
     const V O4 = (V)a.O4, E4 = (V)a.E4;
     const char* tbytes = reinterpret_cast<const char*>(s_table);
+    // opaque ~3 / tag constants (from the runtime 1) for the one-LOP3 retags
+    const uint32_t tag1 = (uint32_t)a.one, tag2 = tag1 + tag1, keep = ~(tag2 + tag1);
     for (;;) {
         __syncthreads();  // previous job fully done; table/lut loaded
         if (threadIdx.x == 0) sm.jid = atomicAdd(a.counter, 1u);
@@ -131,12 +152,17 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
             const bool has_in = NWW > 1 && band > 0;
             const bool has_out = NWW > 1 && band + 1 < nbands;
             V sM = 0, sGB = 0, sGA = 0;
-            const uint32_t steps = m + 31;
-            for (uint32_t s = 0; s < steps; ++s) {
+            // One column step of the band's lane pipeline. CHK: generic step
+            // (pipeline fill/drain: lanes may be outside 1..m; ring flow
+            // control decided from s). Steady steps (every lane inside, s in
+            // whole 16-column chunks, k = s mod 16) drop the range checks and
+            // take the flow-control points from k alone (warp-uniform).
+            auto step = [&](uint32_t s, auto chk, int k) {
+                constexpr bool CHK = decltype(chk)::value;
                 const V rM = shfl_up1(sM), rGB = shfl_up1(sGB), rGA = shfl_up1(sGA);
                 if constexpr (NWW > 1) {
                     // consumer side (lane 0 reads column s+1 this step)
-                    if (has_in && (s % CHUNK) == 0 && s < m) {
+                    if (CHK ? (has_in && (s % CHUNK) == 0 && s < m) : (has_in && k == 0)) {
                         if (g == 0) {
                             const uint32_t need = seq_in + min(s + CHUNK, m);
                             while (sm.pub[rin] < need) {
@@ -145,7 +171,8 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
                         __syncwarp();
                     }
                     // producer side (lane 31 writes column s-30 this step)
-                    if (has_out && s >= 31 && ((s - 31) % CHUNK) == 0 && s - 31 < m) {
+                    if (CHK ? (has_out && s >= 31 && ((s - 31) % CHUNK) == 0 && s - 31 < m)
+                            : (has_out && k == CHUNK - 1)) {
                         if (g == 31) {
                             const uint32_t jj = s - 30;  // first column of the chunk
                             const uint32_t last = seq_out + min(jj + CHUNK - 1, m);
@@ -156,24 +183,24 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
                     }
                 }
                 const uint32_t j = s - (uint32_t)g + 1;  // 1..m when active
-                if (j - 1 < m) {
-                    V uM, uGB, uGA;
-                    if (g == 0) {
-                        if (band == 0) {  // row 0 (pairwise.cpp:322-330)
-                            uM = (V)(NEG | 2);
-                            uGB = (V)(NEG | 1);
-                            uGA = (V)(a.O4 + (int64_t)j * a.E4);
-                        } else {
-                            const V* e = sm.ring[rin][(seq_in + j) % RING];
-                            uM = e[0];
-                            uGB = e[1];
-                            uGA = e[2];
-                        }
+                if (!CHK || j - 1 < m) {
+                    // lane 0's input row (band 0: row 0, pairwise.cpp:322-330;
+                    // else the band above via the ring), read at lane 0's
+                    // column s+1 by every lane (one broadcast, no divergence)
+                    V iM, iGB, iGA;
+                    if (band == 0) {
+                        iM = (V)(NEG | 2);
+                        iGB = (V)(NEG | 1);
+                        iGA = (V)(a.O4 + (int64_t)(s + 1) * a.E4);
                     } else {
-                        uM = rM;
-                        uGB = rGB;
-                        uGA = rGA;
+                        const V* e = sm.ring[rin][(seq_in + s + 1) % RING];
+                        iM = e[0];
+                        iGB = e[1];
+                        iGA = e[2];
                     }
+                    V uM = g == 0 ? iM : rM;
+                    V uGB = g == 0 ? iGB : rGB;
+                    V uGA = g == 0 ? iGA : rGA;
                     // diagonal of row r = old (previous column) values of row r-1,
                     // pre-reduced to their max before row r-1 is overwritten, so
                     // every state updates in place (no register rotation)
@@ -196,10 +223,12 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
                             const uint32_t wm = gather_lo(tm[0], tm[1], tm[2], tm[3]);
                             const uint32_t wb = gather_lo(tgb[0], tgb[1], tgb[2], tgb[3]);
                             const uint32_t wa = gather_lo(tga[0], tga[1], tga[2], tga[3]);
-                            tw[r >> 2] = (wm & 0x03030303u) | ((wb & 0x03030303u) << 2) | ((wa & 0x03030303u) << 4);
+                            // byte = tagM | tagGB << 2 | tagGA << 4 (bits 6-7 are
+                            // don't-care: the traceback masks every field)
+                            tw[r >> 2] = bitsel(bitsel(wm, wb << 2, 0x03030303u), wa << 4, 0x0F0F0F0Fu);
                         }
-                        LM[r] = (mraw & ~(V)3) | 2;
-                        LGB[r] = (gbraw & ~(V)3) | 1;
+                        LM[r] = retag(mraw, keep, tag2);
+                        LGB[r] = retag(gbraw, keep, tag1);
                         LGA[r] = garaw & ~(V)3;
                         uM = LM[r];
                         uGB = LGB[r];
@@ -217,18 +246,30 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
                             e[0] = uM;
                             e[1] = uGB;
                             e[2] = uGA;
-                            if ((j % CHUNK) == 0 || j == m) {
+                            if (CHK ? ((j % CHUNK) == 0 || j == m) : (k == CHUNK - 2)) {
                                 __threadfence_block();
                                 sm.pub[rout] = seq_out + j;
                             }
                         }
-                        if (has_in && g == 0 && ((j % CHUNK) == 0 || j == m)) {
+                        if (has_in && g == 0 && (CHK ? ((j % CHUNK) == 0 || j == m) : (k == CHUNK - 1))) {
                             __threadfence_block();  // ring reads complete before the slot is released
                             sm.con[rin] = seq_in + j;
                         }
                     }
                 }
+            };
+            const uint32_t steps = m + 31;
+            uint32_t s = 0;
+            for (; s < min(32u, steps); ++s) step(s, std::true_type{}, 0);
+            // steady state: s in [32, m), whole chunks of CHUNK columns
+            if (m > 32) {
+                const uint32_t s_end = 32 + ((m - 32) & ~(uint32_t)(CHUNK - 1));
+                // not unrolled: one step is ~300 instructions, a chunk of them
+                // would not fit the instruction cache
+#pragma unroll 1
+                for (; s < s_end; ++s) step(s, std::false_type{}, (int)(s % CHUNK));
             }
+            for (; s < steps; ++s) step(s, std::true_type{}, 0);
             // final state at (n, m) (pairwise.cpp:374-375): the lane owning row n
             if (n >= i0 && n < i0 + RR) {
                 V fM = LM[0], fGB = LGB[0], fGA = LGA[0];
