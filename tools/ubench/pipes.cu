@@ -39,6 +39,11 @@ __global__ void k(uint32_t* out, int iters, uint32_t seed) {
                           else asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[q]) : "r"(b), "r"(c)); }
         if (MODE == 18) a[q] = __vimax3_s16x2_relu(a[q], b, c) ^ a[q];
         if (MODE == 19) asm volatile("vadd2.s32.s32.s32.sat %0, %0, %1, %2;" : "+r"(a[q]) : "r"(b), "r"(c));
+        if (MODE == 20) a[q] = __vimax3_s16x2(a[q], b, c);
+        if (MODE == 21) a[q] = __vmaxs2(a[q], b);
+        if (MODE == 22) a[q] = __vimax_s16x2_relu(a[q], b) ^ c;
+        if (MODE == 23) { if (q & 1) a[q] = __vimax3_s16x2(a[q], b, c);
+                          else asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[q]) : "r"(b | 1u), "r"(c)); }
         if (MODE == 6) { if (q & 1) asm volatile("shf.l.wrap.b32 %0, %0, %1, 1;" : "+r"(a[q]) : "r"(b));
                          else asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[q]) : "r"(b | 1u), "r"(c)); }
       }
@@ -66,9 +71,10 @@ int main() {
   uint32_t* d; cudaMalloc(&d, 64);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const char* names[] = {"LOP3", "IMAD", "IMAD.HI", "LOP3+IMAD.HI", "LOP3+IMAD", "SHF.L.W", "SHF+IMAD", "IMAD.WIDE(+LOP3)", "LOP3+IMAD.WIDE", "IADD3cc+IMAD",
-                         "IMNMX", "VIADDMNMX", "VIMNMX3", "IMNMX+IMAD", "VIADDMNMX.16x2", "PRMT", "VIADDMNMX+IMAD", "IMNMX+LOP3", "VIMNMX3.16x2relu", "vadd2.sat"};
-  double v[20] = {run<0>(d, sms), run<1>(d, sms), run<2>(d, sms), run<3>(d, sms), run<4>(d, sms), run<5>(d, sms), run<6>(d, sms), run<7>(d, sms), run<8>(d, sms), run<9>(d, sms),
-                  run<10>(d, sms), run<11>(d, sms), run<12>(d, sms), run<13>(d, sms), run<14>(d, sms), run<15>(d, sms), run<16>(d, sms), run<17>(d, sms), run<18>(d, sms), run<19>(d, sms)};
-  for (int i = 0; i < 20; ++i) printf("%-18s %.3e lane-ops/s\n", names[i], v[i]);
+                         "IMNMX", "VIADDMNMX", "VIMNMX3", "IMNMX+IMAD", "VIADDMNMX.16x2", "PRMT", "VIADDMNMX+IMAD", "IMNMX+LOP3", "VIMNMX3.16x2relu", "vadd2.sat", "VIMNMX3.16x2", "vmaxs2", "VIMNMX.16x2relu^", "VIMNMX3.16x2+IMAD"};
+  double v[24] = {run<0>(d, sms), run<1>(d, sms), run<2>(d, sms), run<3>(d, sms), run<4>(d, sms), run<5>(d, sms), run<6>(d, sms), run<7>(d, sms), run<8>(d, sms), run<9>(d, sms),
+                  run<10>(d, sms), run<11>(d, sms), run<12>(d, sms), run<13>(d, sms), run<14>(d, sms), run<15>(d, sms), run<16>(d, sms), run<17>(d, sms), run<18>(d, sms), run<19>(d, sms),
+                  run<20>(d, sms), run<21>(d, sms), run<22>(d, sms), run<23>(d, sms)};
+  for (int i = 0; i < 24; ++i) printf("%-18s %.3e lane-ops/s\n", names[i], v[i]);
   return 0;
 }
