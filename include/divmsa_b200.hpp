@@ -335,4 +335,97 @@ inline Msa align_all(const ClusterTree& tree, std::span<const std::string_view> 
     return m;
 }
 
+// ---- quality metrics (metrics.hpp, distance.hpp:hamming_aligned) -------------
+/// metrics.hpp:13-35
+struct MetricsReport {
+    std::size_t width = 0;
+    double stretch = 0.0;
+    double gap_percent = 0.0;
+    double distortion = 0.0;
+    double p_min = 0.0;
+    double p_avg = 0.0;
+    double p_max = 0.0;
+    std::size_t sample_size = 0;
+    std::size_t pair_count = 0;
+    std::uint64_t seed = 0;
+    std::size_t zero_distance_pairs = 0;
+    double time_s = 0.0;
+};
+
+inline constexpr std::size_t kDefaultSampleSize = 10000;
+inline constexpr std::size_t kDefaultPairBudget = 100000;
+
+namespace detail {
+inline std::string flatten(const Msa& msa) {
+    std::string flat;
+    flat.reserve(msa.rows.size() * msa.width);
+    for (const auto& r : msa.rows) flat += r;
+    return flat;
+}
+inline void row_pair(std::string_view a, std::string_view b, const char* what, std::uint32_t* cons,
+                     std::uint32_t* mism, std::uint32_t* ham) {
+    if (a.size() != b.size()) throw std::invalid_argument(std::string(what) + " requires equal-length rows");
+    check(dm_row_pair_stats(ctx(), a.data(), a.size(), b.data(), b.size(), cons, mism, ham));
+}
+}  // namespace detail
+
+/// distance.hpp (distance.cpp:50-57)
+inline std::uint32_t hamming_aligned(std::string_view a, std::string_view b) {
+    std::uint32_t c, m, h;
+    detail::row_pair(a, b, "hamming_aligned", &c, &m, &h);
+    return h;
+}
+
+/// metrics.hpp:37-39 (metrics.cpp:16-27)
+inline double gap_percent(const Msa& msa) {
+    const std::string flat = detail::flatten(msa);
+    double v = 0.0;
+    detail::check(dm_gap_percent(detail::ctx(), flat.data(), msa.rows.size(), msa.width, &v));
+    return v;
+}
+
+/// metrics.hpp:41-43 (metrics.cpp:29-45)
+inline double p_score(std::string_view a, std::string_view b) {
+    std::uint32_t c, m, h;
+    detail::row_pair(a, b, "p_score", &c, &m, &h);
+    return c == 0 ? 1.0 : static_cast<double>(m) / static_cast<double>(c);
+}
+
+/// metrics.hpp:45-49 (metrics.cpp:47-56)
+inline double distortion_pair(std::string_view a_aligned, std::string_view b_aligned, std::string_view a_raw,
+                              std::string_view b_raw) {
+    const std::uint32_t lev = levenshtein(a_raw, b_raw);
+    if (lev == 0) throw std::invalid_argument("distortion is undefined for identical sequences");
+    return static_cast<double>(hamming_aligned(a_aligned, b_aligned)) / static_cast<double>(lev);
+}
+
+/// metrics.hpp:51-56 (metrics.cpp:84-169); the pair sweep runs on the GPU.
+inline MetricsReport evaluate(const Msa& msa, std::span<const std::string_view> raws, std::size_t sample_size,
+                              std::size_t pair_budget, std::uint64_t seed, ThreadPool&) {
+    const std::string flat = detail::flatten(msa);
+    std::string raw;
+    std::vector<std::uint64_t> off{0};
+    for (auto r : raws) {
+        raw += r;
+        off.push_back(raw.size());
+    }
+    dm_metrics m{};
+    detail::check(dm_evaluate(detail::ctx(), flat.data(), msa.rows.size(), msa.width, msa.row_to_sequence.data(),
+                              raw.data(), off.data(), static_cast<std::uint32_t>(raws.size()), sample_size,
+                              pair_budget, seed, &m));
+    MetricsReport r;
+    r.width = m.width;
+    r.stretch = m.stretch;
+    r.gap_percent = m.gap_percent;
+    r.distortion = m.distortion;
+    r.p_min = m.p_min;
+    r.p_avg = m.p_avg;
+    r.p_max = m.p_max;
+    r.sample_size = m.sample_size;
+    r.pair_count = m.pair_count;
+    r.seed = m.seed;
+    r.zero_distance_pairs = m.zero_distance_pairs;
+    return r;
+}
+
 }  // namespace divmsa

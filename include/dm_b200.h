@@ -114,6 +114,31 @@ int dm_lev_one_to_many(dm_ctx* ctx, const dm_seqset* s, uint32_t from, const uin
 int dm_geometric_median(dm_ctx* ctx, const dm_seqset* s, const uint32_t* members, uint64_t n,
                         uint64_t seed, uint64_t exact_cap, uint32_t* out);
 
+/* ---- quality metrics (divmsa::evaluate, metrics.cpp:84-169) ------------ */
+/* Mirrors divmsa::MetricsReport (metrics.hpp:13-35). */
+typedef struct {
+    uint64_t width;
+    double stretch, gap_percent, distortion, p_min, p_avg, p_max;
+    uint64_t sample_size, pair_count, seed, zero_distance_pairs;
+    double time_s;
+} dm_metrics;
+/* rows: nrows x width bytes (row r = msa.rows[r]); row_to_sequence[r] indexes
+ * the raw sequences (raw, raw_offsets[nraw + 1]). Seeded sampling identical
+ * to the reference (sample_size rows, then pair_budget pairs); every field is
+ * bit-identical to divmsa::evaluate. DM_EINVAL "cannot evaluate an empty
+ * alignment" / "gap_percent of an empty alignment". */
+int dm_evaluate(dm_ctx* ctx, const char* rows, uint64_t nrows, uint64_t width, const uint32_t* row_to_sequence,
+                const char* raw, const uint64_t* raw_offsets, uint32_t nraw, uint64_t sample_size,
+                uint64_t pair_budget, uint64_t seed, dm_metrics* out);
+/* divmsa::gap_percent (metrics.cpp:16-27). */
+int dm_gap_percent(dm_ctx* ctx, const char* rows, uint64_t nrows, uint64_t width, double* out);
+/* Column counts of two equal-length aligned rows: columns where both carry a
+ * residue, mismatches among those (p_score = mismatched / considered, 1.0
+ * when considered == 0; metrics.cpp:29-45) and differing columns
+ * (hamming_aligned, distance.cpp:50-57). DM_EINVAL on unequal lengths. */
+int dm_row_pair_stats(dm_ctx* ctx, const char* a, uint64_t na, const char* b, uint64_t nb, uint32_t* considered,
+                      uint32_t* mismatched, uint32_t* hamming);
+
 /* ---- guide tree ------------------------------------------------------- */
 /* nodes: capacity 2n-1; order: n. Errors: DM_ERUNTIME "cannot build a cluster
  * tree from zero sequences" / "...input was not de-duplicated". */

@@ -186,6 +186,13 @@ class Restatement:
         return [raw[r * W:(r + 1) * W].decode() for r in range(len(bs))], W
 
 
+class RefMetrics(C.Structure):
+    """ref_metrics in oracle/ref_capi.cpp (divmsa::MetricsReport fields)."""
+    _fields_ = [("width", C.c_uint64)] + [(f, C.c_double) for f in (
+        "stretch", "gap_percent", "distortion", "p_min", "p_avg", "p_max")] + [(f, C.c_uint64) for f in (
+            "sample_size", "pair_count", "seed", "zero_distance_pairs")] + [("time_s", C.c_double)]
+
+
 class Reference:
     """The unmodified reference library (oracle/_ref/libdivmsa_ref.so)."""
 
@@ -235,6 +242,18 @@ class Reference:
         L.ref_free.argtypes = [C.c_void_p]
         L.ref_insert_gap_columns.restype = C.c_int
         L.ref_insert_gap_columns.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, _u32p, C.c_uint64, C.c_char_p]
+        L.ref_evaluate.restype = C.c_int
+        L.ref_evaluate.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, _u32p, C.POINTER(C.c_char_p), _u32p,
+                                   C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, C.POINTER(RefMetrics)]
+        L.ref_gap_percent.restype = C.c_int
+        L.ref_gap_percent.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, C.POINTER(C.c_double)]
+        L.ref_p_score.restype = C.c_int
+        L.ref_p_score.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64, C.POINTER(C.c_double)]
+        L.ref_hamming_aligned.restype = C.c_int
+        L.ref_hamming_aligned.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64, _u32p]
+        L.ref_distortion_pair.restype = C.c_int
+        L.ref_distortion_pair.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64,
+                                          C.c_char_p, C.c_uint64, C.POINTER(C.c_double)]
         self.L = L
 
     def _check(self, rc):
@@ -346,6 +365,43 @@ class Reference:
         self.L.ref_free(p)
         W = w.value
         return [raw[r * W:(r + 1) * W].decode() for r in range(len(bs))]
+
+    def evaluate(self, rows: List[str], row_to_sequence, raws, sample_size: int = 10000,
+                 pair_budget: int = 100000, seed: int = 42, threads: int = 0) -> dict:
+        """divmsa::evaluate (metrics.cpp:84-169) on an Msa given as rows."""
+        width = len(rows[0]) if rows else 0
+        block = "".join(rows).encode()
+        rts = np.ascontiguousarray(row_to_sequence, dtype=np.uint32)
+        bs, arr, lens = _seq_arrays(raws)
+        out = RefMetrics()
+        self._check(self.L.ref_evaluate(block, len(rows), width, rts.ctypes.data_as(_u32p), arr,
+                                        lens.ctypes.data_as(_u32p), len(bs), sample_size, pair_budget, seed,
+                                        threads or os.cpu_count() or 1, C.byref(out)))
+        return {f: getattr(out, f) for f, _ in RefMetrics._fields_}
+
+    def gap_percent(self, rows: List[str]) -> float:
+        width = len(rows[0]) if rows else 0
+        v = C.c_double()
+        self._check(self.L.ref_gap_percent("".join(rows).encode(), len(rows), width, C.byref(v)))
+        return v.value
+
+    def p_score(self, a, b) -> float:
+        a, b = _bytes(a), _bytes(b)
+        v = C.c_double()
+        self._check(self.L.ref_p_score(a, len(a), b, len(b), C.byref(v)))
+        return v.value
+
+    def hamming_aligned(self, a, b) -> int:
+        a, b = _bytes(a), _bytes(b)
+        v = C.c_uint32()
+        self._check(self.L.ref_hamming_aligned(a, len(a), b, len(b), C.byref(v)))
+        return v.value
+
+    def distortion_pair(self, a, b, ra, rb) -> float:
+        a, b, ra, rb = _bytes(a), _bytes(b), _bytes(ra), _bytes(rb)
+        v = C.c_double()
+        self._check(self.L.ref_distortion_pair(a, len(a), b, len(b), ra, len(ra), rb, len(rb), C.byref(v)))
+        return v.value
 
     def insert_gap_columns(self, rows: List[str], positions) -> List[str]:
         width = len(rows[0]) if rows else 0

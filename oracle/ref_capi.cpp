@@ -16,6 +16,9 @@
 //   ref_msa              -> build_tree + align_all         (pipeline.cpp:116,128)
 //   ref_align            -> divmsa::align_sequences        (pipeline.hpp:59)
 //   ref_insert_gap_columns -> divmsa::insert_gap_columns   (msa_merge.hpp:34)
+//   ref_evaluate         -> divmsa::evaluate               (metrics.hpp:53-56)
+//   ref_gap_percent, ref_p_score, ref_hamming_aligned, ref_distortion_pair
+//                        -> the metrics helpers            (metrics.hpp:39-49, distance.hpp)
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -26,6 +29,7 @@
 
 #include "divmsa/cluster_tree.hpp"
 #include "divmsa/distance.hpp"
+#include "divmsa/metrics.hpp"
 #include "divmsa/msa_merge.hpp"
 #include "divmsa/pairwise.hpp"
 #include "divmsa/parallel.hpp"
@@ -295,6 +299,84 @@ int ref_insert_gap_columns(const char* rows, std::uint64_t nrows, std::uint64_t 
         return fail(e, kInvalidArgument);
     } catch (const std::exception& e) {
         return fail(e, kRuntimeError);
+    }
+}
+
+
+// Same field order as dm_metrics (include/dm_b200.h).
+struct ref_metrics {
+    std::uint64_t width;
+    double stretch, gap_percent, distortion, p_min, p_avg, p_max;
+    std::uint64_t sample_size, pair_count, seed, zero_distance_pairs;
+    double time_s;
+};
+
+int ref_evaluate(const char* rows, std::uint64_t nrows, std::uint64_t width, const std::uint32_t* row_to_sequence,
+                 const char* const* raws, const std::uint32_t* raw_lens, std::uint64_t nraw,
+                 std::uint64_t sample_size, std::uint64_t pair_budget, std::uint64_t seed, int threads,
+                 ref_metrics* out) {
+    try {
+        divmsa::Msa m;
+        m.width = width;
+        for (std::uint64_t r = 0; r < nrows; ++r) {
+            m.rows.emplace_back(rows + r * width, width);
+            m.row_to_sequence.push_back(row_to_sequence[r]);
+        }
+        const auto v = views(raws, raw_lens, nraw);
+        divmsa::ThreadPool pool(threads > 0 ? (unsigned)threads : 1u);
+        const auto t0 = std::chrono::steady_clock::now();
+        const divmsa::MetricsReport r = divmsa::evaluate(m, v, sample_size, pair_budget, seed, pool);
+        *out = ref_metrics{r.width, r.stretch, r.gap_percent, r.distortion, r.p_min, r.p_avg, r.p_max,
+                           r.sample_size, r.pair_count, r.seed, r.zero_distance_pairs,
+                           std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count()};
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, kInvalidArgument);
+    } catch (const std::exception& e) {
+        return fail(e, kRuntimeError);
+    }
+}
+
+int ref_gap_percent(const char* rows, std::uint64_t nrows, std::uint64_t width, double* out) {
+    try {
+        divmsa::Msa m;
+        m.width = width;
+        for (std::uint64_t r = 0; r < nrows; ++r) m.rows.emplace_back(rows + r * width, width);
+        *out = divmsa::gap_percent(m);
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, kInvalidArgument);
+    } catch (const std::exception& e) {
+        return fail(e, kRuntimeError);
+    }
+}
+
+int ref_p_score(const char* a, std::uint64_t na, const char* b, std::uint64_t nb, double* out) {
+    try {
+        *out = divmsa::p_score(std::string_view(a, na), std::string_view(b, nb));
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, kInvalidArgument);
+    }
+}
+
+int ref_hamming_aligned(const char* a, std::uint64_t na, const char* b, std::uint64_t nb, std::uint32_t* out) {
+    try {
+        *out = divmsa::hamming_aligned(std::string_view(a, na), std::string_view(b, nb));
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, kInvalidArgument);
+    }
+}
+
+int ref_distortion_pair(const char* a, std::uint64_t na, const char* b, std::uint64_t nb, const char* ra,
+                        std::uint64_t nra, const char* rb, std::uint64_t nrb, double* out) {
+    try {
+        *out = divmsa::distortion_pair(std::string_view(a, na), std::string_view(b, nb), std::string_view(ra, nra),
+                                       std::string_view(rb, nrb));
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, kInvalidArgument);
     }
 }
 

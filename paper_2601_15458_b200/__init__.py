@@ -15,7 +15,7 @@ from typing import List, Sequence
 
 import numpy as np
 
-from ._lib import DmError, check, dm_node, dm_stats, lib
+from ._lib import DmError, check, dm_metrics, dm_node, dm_stats, lib
 
 __version__ = "0.1.0"
 
@@ -453,6 +453,72 @@ def align(sequences: Sequence, alphabet: str = "auto", gap_open: int = -10, gap_
     if summary:
         return out, {f: getattr(summ, f) for f, _ in summ._fields_}, s.as_dict()
     return out
+
+
+# ---- quality metrics (divmsa/metrics.hpp; metrics.cpp, distance.cpp:50-57) --------------
+
+def _rows_block(rows) -> tuple:
+    rows = [r.encode() if isinstance(r, str) else bytes(r) for r in rows]
+    width = len(rows[0]) if rows else 0
+    if any(len(r) != width for r in rows):
+        raise ValueError("alignment rows must have equal width")
+    return b"".join(rows), len(rows), width
+
+
+def evaluate(msa_: Msa, raws, sample_size: int = 10000, pair_budget: int = 100000, seed: int = 42,
+             ctx: Context | None = None) -> dict:
+    """divmsa::evaluate (metrics.hpp:53-56): width, stretch, gap_percent and
+    the seeded pair sample's p-distance / distortion statistics. `raws` are
+    the unaligned sequences indexed by msa_.row_to_sequence. Bit-identical
+    to the reference; the pair work runs on the GPU."""
+    ctx = ctx or default_context()
+    block, nrows, width = _rows_block(msa_.rows)
+    rts = np.ascontiguousarray(msa_.row_to_sequence, dtype=np.uint32)
+    raw, offs = _pack(raws)
+    out = dm_metrics()
+    check(lib().dm_evaluate(ctx.handle, block, nrows, width, _ptr(rts), raw, _ptr(offs, C.c_uint64), len(offs) - 1,
+                            int(sample_size), int(pair_budget), int(seed), C.byref(out)))
+    return out.as_dict()
+
+
+def gap_percent(msa_or_rows, ctx: Context | None = None) -> float:
+    """divmsa::gap_percent (metrics.cpp:16-27)."""
+    ctx = ctx or default_context()
+    rows = msa_or_rows.rows if isinstance(msa_or_rows, Msa) else msa_or_rows
+    block, nrows, width = _rows_block(rows)
+    v = C.c_double()
+    check(lib().dm_gap_percent(ctx.handle, block, nrows, width, C.byref(v)))
+    return v.value
+
+
+def _row_pair(a, b, ctx, what: str):
+    a = a.encode() if isinstance(a, str) else bytes(a)
+    b = b.encode() if isinstance(b, str) else bytes(b)
+    if len(a) != len(b):
+        raise ValueError(f"{what} requires equal-length rows")
+    cons, mism, ham = C.c_uint32(), C.c_uint32(), C.c_uint32()
+    check(lib().dm_row_pair_stats((ctx or default_context()).handle, a, len(a), b, len(b), C.byref(cons),
+                                  C.byref(mism), C.byref(ham)))
+    return cons.value, mism.value, ham.value
+
+
+def p_score(a, b, ctx: Context | None = None) -> float:
+    """divmsa::p_score (metrics.cpp:29-45): mismatches over shared residue columns, 1.0 when none."""
+    cons, mism, _ = _row_pair(a, b, ctx, "p_score")
+    return 1.0 if cons == 0 else mism / cons
+
+
+def hamming_aligned(a, b, ctx: Context | None = None) -> int:
+    """divmsa::hamming_aligned (distance.cpp:50-57)."""
+    return _row_pair(a, b, ctx, "hamming_aligned")[2]
+
+
+def distortion_pair(a_aligned, b_aligned, a_raw, b_raw, ctx: Context | None = None) -> float:
+    """divmsa::distortion_pair (metrics.cpp:47-56): aligned hamming / raw levenshtein."""
+    lev = levenshtein(a_raw, b_raw, ctx)
+    if lev == 0:
+        raise ValueError("distortion is undefined for identical sequences")
+    return hamming_aligned(a_aligned, b_aligned, ctx) / lev
 
 
 def synth(cfg: int, scale: float = 1.0, seed: int = 0):

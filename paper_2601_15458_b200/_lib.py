@@ -24,6 +24,16 @@ class dm_node(C.Structure):
         (f, C.c_int32) for f in ("left", "right", "parent")] + [("depth", C.c_uint32)]
 
 
+class dm_metrics(C.Structure):
+    """divmsa::MetricsReport (metrics.hpp:13-35)."""
+    _fields_ = [("width", C.c_uint64)] + [(f, C.c_double) for f in (
+        "stretch", "gap_percent", "distortion", "p_min", "p_avg", "p_max")] + [(f, C.c_uint64) for f in (
+            "sample_size", "pair_count", "seed", "zero_distance_pairs")] + [("time_s", C.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
 class dm_stats(C.Structure):
     _fields_ = [("kernel_ms", C.c_double), ("total_ms", C.c_double), ("cells", C.c_uint64),
                 ("cells_executed", C.c_uint64), ("launches", C.c_uint64), ("tree_ms", C.c_double),
@@ -101,6 +111,10 @@ SIGNATURES = {
                                      _u8p, C.c_uint64, C.c_int, C.POINTER(C.c_void_p), _u64p, _P,
                                      C.POINTER(dm_stats)]),
     "dm_synth": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.POINTER(C.c_char_p), C.POINTER(_u64p), _u64p]),
+    "dm_evaluate": (C.c_int, [_P, C.c_char_p, C.c_uint64, C.c_uint64, _u32p, C.c_char_p, _u64p, C.c_uint32,
+                              C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(dm_metrics)]),
+    "dm_gap_percent": (C.c_int, [_P, C.c_char_p, C.c_uint64, C.c_uint64, C.POINTER(C.c_double)]),
+    "dm_row_pair_stats": (C.c_int, [_P, C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64, _u32p, _u32p, _u32p]),
     "dm_free": (None, [_P]),
 }
 

@@ -19,16 +19,11 @@
 #include <vector>
 
 #include "dm_b200.h"
+#include "rng.h"
 
 namespace {
 
-uint64_t mix_seed(uint64_t x) {
-    x += 0x9e3779b97f4a7c15ULL;
-    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
-    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
-    return x ^ (x >> 31);
-}
-uint64_t combine_seed(uint64_t seed, uint64_t salt) { return mix_seed(seed ^ mix_seed(salt)); }
+using dm::rng::combine_seed;
 
 struct Rng {
     std::mt19937_64 g;

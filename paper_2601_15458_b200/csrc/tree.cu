@@ -31,6 +31,7 @@
 #include <unordered_set>
 
 #include "dm_internal.h"
+#include "rng.h"
 
 namespace dm {
 namespace {
@@ -38,37 +39,11 @@ namespace {
 constexpr uint32_t kNo = 0xffffffffu;
 constexpr int kSubMax = 128;  // largest subtree resolved in shared memory
 
-// ---------------------------------------------------------------- host rng
-uint64_t mix_seed(uint64_t x) {
-    x += 0x9e3779b97f4a7c15ULL;
-    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
-    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
-    return x ^ (x >> 31);
-}
-uint64_t combine_seed(uint64_t seed, uint64_t salt) { return mix_seed(seed ^ mix_seed(salt)); }
-uint64_t bounded_draw(std::mt19937_64& g, uint64_t bound) {
-    const uint64_t limit = UINT64_MAX - UINT64_MAX % bound;
-    uint64_t v;
-    do v = g(); while (v >= limit);
-    return v % bound;
-}
-std::vector<uint64_t> sample_distinct(std::mt19937_64& g, uint64_t n, uint64_t k) {
-    std::vector<uint64_t> out;
-    if (k >= n) {
-        out.resize(n);
-        std::iota(out.begin(), out.end(), 0);
-        return out;
-    }
-    std::unordered_set<uint64_t> picked;
-    picked.reserve(k * 2);
-    for (uint64_t j = n - k; j < n; ++j) {
-        const uint64_t t = bounded_draw(g, j + 1);
-        picked.insert(picked.count(t) ? j : t);
-    }
-    out.assign(picked.begin(), picked.end());
-    std::sort(out.begin(), out.end());
-    return out;
-}
+// ---------------------------------------------------------------- host rng (rng.h)
+using rng::bounded_draw;
+using rng::combine_seed;
+using rng::sample_distinct;
+
 uint64_t hash_members(const uint32_t* m, size_t n) {
     uint64_t h = 14695981039346656037ULL;
     for (size_t i = 0; i < n; ++i) {

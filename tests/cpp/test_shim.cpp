@@ -3,6 +3,7 @@
 // pins: /root/reference/proj/tests/test_distance.cpp:11-28,
 // test_pairwise.cpp:137-186, test_cluster_tree.cpp:115-221,
 // test_msa_merge.cpp:79-176.
+#include <cmath>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -109,6 +110,24 @@ int main() {
         t.nodes[2] = ClusterNode{1, 2, 1, 0, kNoSequence, kNoSequence, -1, -1, 0, 1};
         const Msa p = merge(t, t.nodes[0], align_leaf(t.nodes[1], seqs), align_leaf(t.nodes[2], seqs), affine, pool);
         CHECK(p.width == 4 && p.rows[0] == "ACGT" && p.rows[1] == "A-GT");
+    }
+    {
+        // metrics (test_metrics.cpp:74-128)
+        Msa m;
+        m.rows = {"AC-T", "AG-T"};
+        m.row_to_sequence = {0, 1};
+        m.width = 4;
+        CHECK(std::abs(gap_percent(m) - 25.0) < 1e-12);
+        CHECK(std::abs(p_score("AC-T", "AG-T") - 1.0 / 3) < 1e-12 && p_score("A---", "-CCC") == 1.0);
+        CHECK(hamming_aligned("ACGT", "A-GT") == 1);
+        CHECK(distortion_pair("AC--", "--GT", "AC", "GT") == 2.0);
+        CHECK(throws<std::invalid_argument>([&] { p_score("AC", "A"); }, "equal-length"));
+        CHECK(throws<std::invalid_argument>([&] { distortion_pair("ACGT", "ACGT", "ACGT", "ACGT"); }, "identical"));
+        const std::vector<std::string_view> raws{"ACT", "AGT"};
+        const MetricsReport r = evaluate(m, raws, 100, 100, 42, pool);
+        CHECK(r.width == 4 && r.sample_size == 2 && r.pair_count == 1 && r.seed == 42);
+        CHECK(std::abs(r.stretch - 4.0 / 3) < 1e-12 && std::abs(r.p_avg - 1.0 / 3) < 1e-12 && r.distortion == 1.0);
+        CHECK(throws<std::invalid_argument>([&] { evaluate(Msa{}, raws, 10, 10, 1, pool); }, "empty alignment"));
     }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "all shim checks passed", failures);
     return failures ? 1 : 0;

@@ -188,3 +188,20 @@ def test_restatement_vs_compiled_reference(orc, ref):
     rows, w = orc.align_all(seqs, n1, o1, orc.table("nt"), -10, -1)
     r = ref.msa(seqs, seed=9)
     assert rows == r["rows"] and w == r["width"]
+
+
+def test_reference_metrics_pins(ref):
+    """The compiled reference's metrics (the oracle of tests/test_metrics_gpu.py)
+    against test_metrics.cpp:74-128."""
+    assert ref.gap_percent(["AC-", "A-C"]) == pytest.approx(100.0 / 3)
+    assert ref.gap_percent(["--", "--"]) == 100.0
+    assert ref.p_score("AC-T", "AG-T") == pytest.approx(1.0 / 3)
+    assert ref.p_score("A---", "-CCC") == 1.0
+    assert ref.distortion_pair("AC--", "--GT", "AC", "GT") == pytest.approx(2.0)
+    with pytest.raises(ValueError, match="identical"):
+        ref.distortion_pair("ACGT", "ACGT", "ACGT", "ACGT")
+    r = ref.evaluate(["AC-T", "AG-T"], [0, 1], ["ACT", "AGT"], 100, 100, 42)
+    assert (r["width"], r["sample_size"], r["pair_count"], r["seed"]) == (4, 2, 1, 42)
+    assert r["p_avg"] == pytest.approx(1.0 / 3) and r["distortion"] == pytest.approx(1.0)
+    with pytest.raises(ValueError, match="empty alignment"):
+        ref.evaluate([], [], [])
