@@ -219,6 +219,25 @@ int dm_align_sequences(dm_ctx* ctx, const char* data, const uint64_t* offsets, u
                        int input_order, char** rows_out, uint64_t* width_out,
                        dm_align_summary* summary, dm_stats* st);
 
+/* ---- FASTA in / out (seq_io.cpp:44-225, pipeline.cpp:160-187) ---------- */
+/* divmsa::run_align: parse `input_path` (alphabet 0 auto = structural parse,
+ * 1/2 = validate while parsing), align_sequences (record ids in errors),
+ * write the aligned FASTA (80-column lines, formatted on the device) to
+ * "<output_path>.partial" and rename it into place. input_order: 1 rows in
+ * input order, 0 tree order (RowOrder::Tree, the CLI default). Errors:
+ * DM_ERUNTIME with the reference's messages ("<file>:<line>: ..."). */
+int dm_run_align(dm_ctx* ctx, const char* input_path, const char* output_path, int alphabet, int gap_open,
+                 int gap_extend, int flat, const int16_t* custom_table, const uint8_t* custom_has, uint64_t seed,
+                 int input_order, dm_align_summary* summary, dm_stats* st);
+/* divmsa::write_fasta over n records given as packed (data, offsets[n+1])
+ * id / description / residue arrays; the text is assembled on the device. */
+int dm_write_fasta(dm_ctx* ctx, const char* path, const char* ids, const uint64_t* id_off, const char* descs,
+                   const uint64_t* desc_off, const char* residues, const uint64_t* res_off, uint64_t n);
+/* divmsa::parse_fasta (alphabet 0 none, 1 nucleotide, 2 protein; allow_gaps =
+ * ParseOptions::allow_gaps). Outputs packed arrays, each freed with dm_free. */
+int dm_parse_fasta(const char* path, int alphabet, int allow_gaps, char** ids, uint64_t** id_off, char** descs,
+                   uint64_t** desc_off, char** residues, uint64_t** res_off, uint64_t* n);
+
 /* ---- synthetic inputs --------------------------- */
 /* cfg 0..4 at `scale` (1.0 = full size). Returns concatenated residues +
  * offsets (free with dm_free). For cfg 1, sequence 2i / 2i+1 form pair i. */

@@ -251,6 +251,12 @@ class Reference:
         L.ref_p_score.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64, C.POINTER(C.c_double)]
         L.ref_hamming_aligned.restype = C.c_int
         L.ref_hamming_aligned.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64, _u32p]
+        L.ref_run_align.restype = C.c_int
+        L.ref_run_align.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64,
+                                    C.c_int, C.c_int]
+        L.ref_write_fasta.restype = C.c_int
+        L.ref_write_fasta.argtypes = [C.c_char_p, C.c_char_p, _u64p, C.c_char_p, _u64p, C.c_char_p, _u64p,
+                                      C.c_uint64]
         L.ref_distortion_pair.restype = C.c_int
         L.ref_distortion_pair.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64,
                                           C.c_char_p, C.c_uint64, C.POINTER(C.c_double)]
@@ -378,6 +384,26 @@ class Reference:
                                         lens.ctypes.data_as(_u32p), len(bs), sample_size, pair_budget, seed,
                                         threads or os.cpu_count() or 1, C.byref(out)))
         return {f: getattr(out, f) for f, _ in RefMetrics._fields_}
+
+    def run_align(self, input_path: str, output_path: str, alphabet: str = "auto", gap_open: int = -10,
+                  gap_extend: int = -1, flat: bool = False, seed: int = 42, order: str = "tree",
+                  threads: int = 0) -> None:
+        """divmsa::run_align (pipeline.cpp:160-187): FASTA in, aligned FASTA out."""
+        a = {"auto": 0, "nt": 1, "aa": 2}[alphabet]
+        self._check(self.L.ref_run_align(input_path.encode(), output_path.encode(), a, gap_open, gap_extend,
+                                         int(flat), seed, int(order == "input"), threads or os.cpu_count() or 1))
+
+    def write_fasta(self, records, path: str) -> None:
+        """divmsa::write_fasta over [(id, description, residues), ...]."""
+        cols = []
+        for f in range(3):
+            bs = [_bytes(r[f]) for r in records]
+            off = np.zeros(len(bs) + 1, dtype=np.uint64)
+            off[1:] = np.cumsum([len(b) for b in bs]) if bs else []
+            cols.append((b"".join(bs), off))
+        self._check(self.L.ref_write_fasta(path.encode(), cols[0][0], cols[0][1].ctypes.data_as(_u64p), cols[1][0],
+                                           cols[1][1].ctypes.data_as(_u64p), cols[2][0],
+                                           cols[2][1].ctypes.data_as(_u64p), len(records)))
 
     def gap_percent(self, rows: List[str]) -> float:
         width = len(rows[0]) if rows else 0

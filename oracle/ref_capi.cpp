@@ -17,6 +17,8 @@
 //   ref_align            -> divmsa::align_sequences        (pipeline.hpp:59)
 //   ref_insert_gap_columns -> divmsa::insert_gap_columns   (msa_merge.hpp:34)
 //   ref_evaluate         -> divmsa::evaluate               (metrics.hpp:53-56)
+//   ref_run_align        -> divmsa::run_align              (pipeline.hpp:63-64)
+//   ref_write_fasta      -> divmsa::write_fasta            (seq_io.hpp:82-83)
 //   ref_gap_percent, ref_p_score, ref_hamming_aligned, ref_distortion_pair
 //                        -> the metrics helpers            (metrics.hpp:39-49, distance.hpp)
 #include <chrono>
@@ -34,6 +36,7 @@
 #include "divmsa/pairwise.hpp"
 #include "divmsa/parallel.hpp"
 #include "divmsa/pipeline.hpp"
+#include "divmsa/seq_io.hpp"
 
 namespace {
 
@@ -377,6 +380,45 @@ int ref_distortion_pair(const char* a, std::uint64_t na, const char* b, std::uin
         return 0;
     } catch (const std::invalid_argument& e) {
         return fail(e, kInvalidArgument);
+    }
+}
+
+
+int ref_run_align(const char* input, const char* output, int alphabet, int gap_open, int gap_extend, int flat,
+                  std::uint64_t seed, int input_order, int threads) {
+    try {
+        divmsa::RunConfig c;
+        c.alphabet = alphabet == 1   ? divmsa::AlphabetChoice::Nucleotide
+                     : alphabet == 2 ? divmsa::AlphabetChoice::Protein
+                                     : divmsa::AlphabetChoice::Auto;
+        c.gap_open = gap_open;
+        c.gap_extend = gap_extend;
+        c.gap_mode = flat ? divmsa::GapMode::Flat : divmsa::GapMode::Affine;
+        c.seed = seed;
+        c.threads = threads > 0 ? (unsigned)threads : 0u;
+        c.order = input_order ? divmsa::RowOrder::Input : divmsa::RowOrder::Tree;
+        divmsa::run_align(c, input, output);
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, kInvalidArgument);
+    } catch (const std::exception& e) {
+        return fail(e, kRuntimeError);
+    }
+}
+
+int ref_write_fasta(const char* path, const char* ids, const std::uint64_t* id_off, const char* descs,
+                    const std::uint64_t* desc_off, const char* residues, const std::uint64_t* res_off,
+                    std::uint64_t n) {
+    try {
+        std::vector<divmsa::FastaRecordView> v(n);
+        for (std::uint64_t k = 0; k < n; ++k)
+            v[k] = divmsa::FastaRecordView{std::string_view(ids + id_off[k], id_off[k + 1] - id_off[k]),
+                                           std::string_view(descs + desc_off[k], desc_off[k + 1] - desc_off[k]),
+                                           std::string_view(residues + res_off[k], res_off[k + 1] - res_off[k])};
+        divmsa::write_fasta(v, path);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e, kRuntimeError);
     }
 }
 

@@ -521,6 +521,61 @@ def distortion_pair(a_aligned, b_aligned, a_raw, b_raw, ctx: Context | None = No
     return hamming_aligned(a_aligned, b_aligned, ctx) / lev
 
 
+# ---- FASTA in / out (seq_io.hpp, pipeline.hpp:63-64) ---------------------------------------
+
+def run_align(input_path, output_path, alphabet: str = "auto", gap_open: int = -10, gap_extend: int = -1,
+              gap_mode: str = "affine", seed: int = 42, order: str = "tree", scheme: ScoringScheme | None = None,
+              ctx: Context | None = None, stats: bool = False):
+    """divmsa::run_align (pipeline.cpp:160-187): parse the FASTA file, align
+    (tree + merges on the GPU), write the aligned FASTA (assembled on the GPU)
+    to output_path via a ".partial" sibling. Returns the AlignSummary fields."""
+    from ._lib import dm_align_summary
+    ctx = ctx or default_context()
+    if alphabet not in ("auto", "nt", "aa"):
+        raise ValueError(f"unknown alphabet '{alphabet}' (expected auto, nt or aa)")
+    if order not in ("tree", "input"):
+        raise ValueError("order must be 'tree' or 'input'")
+    summ = dm_align_summary()
+    s = dm_stats()
+    check(lib().dm_run_align(ctx.handle, str(input_path).encode(), str(output_path).encode(),
+                             {"auto": 0, "nt": 1, "aa": 2}[alphabet], gap_open, gap_extend, int(_flat(gap_mode)),
+                             None if scheme is None else _ptr(scheme.table, C.c_int16),
+                             None if scheme is None else _ptr(scheme.has_symbol, C.c_uint8), int(seed),
+                             int(order == "input"), C.byref(summ), C.byref(s)))
+    out = {f: getattr(summ, f) for f, _ in summ._fields_}
+    return (out, s.as_dict()) if stats else out
+
+
+def write_fasta(records, path, ctx: Context | None = None) -> None:
+    """divmsa::write_fasta (seq_io.cpp:188-225) over [(id, description, residues), ...]:
+    80-column lines, text assembled on the GPU."""
+    ctx = ctx or default_context()
+    cols = [_pack([r[f] for r in records]) for f in range(3)]
+    check(lib().dm_write_fasta(ctx.handle, str(path).encode(), cols[0][0], _ptr(cols[0][1], C.c_uint64), cols[1][0],
+                               _ptr(cols[1][1], C.c_uint64), cols[2][0], _ptr(cols[2][1], C.c_uint64), len(records)))
+
+
+def parse_fasta(path, alphabet: str | None = None, allow_gaps: bool = False) -> list:
+    """divmsa::parse_fasta (seq_io.cpp:44-119): [(id, description, residues), ...]."""
+    a = {None: 0, "nt": 1, "aa": 2}[alphabet]
+    ptrs = [C.c_void_p() for _ in range(3)]
+    offs = [C.POINTER(C.c_uint64)() for _ in range(3)]
+    n = C.c_uint64()
+    check(lib().dm_parse_fasta(str(path).encode(), a, int(allow_gaps), C.byref(ptrs[0]), C.byref(offs[0]),
+                               C.byref(ptrs[1]), C.byref(offs[1]), C.byref(ptrs[2]), C.byref(offs[2]), C.byref(n)))
+    try:
+        cols = []
+        for f in range(3):
+            o = np.ctypeslib.as_array(offs[f], shape=(n.value + 1,)).copy()
+            raw = C.string_at(ptrs[f], int(o[-1])) if o[-1] else b""
+            cols.append([raw[int(o[k]):int(o[k + 1])].decode("latin-1") for k in range(n.value)])
+    finally:
+        for f in range(3):
+            lib().dm_free(ptrs[f])
+            lib().dm_free(C.cast(offs[f], C.c_void_p))
+    return list(zip(*cols))
+
+
 def synth(cfg: int, scale: float = 1.0, seed: int = 0):
     """Seeded synthetic inputs of BASELINE config `cfg`.
 

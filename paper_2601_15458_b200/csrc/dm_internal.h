@@ -154,6 +154,7 @@ struct dm_seqset {
 // Result of align_all / dm_msa (host side).
 struct dm_msa_out {
     uint64_t width = 0;
+    uint64_t dev_pitch = 0;  // the rows also stay in ctx->rows_a at this pitch until the next call on ctx
     std::vector<char> rows;  // rows x width, tree order
     std::vector<uint32_t> row_seq;
     std::vector<dm_node> nodes;

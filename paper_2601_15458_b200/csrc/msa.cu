@@ -245,6 +245,7 @@ dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node
         }
         const uint64_t width = W[0];
         out->width = width;
+        out->dev_pitch = pitch;
         out->rows.resize((uint64_t)n * width);
         if (width)
             DM_CUDA(cudaMemcpy2DAsync(out->rows.data(), width, rowsbuf.p, pitch, width, n, cudaMemcpyDeviceToHost,

@@ -14,7 +14,9 @@
 
 #include "capi_guard.h"
 #include "nw.h"
+#include "pipeline.h"
 
+namespace dm {
 namespace {
 
 constexpr std::string_view kNucleotide = "ACGTURYSWKMBDHVN";
@@ -37,6 +39,131 @@ int detect_alphabet(const char* data, uint64_t nbytes) {  // alphabet.cpp:37-57;
 }
 
 }  // namespace
+}  // namespace dm
+
+namespace dm {
+
+// align_sequences (pipeline.cpp:78-159) up to the re-expansion: validation,
+// de-duplication, tree + merges on the device. `ids` (optional) names the
+// records in error messages; without it they are "seq<i>" (py_module.cpp:134-138).
+AlignCore align_core(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint32_t n,
+                     const std::vector<std::string>* ids, int alphabet, int gap_open, int gap_extend, int flat,
+                     const int16_t* custom_table, const uint8_t* custom_has, uint64_t seed, int input_order,
+                     dm_stats* st) {
+    AlignCore res;
+    const auto t0 = std::chrono::steady_clock::now();
+    if (n == 0) throw runtime_error("no sequences to align");
+    if (gap_open > gap_extend || gap_extend > 0)
+        throw invalid_argument("gap penalties must satisfy gap_open <= gap_extend <= 0");
+    const uint64_t base = offsets[0];
+    const int kind = alphabet == 1 ? 0 : alphabet == 2 ? 1 : detect_alphabet(data + base, offsets[n] - base);
+    auto rec = [ids](uint32_t i) {
+        return "record '" + (ids ? (*ids)[i] : "seq" + std::to_string(i)) + "'";
+    };
+    if (!custom_table) {
+        bool member[256] = {};
+        for (char c : (kind == 0 ? kNucleotide : kProtein)) member[(unsigned char)c] = true;
+        for (uint32_t i = 0; i < n; ++i)
+            for (uint64_t p = offsets[i]; p < offsets[i + 1]; ++p) {
+                const char c = data[p];
+                if (c == '-') throw runtime_error(rec(i) + " contains gap symbol '-' in unaligned input");
+                if (!member[(unsigned char)c])
+                    throw runtime_error(rec(i) + " contains character '" + std::string(1, c) + "' outside the " +
+                                        (kind == 0 ? "nucleotide" : "protein") + " alphabet");
+            }
+    }
+    int16_t table[128 * 128];
+    uint8_t has[128];
+    int osur = 0;
+    if (custom_table) {
+        std::memcpy(table, custom_table, sizeof(table));
+        std::memcpy(has, custom_has, sizeof(has));
+        osur = flat ? 0 : gap_open;
+    } else {
+        const int rc = dm_scheme_default(kind, gap_open, gap_extend, flat, table, has, &osur);
+        if (rc != DM_OK) throw invalid_argument(last_error());
+    }
+    for (uint32_t i = 0; i < n; ++i)
+        for (uint64_t p = offsets[i]; p < offsets[i + 1]; ++p) {
+            const unsigned char c = (unsigned char)data[p];
+            if (c >= 128 || !has[c])
+                throw runtime_error(rec(i) + " contains character '" + std::string(1, (char)c) +
+                                    "' that the substitution matrix does not score");
+        }
+    // deduplicate: first occurrences in order (seq_io.cpp:168-186)
+    std::unordered_map<std::string_view, uint32_t> first;
+    first.reserve(n * 2);
+    std::vector<uint32_t> reps;
+    std::vector<std::vector<uint32_t>> dups;
+    for (uint32_t i = 0; i < n; ++i) {
+        std::string_view sv(data + offsets[i], offsets[i + 1] - offsets[i]);
+        auto it = first.find(sv);
+        if (it == first.end()) {
+            first.emplace(sv, (uint32_t)reps.size());
+            reps.push_back(i);
+            dups.emplace_back();
+        } else {
+            dups[it->second].push_back(i);
+        }
+    }
+    std::vector<uint64_t> roff(reps.size() + 1);
+    std::string rdata;
+    uint64_t tot = 0;
+    for (size_t r = 0; r < reps.size(); ++r) tot += offsets[reps[r] + 1] - offsets[reps[r]];
+    rdata.reserve(tot);
+    for (size_t r = 0; r < reps.size(); ++r) {
+        roff[r] = rdata.size();
+        rdata.append(data + offsets[reps[r]], offsets[reps[r] + 1] - offsets[reps[r]]);
+    }
+    roff[reps.size()] = rdata.size();
+    dm_seqset* s = seqset_create(ctx, rdata.data(), roff.data(), (uint32_t)reps.size());
+    try {
+        const NwScheme sc = make_scheme(table, has, osur, gap_extend);
+        std::vector<dm_node> nodes;
+        std::vector<uint32_t> order;
+        dm_stats ts{}, as{};
+        build_tree(ctx, s, seed, 100, nodes, order, st ? &ts : nullptr);
+        res.msa.reset(align_all(ctx, s, nodes, order, sc, st ? &as : nullptr));
+        // re-expand duplicates (pipeline.cpp:130-146): output slot -> (input record, MSA row)
+        res.slot_input.assign(n, 0);
+        res.slot_row.assign(n, 0);
+        uint64_t slot = 0;
+        for (size_t r = 0; r < res.msa->row_seq.size(); ++r) {
+            const uint32_t rep = res.msa->row_seq[r];
+            const auto place = [&](uint32_t orig) {
+                const uint64_t at = input_order ? orig : slot++;
+                res.slot_input[at] = orig;
+                res.slot_row[at] = (uint32_t)r;
+            };
+            place(reps[rep]);
+            for (uint32_t d : dups[rep]) place(d);
+        }
+        res.summary.input_count = n;
+        res.summary.unique_count = reps.size();
+        res.summary.duplicate_count = n - reps.size();
+        uint32_t depth = 0;
+        for (const auto& nd : nodes) depth = std::max(depth, nd.depth);
+        res.summary.tree_depth = depth;
+        res.summary.width = res.msa->width;
+        res.summary.alphabet = kind;
+        res.summary.elapsed_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (st) {
+            std::memset(st, 0, sizeof(*st));
+            st->cells = ts.cells + as.cells;
+            st->cells_executed = ts.cells_executed + as.cells;
+            st->kernel_ms = ts.kernel_ms + as.kernel_ms;
+            st->launches = ts.launches + as.launches;
+            st->nw_calls = as.nw_calls;
+        }
+    } catch (...) {
+        delete s;
+        throw;
+    }
+    delete s;
+    return res;
+}
+
+}  // namespace dm
 
 extern "C" {
 
@@ -46,119 +173,15 @@ int dm_align_sequences(dm_ctx* ctx, const char* data, const uint64_t* offsets, u
                        uint64_t* width_out, dm_align_summary* summary, dm_stats* st) {
     return dm::guard([&] {
         dm::require(ctx && offsets && rows_out && width_out, "null argument");
-        const auto t0 = std::chrono::steady_clock::now();
-        if (n == 0) throw dm::runtime_error("no sequences to align");
-        if (gap_open > gap_extend || gap_extend > 0)
-            throw dm::invalid_argument("gap penalties must satisfy gap_open <= gap_extend <= 0");
-        const uint64_t base = offsets[0];
-        const int kind = alphabet == 1 ? 0 : alphabet == 2 ? 1 : detect_alphabet(data + base, offsets[n] - base);
-        auto rec = [](uint32_t i) { return "record 'seq" + std::to_string(i) + "'"; };
-        if (!custom_table) {
-            bool member[256] = {};
-            for (char c : (kind == 0 ? kNucleotide : kProtein)) member[(unsigned char)c] = true;
-            for (uint32_t i = 0; i < n; ++i)
-                for (uint64_t p = offsets[i]; p < offsets[i + 1]; ++p) {
-                    const char c = data[p];
-                    if (c == '-') throw dm::runtime_error(rec(i) + " contains gap symbol '-' in unaligned input");
-                    if (!member[(unsigned char)c])
-                        throw dm::runtime_error(rec(i) + " contains character '" + std::string(1, c) +
-                                                "' outside the " + (kind == 0 ? "nucleotide" : "protein") +
-                                                " alphabet");
-                }
-        }
-        int16_t table[128 * 128];
-        uint8_t has[128];
-        int osur = 0;
-        if (custom_table) {
-            std::memcpy(table, custom_table, sizeof(table));
-            std::memcpy(has, custom_has, sizeof(has));
-            osur = flat ? 0 : gap_open;
-        } else {
-            const int rc = dm_scheme_default(kind, gap_open, gap_extend, flat, table, has, &osur);
-            if (rc != DM_OK) throw dm::invalid_argument(dm::last_error());
-        }
-        for (uint32_t i = 0; i < n; ++i)
-            for (uint64_t p = offsets[i]; p < offsets[i + 1]; ++p) {
-                const unsigned char c = (unsigned char)data[p];
-                if (c >= 128 || !has[c])
-                    throw dm::runtime_error(rec(i) + " contains character '" + std::string(1, (char)c) +
-                                            "' that the substitution matrix does not score");
-            }
-        // deduplicate: first occurrences in order (seq_io.cpp:168-186)
-        std::unordered_map<std::string_view, uint32_t> first;
-        first.reserve(n * 2);
-        std::vector<uint32_t> reps;
-        std::vector<std::vector<uint32_t>> dups;
-        for (uint32_t i = 0; i < n; ++i) {
-            std::string_view sv(data + offsets[i], offsets[i + 1] - offsets[i]);
-            auto it = first.find(sv);
-            if (it == first.end()) {
-                first.emplace(sv, (uint32_t)reps.size());
-                reps.push_back(i);
-                dups.emplace_back();
-            } else {
-                dups[it->second].push_back(i);
-            }
-        }
-        std::vector<uint64_t> roff(reps.size() + 1);
-        std::string rdata;
-        uint64_t tot = 0;
-        for (size_t r = 0; r < reps.size(); ++r) tot += offsets[reps[r] + 1] - offsets[reps[r]];
-        rdata.reserve(tot);
-        for (size_t r = 0; r < reps.size(); ++r) {
-            roff[r] = rdata.size();
-            rdata.append(data + offsets[reps[r]], offsets[reps[r] + 1] - offsets[reps[r]]);
-        }
-        roff[reps.size()] = rdata.size();
-        dm_seqset* s = dm::seqset_create(ctx, rdata.data(), roff.data(), (uint32_t)reps.size());
-        dm_msa_out* m = nullptr;
-        try {
-            const dm::NwScheme sc = dm::make_scheme(table, has, osur, gap_extend);
-            std::vector<dm_node> nodes;
-            std::vector<uint32_t> order;
-            dm_stats ts{}, as{};
-            dm::build_tree(ctx, s, seed, 100, nodes, order, st ? &ts : nullptr);
-            m = dm::align_all(ctx, s, nodes, order, sc, st ? &as : nullptr);
-            const uint64_t W = m->width;
-            char* out = (char*)std::malloc(std::max<uint64_t>((uint64_t)n * W, 1));
-            if (!out) throw std::bad_alloc();
-            uint64_t slot = 0;
-            for (size_t r = 0; r < m->row_seq.size(); ++r) {
-                const uint32_t rep = m->row_seq[r];
-                const char* row = m->rows.data() + r * W;
-                const uint32_t orig = reps[rep];
-                std::memcpy(out + (input_order ? orig : slot++) * W, row, W);
-                for (uint32_t d : dups[rep]) std::memcpy(out + (input_order ? d : slot++) * W, row, W);
-            }
-            *rows_out = out;
-            *width_out = W;
-            if (summary) {
-                summary->input_count = n;
-                summary->unique_count = reps.size();
-                summary->duplicate_count = n - reps.size();
-                uint32_t depth = 0;
-                for (const auto& nd : nodes) depth = std::max(depth, nd.depth);
-                summary->tree_depth = depth;
-                summary->width = W;
-                summary->alphabet = kind;
-                summary->elapsed_s =
-                    std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-            }
-            if (st) {
-                std::memset(st, 0, sizeof(*st));
-                st->cells = ts.cells + as.cells;
-                st->cells_executed = ts.cells_executed + as.cells;
-                st->kernel_ms = ts.kernel_ms + as.kernel_ms;
-                st->launches = ts.launches + as.launches;
-                st->nw_calls = as.nw_calls;
-            }
-        } catch (...) {
-            delete m;
-            delete s;
-            throw;
-        }
-        delete m;
-        delete s;
+        dm::AlignCore res = dm::align_core(ctx, data, offsets, n, nullptr, alphabet, gap_open, gap_extend, flat,
+                                           custom_table, custom_has, seed, input_order, st);
+        const uint64_t W = res.msa->width;
+        char* out = (char*)std::malloc(std::max<uint64_t>((uint64_t)n * W, 1));
+        if (!out) throw std::bad_alloc();
+        for (uint32_t k = 0; k < n; ++k) std::memcpy(out + (uint64_t)k * W, res.msa->rows.data() + (uint64_t)res.slot_row[k] * W, W);
+        *rows_out = out;
+        *width_out = W;
+        if (summary) *summary = res.summary;
     });
 }
 
