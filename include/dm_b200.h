@@ -224,11 +224,18 @@ int dm_align_sequences(dm_ctx* ctx, const char* data, const uint64_t* offsets, u
  * 1/2 = validate while parsing), align_sequences (record ids in errors),
  * write the aligned FASTA (80-column lines, formatted on the device) to
  * "<output_path>.partial" and rename it into place. input_order: 1 rows in
- * input order, 0 tree order (RowOrder::Tree, the CLI default). Errors:
+ * input order, 0 tree order (RowOrder::Tree, the CLI default); non-empty
+ * dump paths write the tree NDJSON / the duplicates TSV (RunConfig dump_*).
+ * Errors:
  * DM_ERUNTIME with the reference's messages ("<file>:<line>: ..."). */
 int dm_run_align(dm_ctx* ctx, const char* input_path, const char* output_path, int alphabet, int gap_open,
                  int gap_extend, int flat, const int16_t* custom_table, const uint8_t* custom_has, uint64_t seed,
-                 int input_order, dm_align_summary* summary, dm_stats* st);
+                 int input_order, const char* dump_tree_path, const char* dump_dedup_path,
+                 dm_align_summary* summary, dm_stats* st);
+/* divmsa::dump_tree (cluster_tree.cpp:253-280): NDJSON, one line per node;
+ * ids[node.center] names the center. Host I/O. */
+int dm_dump_tree(const dm_node* nodes, uint64_t nnodes, const char* ids, const uint64_t* id_off, uint64_t nids,
+                 const char* path);
 /* divmsa::write_fasta over n records given as packed (data, offsets[n+1])
  * id / description / residue arrays; the text is assembled on the device. */
 int dm_write_fasta(dm_ctx* ctx, const char* path, const char* ids, const uint64_t* id_off, const char* descs,

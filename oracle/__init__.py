@@ -253,7 +253,7 @@ class Reference:
         L.ref_hamming_aligned.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64, _u32p]
         L.ref_run_align.restype = C.c_int
         L.ref_run_align.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64,
-                                    C.c_int, C.c_int]
+                                    C.c_int, C.c_int, C.c_char_p, C.c_char_p]
         L.ref_write_fasta.restype = C.c_int
         L.ref_write_fasta.argtypes = [C.c_char_p, C.c_char_p, _u64p, C.c_char_p, _u64p, C.c_char_p, _u64p,
                                       C.c_uint64]
@@ -387,11 +387,13 @@ class Reference:
 
     def run_align(self, input_path: str, output_path: str, alphabet: str = "auto", gap_open: int = -10,
                   gap_extend: int = -1, flat: bool = False, seed: int = 42, order: str = "tree",
-                  threads: int = 0) -> None:
+                  threads: int = 0, dump_tree: str | None = None, dump_dedup: str | None = None) -> None:
         """divmsa::run_align (pipeline.cpp:160-187): FASTA in, aligned FASTA out."""
         a = {"auto": 0, "nt": 1, "aa": 2}[alphabet]
         self._check(self.L.ref_run_align(input_path.encode(), output_path.encode(), a, gap_open, gap_extend,
-                                         int(flat), seed, int(order == "input"), threads or os.cpu_count() or 1))
+                                         int(flat), seed, int(order == "input"), threads or os.cpu_count() or 1,
+                                         dump_tree.encode() if dump_tree else None,
+                                         dump_dedup.encode() if dump_dedup else None))
 
     def write_fasta(self, records, path: str) -> None:
         """divmsa::write_fasta over [(id, description, residues), ...]."""

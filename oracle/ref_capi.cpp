@@ -385,7 +385,8 @@ int ref_distortion_pair(const char* a, std::uint64_t na, const char* b, std::uin
 
 
 int ref_run_align(const char* input, const char* output, int alphabet, int gap_open, int gap_extend, int flat,
-                  std::uint64_t seed, int input_order, int threads) {
+                  std::uint64_t seed, int input_order, int threads, const char* dump_tree,
+                  const char* dump_dedup) {
     try {
         divmsa::RunConfig c;
         c.alphabet = alphabet == 1   ? divmsa::AlphabetChoice::Nucleotide
@@ -397,6 +398,8 @@ int ref_run_align(const char* input, const char* output, int alphabet, int gap_o
         c.seed = seed;
         c.threads = threads > 0 ? (unsigned)threads : 0u;
         c.order = input_order ? divmsa::RowOrder::Input : divmsa::RowOrder::Tree;
+        if (dump_tree) c.dump_tree_path = dump_tree;
+        if (dump_dedup) c.dump_dedup_path = dump_dedup;
         divmsa::run_align(c, input, output);
         return 0;
     } catch (const std::invalid_argument& e) {

@@ -525,7 +525,7 @@ def distortion_pair(a_aligned, b_aligned, a_raw, b_raw, ctx: Context | None = No
 
 def run_align(input_path, output_path, alphabet: str = "auto", gap_open: int = -10, gap_extend: int = -1,
               gap_mode: str = "affine", seed: int = 42, order: str = "tree", scheme: ScoringScheme | None = None,
-              ctx: Context | None = None, stats: bool = False):
+              dump_tree=None, dump_dedup=None, ctx: Context | None = None, stats: bool = False):
     """divmsa::run_align (pipeline.cpp:160-187): parse the FASTA file, align
     (tree + merges on the GPU), write the aligned FASTA (assembled on the GPU)
     to output_path via a ".partial" sibling. Returns the AlignSummary fields."""
@@ -541,9 +541,20 @@ def run_align(input_path, output_path, alphabet: str = "auto", gap_open: int = -
                              {"auto": 0, "nt": 1, "aa": 2}[alphabet], gap_open, gap_extend, int(_flat(gap_mode)),
                              None if scheme is None else _ptr(scheme.table, C.c_int16),
                              None if scheme is None else _ptr(scheme.has_symbol, C.c_uint8), int(seed),
-                             int(order == "input"), C.byref(summ), C.byref(s)))
+                             int(order == "input"), str(dump_tree).encode() if dump_tree else None,
+                             str(dump_dedup).encode() if dump_dedup else None, C.byref(summ), C.byref(s)))
     out = {f: getattr(summ, f) for f, _ in summ._fields_}
     return (out, s.as_dict()) if stats else out
+
+
+def dump_tree(nodes, ids, path) -> None:
+    """divmsa::dump_tree (cluster_tree.cpp:253-280): NDJSON, one line per node
+    (`nodes` as returned by build_tree, `ids` indexed by sequence)."""
+    arr = nodes if isinstance(nodes, np.ndarray) else np.asarray(nodes)
+    nn = len(arr)
+    cn = array_to_nodes(arr)
+    data, offs = _pack(ids)
+    check(lib().dm_dump_tree(cn, nn, data, _ptr(offs, C.c_uint64), len(ids), str(path).encode()))
 
 
 def write_fasta(records, path, ctx: Context | None = None) -> None:

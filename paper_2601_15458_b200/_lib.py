@@ -116,7 +116,8 @@ SIGNATURES = {
     "dm_gap_percent": (C.c_int, [_P, C.c_char_p, C.c_uint64, C.c_uint64, C.POINTER(C.c_double)]),
     "dm_row_pair_stats": (C.c_int, [_P, C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64, _u32p, _u32p, _u32p]),
     "dm_run_align": (C.c_int, [_P, C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, _i16p, _u8p,
-                               C.c_uint64, C.c_int, _P, C.POINTER(dm_stats)]),
+                               C.c_uint64, C.c_int, C.c_char_p, C.c_char_p, _P, C.POINTER(dm_stats)]),
+    "dm_dump_tree": (C.c_int, [C.POINTER(dm_node), C.c_uint64, C.c_char_p, _u64p, C.c_uint64, C.c_char_p]),
     "dm_write_fasta": (C.c_int, [_P, C.c_char_p, C.c_char_p, _u64p, C.c_char_p, _u64p, C.c_char_p, _u64p,
                                  C.c_uint64]),
     "dm_parse_fasta": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_void_p), C.POINTER(_u64p),

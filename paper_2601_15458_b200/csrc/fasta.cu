@@ -200,6 +200,59 @@ void write_atomically(const std::string& path, const std::string& text) {
     }
 }
 
+// nlohmann::json::dump() of a string (ensure_ascii = false): '"' '\\' and
+// the named control escapes, other bytes < 0x20 as \u00xx, the rest verbatim.
+void json_string(std::string& o, std::string_view s) {
+    static const char* hex = "0123456789abcdef";
+    o.push_back('"');
+    for (unsigned char c : s) {
+        switch (c) {
+            case '"': o += "\\\""; break;
+            case '\\': o += "\\\\"; break;
+            case '\b': o += "\\b"; break;
+            case '\f': o += "\\f"; break;
+            case '\n': o += "\\n"; break;
+            case '\r': o += "\\r"; break;
+            case '\t': o += "\\t"; break;
+            default:
+                if (c < 0x20) {
+                    o += "\\u00";
+                    o.push_back(hex[c >> 4]);
+                    o.push_back(hex[c & 15]);
+                } else {
+                    o.push_back((char)c);
+                }
+        }
+    }
+    o.push_back('"');
+}
+
+// dump_tree (cluster_tree.cpp:253-270): one JSON object per node, keys in
+// nlohmann's (sorted) order.
+std::string tree_ndjson(const dm_node* nodes, uint64_t nn, const std::vector<std::string>& center_ids) {
+    std::string o;
+    o.reserve(nn * 96);
+    for (uint64_t i = 0; i < nn; ++i) {
+        const dm_node& nd = nodes[i];
+        o += "{\"cardinality\":" + std::to_string(nd.end - nd.begin) + ",\"center\":";
+        json_string(o, center_ids[nd.center]);
+        o += ",\"depth\":" + std::to_string(nd.depth) + ",\"node\":" + std::to_string(i) + ",\"parent\":" +
+             (nd.parent < 0 ? std::string("null") : std::to_string(nd.parent)) +
+             ",\"radius\":" + std::to_string(nd.radius) + "}\n";
+    }
+    return o;
+}
+
+void write_plain(const std::string& path, const std::string& text, const std::string& open_msg,
+                 const std::string& io_msg) {
+    FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw runtime_error(open_msg);
+    const size_t w = text.empty() ? 0 : std::fwrite(text.data(), 1, text.size(), f);
+    const bool ok = w == text.size() && std::fflush(f) == 0;
+    std::fclose(f);
+    if (!ok) throw runtime_error(io_msg);
+}
+
 }  // namespace
 }  // namespace dm
 
@@ -207,7 +260,8 @@ extern "C" {
 
 int dm_run_align(dm_ctx* ctx, const char* input_path, const char* output_path, int alphabet, int gap_open,
                  int gap_extend, int flat, const int16_t* custom_table, const uint8_t* custom_has, uint64_t seed,
-                 int input_order, dm_align_summary* summary, dm_stats* st) {
+                 int input_order, const char* dump_tree_path, const char* dump_dedup_path,
+                 dm_align_summary* summary, dm_stats* st) {
     return dm::guard([&] {
         dm::require(ctx && input_path && output_path, "null argument");
         const std::string in(input_path);
@@ -226,6 +280,20 @@ int dm_run_align(dm_ctx* ctx, const char* input_path, const char* output_path, i
         dm::AlignCore res = dm::align_core(ctx, data.data(), off.data(), (uint32_t)recs.size(), &ids, alphabet,
                                            gap_open, gap_extend, flat, custom_table, custom_has, seed, input_order,
                                            st);
+        if (dump_dedup_path && *dump_dedup_path) {  // write_dedup_tsv (seq_io.cpp:227-249)
+            std::string tsv;
+            for (size_t r = 0; r < res.reps.size(); ++r)
+                for (uint32_t d : res.dups[r]) tsv += recs[res.reps[r]].id + '\t' + recs[d].id + '\n';
+            const std::string p(dump_dedup_path);
+            dm::write_plain(p, tsv, "cannot open " + p + " for writing", "I/O error while writing " + p);
+        }
+        if (dump_tree_path && *dump_tree_path) {  // dump_tree (cluster_tree.cpp:253-280), leaf ids = representatives
+            std::vector<std::string> rep_ids(res.reps.size());
+            for (size_t r = 0; r < res.reps.size(); ++r) rep_ids[r] = recs[res.reps[r]].id;
+            const std::string p(dump_tree_path);
+            dm::write_plain(p, dm::tree_ndjson(res.msa->nodes.data(), res.msa->nodes.size(), rep_ids),
+                            "cannot open tree dump file: " + p, "failed writing tree dump: " + p);
+        }
         const uint64_t n = recs.size(), W = res.msa->width;
         std::vector<std::string> headers(n);
         std::vector<uint64_t> src(n);
@@ -239,6 +307,20 @@ int dm_run_align(dm_ctx* ctx, const char* input_path, const char* output_path, i
             dm::format_on_device(ctx, (const uint8_t*)ctx->rows_a.p, headers, src, len);
         dm::write_atomically(output_path, text);
         if (summary) *summary = res.summary;  // elapsed_s covers align_sequences, as in the reference
+    });
+}
+
+int dm_dump_tree(const dm_node* nodes, uint64_t nnodes, const char* ids, const uint64_t* id_off, uint64_t nids,
+                 const char* path) {
+    return dm::guard([&] {
+        dm::require(nodes && id_off && path, "null argument");
+        std::vector<std::string> v(nids);
+        for (uint64_t k = 0; k < nids; ++k) v[k] = std::string(ids + id_off[k], id_off[k + 1] - id_off[k]);
+        for (uint64_t i = 0; i < nnodes; ++i)
+            if (nodes[i].center >= nids) throw dm::invalid_argument("node center outside the id list");
+        const std::string p(path);
+        dm::write_plain(p, dm::tree_ndjson(nodes, nnodes, v), "cannot open tree dump file: " + p,
+                        "failed writing tree dump: " + p);
     });
 }
 

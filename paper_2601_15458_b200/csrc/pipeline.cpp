@@ -116,6 +116,8 @@ AlignCore align_core(dm_ctx* ctx, const char* data, const uint64_t* offsets, uin
         rdata.append(data + offsets[reps[r]], offsets[reps[r] + 1] - offsets[reps[r]]);
     }
     roff[reps.size()] = rdata.size();
+    res.reps = reps;
+    res.dups = dups;
     dm_seqset* s = seqset_create(ctx, rdata.data(), roff.data(), (uint32_t)reps.size());
     try {
         const NwScheme sc = make_scheme(table, has, osur, gap_extend);

@@ -15,6 +15,8 @@ struct AlignCore {
     std::vector<uint32_t> slot_input;  // output slot -> input record index
     std::vector<uint32_t> slot_row;    // output slot -> MSA row (duplicates share their representative's)
     dm_align_summary summary{};
+    std::vector<uint32_t> reps;               // input index of each distinct sequence (tree leaf ids)
+    std::vector<std::vector<uint32_t>> dups;  // input indices collapsed onto each representative
 };
 
 AlignCore align_core(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint32_t n,

@@ -135,3 +135,29 @@ def test_parse_fasta_round_trip(dm, tmp_path):
     assert dm.parse_fasta(src, allow_gaps=True) == [("x", "two  words ", "ACGTAC"), ("y", "", "A-C")]
     with pytest.raises(RuntimeError, match="gap symbol"):
         dm.parse_fasta(src)
+
+
+def test_run_align_dumps_match_reference(dm, ctx, ref, tmp_path):
+    """RunConfig dump_tree_path / dump_dedup_path: the tree NDJSON
+    (cluster_tree.cpp:253-280, nlohmann key order and escaping) and the
+    duplicates TSV (seq_io.cpp:227-249) byte-identical to the reference."""
+    rng = random.Random(8)
+    text = family_fasta(rng, 60, 120, dup_every=4)
+    text += '>we"ird\\id\tx\nACGTACGTAAC\n>ctl\x01id\nACGTTCGTAAC\n'
+    src = write(tmp_path / "in.fa", text)
+    dm.run_align(src, tmp_path / "g.fa", dump_tree=tmp_path / "g.tree", dump_dedup=tmp_path / "g.tsv", ctx=ctx)
+    ref.run_align(src, str(tmp_path / "r.fa"), dump_tree=str(tmp_path / "r.tree"), dump_dedup=str(tmp_path / "r.tsv"))
+    for ext in ("fa", "tree", "tsv"):
+        assert open(tmp_path / f"g.{ext}", "rb").read() == open(tmp_path / f"r.{ext}", "rb").read(), ext
+    assert open(tmp_path / "g.tsv").read().count("\n") > 5
+
+
+def test_dump_tree_api(dm, ctx, tmp_path):
+    import json
+    seqs = ["ACGTACGT", "ACGTTCGT", "TTTTACGA", "ACGAACGT", "GGGTACGT"]
+    nodes, order = dm.build_tree(dm.SeqSet(seqs, ctx))
+    dm.dump_tree(nodes, [f"s{i}" for i in range(len(seqs))], tmp_path / "t.ndjson")
+    lines = [json.loads(x) for x in open(tmp_path / "t.ndjson")]
+    assert len(lines) == 2 * len(seqs) - 1
+    assert lines[0]["parent"] is None and lines[0]["cardinality"] == len(seqs) and lines[0]["node"] == 0
+    assert list(lines[0]) == ["cardinality", "center", "depth", "node", "parent", "radius"]
