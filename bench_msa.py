@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--scale4", type=float, default=0.1)
     ap.add_argument("--repeat", type=int, default=2)
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--files", action="store_true",
+                    help="also time FASTA-to-FASTA (dm.run_align on a FASTA file) and dm.evaluate")
     ap.add_argument("--simulate-world", type=int, default=1,
                     help="run the sharded path with k shards on one GPU (checks, not a speed number)")
     args = ap.parse_args()
@@ -87,6 +89,24 @@ def main():
                 "reference_cpu_s": (golden[key]["tree_s"] + golden[key]["align_s"]) if key in golden else None,
                 "reference_threads": golden[key]["threads"] if key in golden else None,
                 "n_gpus": world, "simulated_world": args.simulate_world}
+        if args.files and world == 1:
+            # FASTA file in -> aligned FASTA file out, and the quality metrics
+            import tempfile
+            with tempfile.TemporaryDirectory() as d:
+                src = os.path.join(d, "in.fa")
+                with open(src, "w") as f:
+                    for i, s in enumerate(dm.split(data, offs)):
+                        f.write(f">s{i}\n{s.decode()}\n")
+                kind = "aa" if cfg == 3 else "nt"
+                dm.run_align(src, os.path.join(d, "out.fa"), alphabet=kind, ctx=ctx)  # warm
+                t0 = time.perf_counter()
+                dm.run_align(src, os.path.join(d, "out.fa"), alphabet=kind, ctx=ctx)
+                line["fasta_to_fasta_s"] = time.perf_counter() - t0
+                line["fasta_out_bytes"] = os.path.getsize(os.path.join(d, "out.fa"))
+            t0 = time.perf_counter()
+            rep = dm.evaluate(m, seqs, ctx=ctx)
+            line["evaluate_s"] = time.perf_counter() - t0
+            line["evaluate"] = {k: rep[k] for k in ("pair_count", "p_avg", "distortion", "gap_percent")}
         print(json.dumps(line), flush=True)
     if world > 1:
         tdist.destroy_process_group()
