@@ -54,3 +54,37 @@ def test_attach_single_rank(dm):
     c = dm.Context(0)
     attach(c, 0, 1, nccl_unique_id())  # world 1: no communicator, plain path
     assert dm.levenshtein("KITTEN", "SITTING", c) == 3
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_run_align_gpu_count_independent(dm, ctx, tmp_path, world):
+    """test_pipeline.cpp:236-255 (byte-identical FASTA at 1/2/8 threads),
+    here across simulated GPU counts, with duplicates and tree order."""
+    from paper_2601_15458_b200.dist import simulate_world
+    data, offs = dm.synth(0, scale=0.3)
+    seqs = [s.decode() for s in dm.split(data, offs)]
+    seqs += seqs[:25]  # duplicates re-expanded on every rank
+    src = tmp_path / "in.fa"
+    src.write_text("".join(f">s{i}\n{s}\n" for i, s in enumerate(seqs)))
+    dm.run_align(src, tmp_path / "w1.fa", dump_tree=tmp_path / "w1.tree", ctx=ctx)
+    c2 = dm.Context(0)
+    simulate_world(c2, world)
+    dm.run_align(src, tmp_path / "wk.fa", dump_tree=tmp_path / "wk.tree", ctx=c2)
+    assert (tmp_path / "w1.fa").read_bytes() == (tmp_path / "wk.fa").read_bytes()
+    assert (tmp_path / "w1.tree").read_bytes() == (tmp_path / "wk.tree").read_bytes()
+
+
+def test_repeat_determinism_2000(dm, ctx):
+    """acceptance.cpp:361-409 (#8): 2,000 sequences aligned twice -> identical."""
+    rng = random.Random(1008)
+    anc = [("".join(rng.choice("ACGT") for _ in range(150))) for _ in range(10)]
+    seqs = []
+    for k in range(2000):
+        s = list(anc[k % 10])
+        for _ in range(12):
+            s[rng.randrange(len(s))] = rng.choice("ACGT")
+        seqs.append("".join(s))
+    seqs = unique(seqs)
+    a = dm.align(seqs, ctx=ctx)
+    b = dm.align(seqs, ctx=ctx)
+    assert a == b
