@@ -4,6 +4,7 @@
 #include <string>
 
 #include "capi_guard.h"
+#include "host_par.h"
 #include "nw.h"
 
 // One batch of PairwiseResults (pairwise.hpp:78-84).
@@ -46,12 +47,13 @@ std::string with_gaps(const char* s, uint64_t n, const std::vector<uint32_t>& as
 
 void run_batch(dm_ctx* ctx, const char* A, const uint64_t* a_off, const char* B, const uint64_t* b_off,
                uint32_t njobs, const dm::NwScheme& sc, dm_pw* pw, dm_stats* st) {
-    for (uint32_t k = 0; k < njobs; ++k) {
-        const uint64_t na = a_off[k + 1] - a_off[k], nb = b_off[k + 1] - b_off[k];
-        if (na == 0 || nb == 0) throw dm::invalid_argument("nw_align requires non-empty inputs");
-        check_symbols(A + a_off[k], na, sc, "a");
-        check_symbols(B + b_off[k], nb, sc, "b");
-    }
+    for (uint32_t k = 0; k < njobs; ++k)
+        if (a_off[k + 1] == a_off[k] || b_off[k + 1] == b_off[k])
+            throw dm::invalid_argument("nw_align requires non-empty inputs");
+    dm::host_parallel_for(njobs, 256, [&](uint64_t k) {
+        check_symbols(A + a_off[k], a_off[k + 1] - a_off[k], sc, "a");
+        check_symbols(B + b_off[k], b_off[k + 1] - b_off[k], sc, "b");
+    });
     const uint64_t abytes = a_off[njobs] - a_off[0], bbytes = b_off[njobs] - b_off[0];
     uint8_t* d_in = (uint8_t*)ctx->rows_b.get(abytes + bbytes + 16);
     if (abytes) DM_CUDA(cudaMemcpyAsync(d_in, A + a_off[0], abytes, cudaMemcpyHostToDevice, ctx->stream));
@@ -66,23 +68,25 @@ void run_batch(dm_ctx* ctx, const char* A, const uint64_t* a_off, const char* B,
     dm::NwOut no;
     dm::nw_run(ctx, d_in, jobs, sc, no, st != nullptr);
     std::vector<dm::NwRes> res(njobs);
-    std::vector<uint32_t> gaps(no.gaps_total);
     if (njobs)
         DM_CUDA(cudaMemcpyAsync(res.data(), no.d_res, njobs * sizeof(dm::NwRes), cudaMemcpyDeviceToHost, ctx->stream));
-    if (no.gaps_total)
-        DM_CUDA(cudaMemcpyAsync(gaps.data(), no.d_gaps, no.gaps_total * 4, cudaMemcpyDeviceToHost, ctx->stream));
     DM_CUDA(cudaStreamSynchronize(ctx->stream));
+    // only the nga + ngb used entries of each job's gap capacity come back
+    std::vector<uint32_t> gaps;
+    std::vector<uint64_t> goff;
+    dm::nw_compact_gaps(ctx, no.d_gaps, jobs, res, gaps, goff);
     pw->r.resize(njobs);
-    for (uint32_t k = 0; k < njobs; ++k) {
+    dm::host_parallel_for(njobs, 64, [&](uint64_t k) {
         auto& o = pw->r[k];
         o.score = res[k].score;
-        o.gaps_a.assign(gaps.begin() + jobs[k].ga_off, gaps.begin() + jobs[k].ga_off + res[k].nga);
-        o.gaps_b.assign(gaps.begin() + jobs[k].gb_off, gaps.begin() + jobs[k].gb_off + res[k].ngb);
+        const uint32_t* g = gaps.data() + goff[k];
+        o.gaps_a.assign(g, g + res[k].nga);
+        o.gaps_b.assign(g + res[k].nga, g + res[k].nga + res[k].ngb);
         std::reverse(o.gaps_a.begin(), o.gaps_a.end());  // pairwise.cpp:410-413
         std::reverse(o.gaps_b.begin(), o.gaps_b.end());
         o.a = with_gaps(A + a_off[k], jobs[k].n, o.gaps_a);
         o.b = with_gaps(B + b_off[k], jobs[k].m, o.gaps_b);
-    }
+    });
     if (st) {
         std::memset(st, 0, sizeof(*st));
         st->kernel_ms = no.fwd_ms + no.tb_ms;

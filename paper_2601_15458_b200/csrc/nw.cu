@@ -305,6 +305,46 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
     }
 }
 
+namespace {
+struct CompactDesc {
+    uint64_t src_a, src_b, dst;
+    uint32_t na, nb;
+};
+__global__ void compact_gaps_kernel(const uint32_t* __restrict__ gaps, const CompactDesc* __restrict__ d, uint64_t n,
+                                    uint32_t* __restrict__ out) {
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t k = warp; k < n; k += nwarps) {
+        const CompactDesc c = d[k];
+        for (uint32_t t = lane; t < c.na; t += 32) out[c.dst + t] = gaps[c.src_a + t];
+        for (uint32_t t = lane; t < c.nb; t += 32) out[c.dst + c.na + t] = gaps[c.src_b + t];
+    }
+}
+}  // namespace
+
+void nw_compact_gaps(dm_ctx* ctx, const uint32_t* d_gaps, const std::vector<NwJob>& jobs,
+                     const std::vector<NwRes>& res, std::vector<uint32_t>& out, std::vector<uint64_t>& off) {
+    const uint64_t n = jobs.size();
+    off.assign(n + 1, 0);
+    std::vector<CompactDesc> desc(n);
+    for (uint64_t k = 0; k < n; ++k) {
+        desc[k] = CompactDesc{jobs[k].ga_off, jobs[k].gb_off, off[k], res[k].nga, res[k].ngb};
+        off[k + 1] = off[k] + res[k].nga + res[k].ngb;
+    }
+    out.resize(off[n]);
+    if (off[n] == 0) return;
+    CompactDesc* d_desc = (CompactDesc*)ctx->aux.get(n * sizeof(CompactDesc));
+    uint32_t* d_out = ctx->aux2.as<uint32_t>(off[n]);
+    DM_CUDA(cudaMemcpyAsync(d_desc, desc.data(), n * sizeof(CompactDesc), cudaMemcpyHostToDevice, ctx->stream));
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((n + 7) / 8, (uint64_t)ctx->sm_count * 16));
+    compact_gaps_kernel<<<grid, 256, 0, ctx->stream>>>(d_gaps, d_desc, n, d_out);
+    DM_CUDA(cudaGetLastError());
+    ++ctx->launches;
+    DM_CUDA(cudaMemcpyAsync(out.data(), d_out, off[n] * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    DM_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
 void nw_run_sharded(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const NwScheme& sc,
                     NwOut& out, bool time_kernels) {
     const int w = shard_world(ctx);

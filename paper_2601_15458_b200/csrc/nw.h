@@ -62,4 +62,9 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
 void nw_run_sharded(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const NwScheme& sc,
                     NwOut& out, bool time_kernels);
 
+// Gathers each job's nga + ngb gap entries (path order, gaps_into_a first)
+// into one compact host array; off[k] = start of job k's entries.
+void nw_compact_gaps(dm_ctx* ctx, const uint32_t* d_gaps, const std::vector<NwJob>& jobs,
+                     const std::vector<NwRes>& res, std::vector<uint32_t>& out, std::vector<uint64_t>& off);
+
 }  // namespace dm
