@@ -171,15 +171,26 @@ NODE_FIELDS = ("begin", "end", "center", "radius", "pole_l", "pole_r", "left", "
 NO_SEQUENCE = 0xFFFFFFFF  # cluster_tree.hpp:15 kNoSequence
 
 
+_SIGNED = [NODE_FIELDS.index(f) for f in ("left", "right", "parent")]
+
+
 def nodes_to_array(nodes, count: int) -> np.ndarray:
-    return np.array([[getattr(nodes[i], f) for f in NODE_FIELDS] for i in range(count)], dtype=np.int64)
+    """dm_node[count] (ten 32-bit fields) -> int64 [count, 10] in NODE_FIELDS order."""
+    if count == 0:
+        return np.zeros((0, len(NODE_FIELDS)), dtype=np.int64)
+    raw = np.ctypeslib.as_array(C.cast(nodes, C.POINTER(C.c_uint32)), shape=(count * len(NODE_FIELDS),))
+    u = raw.reshape(count, len(NODE_FIELDS))
+    out = u.astype(np.int64)
+    out[:, _SIGNED] = u[:, _SIGNED].view(np.int32)
+    return out
 
 
 def array_to_nodes(arr: np.ndarray):
-    out = (dm_node * len(arr))()
-    for i, row in enumerate(np.asarray(arr, dtype=np.int64)):
-        for f, v in zip(NODE_FIELDS, row):
-            setattr(out[i], f, int(v))
+    a = np.asarray(arr, dtype=np.int64).reshape(-1, len(NODE_FIELDS))
+    out = (dm_node * max(len(a), 1))()
+    if len(a):
+        u = np.ascontiguousarray(a.astype(np.uint32))  # keep alive across the copy
+        C.memmove(out, u.ctypes.data, u.nbytes)
     return out
 
 
@@ -377,16 +388,16 @@ class Msa:
 def _msa_from(h) -> Msa:
     L = lib()
     W, R = L.dm_msa_width(h), L.dm_msa_rows(h)
-    buf = C.create_string_buffer(max(W * R, 1))
-    L.dm_msa_copy_rows(h, buf)
+    buf = bytearray(max(W * R, 1))
+    L.dm_msa_copy_rows(h, (C.c_char * len(buf)).from_buffer(buf))
     rs = np.zeros(max(R, 1), dtype=np.uint32)
     L.dm_msa_copy_row_seq(h, _ptr(rs))
     nn = L.dm_msa_nnodes(h)
     nodes = (dm_node * max(nn, 1))()
     order = np.zeros(max(R, 1), dtype=np.uint32)
     L.dm_msa_copy_tree(h, nodes, _ptr(order))
-    raw = buf.raw
-    return Msa([raw[r * W:(r + 1) * W].decode("latin-1") for r in range(R)], rs[:R].copy(), int(W),
+    text = buf.decode("latin-1") if W * R else ""  # one decode, then str slices
+    return Msa([text[r * W:(r + 1) * W] for r in range(R)], rs[:R].copy(), int(W),
                nodes_to_array(nodes, nn), order[:R].copy())
 
 
@@ -449,7 +460,8 @@ def align(sequences: Sequence, alphabet: str = "auto", gap_open: int = -10, gap_
         raw = C.string_at(rows, W * (len(offs) - 1))
     finally:
         lib().dm_free(rows)
-    out = [raw[r * W:(r + 1) * W].decode("latin-1") for r in range(len(offs) - 1)]
+    text = raw.decode("latin-1")
+    out = [text[r * W:(r + 1) * W] for r in range(len(offs) - 1)]
     if summary:
         return out, {f: getattr(summ, f) for f, _ in summ._fields_}, s.as_dict()
     return out

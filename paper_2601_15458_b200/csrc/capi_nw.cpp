@@ -45,6 +45,33 @@ std::string with_gaps(const char* s, uint64_t n, const std::vector<uint32_t>& as
     return out;
 }
 
+// A caller-supplied ClusterTree must be a well-formed divisive tree over
+// `order` (cluster_tree.hpp:20-45) before the merge scheduler indexes with it.
+void validate_tree(const std::vector<dm_node>& nodes, const std::vector<uint32_t>& order, uint32_t n) {
+    auto bad = [](const char* why) { throw dm::invalid_argument(std::string("invalid cluster tree: ") + why); };
+    if (n == 0 || nodes.size() != 2ull * n - 1) bad("expected 2n-1 nodes");
+    std::vector<uint8_t> seen(n, 0);
+    for (uint32_t v : order) {
+        if (v >= n || seen[v]) bad("order is not a permutation");
+        seen[v] = 1;
+    }
+    if (nodes[0].begin != 0 || nodes[0].end != n) bad("root does not cover every sequence");
+    for (size_t v = 0; v < nodes.size(); ++v) {
+        const dm_node& nd = nodes[v];
+        if (nd.begin >= nd.end || nd.end > n || nd.center >= n) bad("node slice or center out of range");
+        if (nd.left < 0 || nd.right < 0) {
+            if (nd.left != -1 || nd.right != -1 || nd.end - nd.begin != 1) bad("leaf with children or width != 1");
+            continue;
+        }
+        if ((size_t)nd.left >= nodes.size() || (size_t)nd.right >= nodes.size() || (size_t)nd.left <= v ||
+            (size_t)nd.right <= v)
+            bad("child index out of range");
+        const dm_node& l = nodes[nd.left];
+        const dm_node& r = nodes[nd.right];
+        if (l.begin != nd.begin || l.end != r.begin || r.end != nd.end) bad("children do not partition the parent");
+    }
+}
+
 void run_batch(dm_ctx* ctx, const char* A, const uint64_t* a_off, const char* B, const uint64_t* b_off,
                uint32_t njobs, const dm::NwScheme& sc, dm_pw* pw, dm_stats* st) {
     for (uint32_t k = 0; k < njobs; ++k)
@@ -170,6 +197,7 @@ int dm_align_all(dm_ctx* ctx, const dm_seqset* s, const dm_node* nodes, uint64_t
         const dm::NwScheme sc = dm::make_scheme(table, has_symbol, open_surcharge, gap_extend);
         std::vector<dm_node> nv(nodes, nodes + nnodes);
         std::vector<uint32_t> ov(order, order + s->n);
+        validate_tree(nv, ov, s->n);
         if (st) std::memset(st, 0, sizeof(*st));
         cudaEvent_t t0, t1;
         DM_CUDA(cudaEventCreate(&t0));

@@ -165,3 +165,23 @@ def test_align_errors(dm, ctx):
         dm.align(["ACGT", "AC-T"], alphabet="nt", ctx=ctx)
     with pytest.raises(ValueError):
         dm.align(["ACGT"], gap_mode="linear", ctx=ctx)
+
+
+def test_align_all_rejects_malformed_trees(dm, ctx):
+    seqs = ["ACGT", "AGT", "ACCT", "TTGA"]
+    ss = dm.SeqSet(seqs, ctx)
+    nodes, order = dm.build_tree(ss)
+    sc = dm.ScoringScheme.nucleotide()
+    assert len(dm.align_all(ss, nodes, order, sc).rows) == 4
+    bad = nodes.copy()
+    bad[0, dm.NODE_FIELDS.index("left")] = 99
+    with pytest.raises(ValueError, match="invalid cluster tree"):
+        dm.align_all(ss, bad, order, sc)
+    bad = nodes.copy()
+    bad[1, dm.NODE_FIELDS.index("center")] = 17
+    with pytest.raises(ValueError, match="invalid cluster tree"):
+        dm.align_all(ss, bad, order, sc)
+    with pytest.raises(ValueError, match="permutation"):
+        dm.align_all(ss, nodes, [0, 0, 1, 2], sc)
+    with pytest.raises(ValueError, match="2n-1"):
+        dm.align_all(ss, nodes[:5], order, sc)
