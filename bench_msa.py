@@ -7,6 +7,9 @@ GCUPS, and (when tests/golden/msa_configs.json has the config) whether the
 output hashes equal the reference's.
 
     python bench_msa.py --configs 0,3,2 [--scale2 1.0] [--scale4 0.1]
+
+wall_s covers the Python API (rows as str objects); api_wall_s the same job
+through the C ABI (packed bytes in, one host row buffer out).
 """
 import argparse
 import hashlib
@@ -56,6 +59,27 @@ def main():
         seqs = list(dict.fromkeys(s.decode() for s in dm.split(data, offs)))
         sc = dm.ScoringScheme.protein() if cfg == 3 else dm.ScoringScheme.nucleotide()
         best = None
+        api_best = None
+        if world == 1:
+            # the same job through the C ABI only: packed bytes in, the MSA rows
+            # in one host buffer out (no Python str objects)
+            import ctypes as C
+            from paper_2601_15458_b200._lib import check as _check, dm_stats as _st, lib as _lib
+            packed, poffs = dm._pack(seqs)
+            for _ in range(args.repeat):
+                t0 = time.perf_counter()
+                ss = dm.SeqSet(data=packed, offsets=poffs, ctx=ctx)
+                h = C.c_void_p()
+                st_ = _st()
+                _check(_lib().dm_msa(ctx.handle, ss.handle, 42, 100, dm._ptr(sc.table, C.c_int16),
+                                     dm._ptr(sc.has_symbol, C.c_uint8), sc.open_surcharge(), sc.gap_extend(),
+                                     C.byref(h), C.byref(st_)))
+                rows = bytearray(_lib().dm_msa_width(h) * _lib().dm_msa_rows(h))
+                _lib().dm_msa_copy_rows(h, (C.c_char * max(len(rows), 1)).from_buffer(rows) if rows else None)
+                t = time.perf_counter() - t0
+                _lib().dm_msa_free(h)
+                del ss
+                api_best = t if api_best is None else min(api_best, t)
         for _ in range(args.repeat):
             if world > 1:
                 tdist.barrier()
@@ -82,7 +106,7 @@ def main():
                 h.update(r.encode())
                 h.update(b"\n")
             match = h.hexdigest() == golden[key]["rows_sha256"]
-        line = {"config": key, "n": len(seqs), "width": m.width, "wall_s": wall,
+        line = {"config": key, "n": len(seqs), "width": m.width, "wall_s": wall, "api_wall_s": api_best,
                 "tree_ms": st["tree_ms"], "align_ms": st["align_ms"], "cells": st["cells"],
                 "gcups_e2e": st["cells"] / wall / 1e9, "launches": st["launches"], "nw_calls": st["nw_calls"],
                 "reference_match": match,
