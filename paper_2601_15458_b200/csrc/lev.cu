@@ -1,5 +1,5 @@
 // Distance engine: batched exact Levenshtein distance,
-// bit-parallel Myers/Hyyro recurrence over 64-bit blocks, warp-cooperative.
+// bit-parallel Myers/Hyyro recurrence, warp-cooperative.
 //
 // Replaces the two-row DP of distance.cpp:30-47 (called from
 // cluster_tree.cpp:38 and :144-145). The value computed is the same
@@ -8,23 +8,27 @@
 //
 // Layout of one job (pattern p of m residues, text t of n residues):
 //   * the pattern is the SHORTER string (distance is symmetric), cut into
-//     B = ceil(m/64) blocks of 64 rows; a GROUP of G lanes (G | 32) owns the
-//     pattern, lane g holding blocks [g*R, g*R+R) in registers (R is a
-//     template parameter, so the block state never leaves the register file);
+//     B = ceil(m/32) 32-row words; a GROUP of G lanes (G | 32) owns the
+//     pattern, lane g holding words [g*W, g*W+W) in registers as ONE
+//     multi-precision bit-vector (W is a template parameter, so the state
+//     never leaves the register file; carries run through the words of a
+//     lane in one add chain and between lanes as the horizontal delta);
 //   * the group sweeps the text column by column as a diagonal pipeline:
 //     lane g works on column s-g at step s, receiving from lane g-1 (one
-//     __shfl_up per column) the horizontal delta leaving the block above and
-//     the text code of that column. Lane 0 reads the text; the top boundary
-//     is D[0][j] = j, i.e. h_in = +1;
-//   * the match mask of a residue code c is built from NP bit-planes of the
-//     pattern: Eq = AND_k (bit_k(c) ? P_k : ~P_k) — one LOP per plane, no
-//     shared-memory table;
+//     __shfl_up per column) the horizontal delta leaving the rows above and
+//     the text code of that column. Lane 0 reads the text (four codes per
+//     32-bit load in the steady state); the top boundary is D[0][j] = j,
+//     i.e. h_in = +1;
+//   * the match masks: DNA (<= 4 symbols) reads them from a per-thread
+//     shared-memory table [code][word][thread]; larger alphabets rebuild Eq
+//     from NP bit-planes with one IMAD per plane;
 //   * the result needs no per-column bookkeeping: after the last column,
 //     D[m][n] = D[0][n] + sum of vertical deltas = n + popc(Pv) - popc(Mv)
 //     over the real rows, reduced across the group.
-// Every warp is persistent and pulls 32/G jobs at a time from an atomic
-// counter; the planner sorts jobs by (bucket, text length desc) so a warp's
-// groups run the same number of steps.
+// Warps pull 32/G jobs at a time from an atomic counter (a bounded number
+// of pulls per warp, so blocks turn over during a launch); the planner
+// sorts jobs by (bucket, text length desc) so a warp's groups run the same
+// number of steps, and the buckets' launches overlap on side streams.
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>

@@ -1,11 +1,12 @@
 // Pairwise aligner: batched Gotoh Needleman-Wunsch
 // with device-side traceback, bit-exact with nw_align (pairwise.cpp:301-415).
 //
-// Forward (K5): one warp per alignment. Lane g owns RR consecutive rows of
-// a 32*RR-row pass and sweeps the columns of b as a diagonal pipeline (lane
-// g is on column s-g+1 at step s); the bottom row of lane g-1 arrives by
-// __shfl_up each step, the bottom row of a pass is parked in a per-warp
-// buffer for the next pass. Scores are kept in "tagged" form
+// Forward (K5, nw_fwd.cuh): one alignment per CTA of 1, 4 or 8 warps. Lane g
+// owns RR = 16 consecutive rows of its warp's 512-row band and sweeps the
+// columns of b as a diagonal pipeline (lane g is on column s-g+1 at step s);
+// the bottom row of lane g-1 arrives by __shfl_up each step, and each band
+// streams its bottom row to the band below through a shared-memory ring, so
+// all bands of an alignment run concurrently. Scores are kept in "tagged" form
 //     V = 4 * score + tag,  tag(M) = 2, tag(GapB) = 1, tag(GapA) = 0,
 // so ONE max over three tagged candidates returns both the best score and,
 // on ties, the state pick_best prefers (M > GapB > GapA, pairwise.cpp:272-
