@@ -62,6 +62,11 @@ const char* dm_last_error(void);
 int dm_abi_version(void);
 
 /* ---- context ---------------------------------------------------------- */
+/* A context owns a CUDA stream and scratch memory on one device. Calls on one
+ * context are serialised by a per-context lock, so a context may be shared by
+ * host threads (as the reference's reentrant functions are); dm_ctx_destroy
+ * must not race with other calls on the same context. Errors: the status
+ * code of the call plus dm_last_error() on the calling thread. */
 int dm_ctx_create(int device, dm_ctx** out);
 int dm_ctx_destroy(dm_ctx* ctx);
 int dm_ctx_sync(dm_ctx* ctx);

@@ -94,11 +94,11 @@ int dm_ctx_destroy(dm_ctx* ctx) {
 }
 
 int dm_ctx_sync(dm_ctx* ctx) {
-    return guard([&] { DM_CUDA(cudaStreamSynchronize(ctx->stream)); });
+    return guard(ctx, [&] { DM_CUDA(cudaStreamSynchronize(ctx->stream)); });
 }
 
 int dm_ctx_set_stream(dm_ctx* ctx, void* stream) {
-    return guard([&] {
+    return guard(ctx, [&] {
         require(ctx != nullptr, "null context");
         DM_CUDA(cudaStreamSynchronize(ctx->stream));
         if (ctx->own_stream) {
@@ -110,7 +110,7 @@ int dm_ctx_set_stream(dm_ctx* ctx, void* stream) {
 }
 
 int dm_int32_peak(dm_ctx* ctx, int mode, double* lane_ops_per_s) {
-    return guard([&] {
+    return guard(ctx, [&] {
         require(ctx && lane_ops_per_s, "null argument");
         require(mode >= 0 && mode <= 2, "mode must be 0, 1 or 2");
         *lane_ops_per_s = dm::int32_peak(ctx, mode);
@@ -118,7 +118,7 @@ int dm_int32_peak(dm_ctx* ctx, int mode, double* lane_ops_per_s) {
 }
 
 int dm_ctx_set_shard(dm_ctx* ctx, int rank, int world) {
-    return guard([&] {
+    return guard(ctx, [&] {
         require(world >= 1 && rank >= 0 && rank < world, "invalid shard (rank, world)");
         ctx->rank = rank;
         ctx->world = world;
@@ -127,7 +127,7 @@ int dm_ctx_set_shard(dm_ctx* ctx, int rank, int world) {
 
 int dm_seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint32_t n,
                      dm_seqset** out) {
-    return guard([&] {
+    return guard(ctx, [&] {
         require(ctx && out && offsets, "null argument");
         DM_CUDA(cudaSetDevice(ctx->device));
         *out = dm::seqset_create(ctx, data, offsets, n);
@@ -135,7 +135,7 @@ int dm_seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets, uin
 }
 
 int dm_seqset_destroy(dm_seqset* s) {
-    return guard([&] { delete s; });
+    return guard(s ? s->ctx : nullptr, [&] { delete s; });
 }
 
 uint32_t dm_seqset_count(const dm_seqset* s) { return s ? s->n : 0; }
@@ -154,7 +154,7 @@ static void fill_stats(dm_stats* st, const dm::LevTotals& t, float total_ms) {
 uint32_t dm_levenshtein(dm_ctx* ctx, const char* a, uint64_t na, const char* b, uint64_t nb,
                         int* status) {
     uint32_t d = 0;
-    int rc = guard([&] {
+    int rc = guard(ctx, [&] {
         require(ctx != nullptr, "null context");
         std::string buf;
         buf.append(a, na);
@@ -179,7 +179,7 @@ uint32_t dm_levenshtein(dm_ctx* ctx, const char* a, uint64_t na, const char* b, 
 
 int dm_lev_pairs(dm_ctx* ctx, const dm_seqset* s, const uint32_t* ia, const uint32_t* ib,
                  uint64_t n, uint32_t* out, dm_stats* st) {
-    return guard([&] {
+    return guard(ctx, [&] {
         require(ctx && s, "null argument");
         for (uint64_t i = 0; i < n; ++i)
             require(ia[i] < s->n && ib[i] < s->n, "sequence index out of range");
@@ -209,7 +209,7 @@ int dm_lev_pairs(dm_ctx* ctx, const dm_seqset* s, const uint32_t* ia, const uint
 
 int dm_lev_pairs_device(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia,
                         const uint32_t* d_ib, uint64_t n, uint32_t* d_out, dm_stats* st) {
-    return guard([&] {
+    return guard(ctx, [&] {
         require(ctx && s, "null argument");
         cudaEvent_t t0, t1;
         DM_CUDA(cudaEventCreate(&t0));
@@ -229,7 +229,7 @@ int dm_lev_pairs_device(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia,
 
 int dm_lev_one_to_many(dm_ctx* ctx, const dm_seqset* s, uint32_t from, const uint32_t* members,
                        uint64_t n, uint32_t* out, dm_stats* st) {
-    return guard([&] {
+    return guard(ctx, [&] {
         require(ctx && s, "null argument");
         require(from < s->n, "sequence index out of range");
         std::vector<dm::LevItem> items(n);
@@ -248,7 +248,7 @@ int dm_lev_one_to_many(dm_ctx* ctx, const dm_seqset* s, uint32_t from, const uin
 
 int dm_geometric_median(dm_ctx* ctx, const dm_seqset* s, const uint32_t* members, uint64_t n,
                         uint64_t seed, uint64_t exact_cap, uint32_t* out) {
-    return guard([&] {
+    return guard(ctx, [&] {
         require(ctx && s && out, "null argument");
         *out = dm::geometric_median(ctx, s, members, n, seed, exact_cap);
     });
@@ -256,7 +256,7 @@ int dm_geometric_median(dm_ctx* ctx, const dm_seqset* s, const uint32_t* members
 
 int dm_build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_cap,
                   dm_node* nodes, uint64_t* nnodes, uint32_t* order, dm_stats* st) {
-    return guard([&] {
+    return guard(ctx, [&] {
         require(ctx && s && nodes && nnodes && order, "null argument");
         std::vector<dm_node> nv;
         std::vector<uint32_t> ov;

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <new>
+#include <utility>
 #include <string>
 
 #include "dm_internal.h"
@@ -28,6 +29,14 @@ int guard(F&& f) {
         last_error() = e.what();
         return DM_ERUNTIME;
     }
+}
+
+// guard() holding the context's lock (null ctx: no lock; the body reports it)
+template <class F>
+int guard(dm_ctx* ctx, F&& f) {
+    if (!ctx) return guard(std::forward<F>(f));
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    return guard(std::forward<F>(f));
 }
 
 inline void require(bool ok, const char* msg) {

@@ -131,7 +131,7 @@ extern "C" {
 
 int dm_nw_align(dm_ctx* ctx, const char* a, uint64_t na, const char* b, uint64_t nb, const int16_t* table,
                 const uint8_t* has_symbol, int open_surcharge, int gap_extend, dm_pw** out) {
-    return guard([&] {
+    return guard(ctx, [&] {
         if (!ctx || !table || !has_symbol || !out) throw dm::invalid_argument("null argument");
         const dm::NwScheme sc = dm::make_scheme(table, has_symbol, open_surcharge, gap_extend);
         auto* pw = new dm_pw;
@@ -149,7 +149,7 @@ int dm_nw_align(dm_ctx* ctx, const char* a, uint64_t na, const char* b, uint64_t
 int dm_nw_batch(dm_ctx* ctx, const char* A, const uint64_t* a_off, const char* B, const uint64_t* b_off,
                 uint32_t njobs, const int16_t* table, const uint8_t* has_symbol, int open_surcharge, int gap_extend,
                 dm_pw** out, dm_stats* st) {
-    return guard([&] {
+    return guard(ctx, [&] {
         if (!ctx || !table || !has_symbol || !out || !a_off || !b_off) throw dm::invalid_argument("null argument");
         const dm::NwScheme sc = dm::make_scheme(table, has_symbol, open_surcharge, gap_extend);
         auto* pw = new dm_pw;
@@ -183,7 +183,7 @@ void dm_pw_free(dm_pw* p) { delete p; }
 
 int dm_insert_gap_columns(dm_ctx* ctx, const char* rows, uint64_t nrows, uint64_t width, const uint32_t* pos,
                           uint64_t npos, char* out) {
-    return guard([&] {
+    return guard(ctx, [&] {
         if (!ctx) throw dm::invalid_argument("null context");
         dm::insert_gap_columns(ctx, rows, nrows, width, pos, npos, out);
     });
@@ -192,7 +192,7 @@ int dm_insert_gap_columns(dm_ctx* ctx, const char* rows, uint64_t nrows, uint64_
 int dm_align_all(dm_ctx* ctx, const dm_seqset* s, const dm_node* nodes, uint64_t nnodes, const uint32_t* order,
                  const int16_t* table, const uint8_t* has_symbol, int open_surcharge, int gap_extend,
                  dm_msa_out** out, dm_stats* st) {
-    return guard([&] {
+    return guard(ctx, [&] {
         if (!ctx || !s || !nodes || !order || !table || !has_symbol || !out) throw dm::invalid_argument("null argument");
         const dm::NwScheme sc = dm::make_scheme(table, has_symbol, open_surcharge, gap_extend);
         std::vector<dm_node> nv(nodes, nodes + nnodes);
@@ -220,7 +220,7 @@ int dm_align_all(dm_ctx* ctx, const dm_seqset* s, const dm_node* nodes, uint64_t
 
 int dm_msa(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_cap, const int16_t* table,
            const uint8_t* has_symbol, int open_surcharge, int gap_extend, dm_msa_out** out, dm_stats* st) {
-    return guard([&] {
+    return guard(ctx, [&] {
         if (!ctx || !s || !table || !has_symbol || !out) throw dm::invalid_argument("null argument");
         const dm::NwScheme sc = dm::make_scheme(table, has_symbol, open_surcharge, gap_extend);
         if (st) std::memset(st, 0, sizeof(*st));

@@ -106,7 +106,7 @@ int dm_nccl_unique_id(uint8_t* id128) {
 }
 
 int dm_ctx_attach_nccl(dm_ctx* ctx, const uint8_t* id128, int rank, int world) {
-    return dm::guard([&] {
+    return dm::guard(ctx, [&] {
         dm::require(ctx && id128, "null argument");
         dm::require(world >= 1 && rank >= 0 && rank < world, "invalid shard (rank, world)");
         DM_CUDA(cudaSetDevice(ctx->device));
@@ -124,7 +124,7 @@ int dm_ctx_attach_nccl(dm_ctx* ctx, const uint8_t* id128, int rank, int world) {
 }
 
 int dm_ctx_simulate_world(dm_ctx* ctx, int world) {
-    return dm::guard([&] {
+    return dm::guard(ctx, [&] {
         dm::require(ctx != nullptr, "null context");
         dm::require(world >= 1 && world <= 64, "simulated world must be in [1, 64]");
         ctx->sim_world = world;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -111,6 +112,10 @@ struct dm_ctx {
     // scratch for the aligner / merge scheduler
     dm::DevBuf nw_in, nw_table, nw_jobs, nw_trace, nw_res, nw_gaps, rows_a, rows_b, colmap, tree_buf;
     uint64_t launches = 0;
+    // Every C ABI call on a context holds this lock (capi_guard.h), so one
+    // context may be shared by host threads (the reference's functions are
+    // reentrant and are called from parallel_for bodies).
+    std::recursive_mutex mu;
     dm_ctx() { attach(&stream); }
     void detach_buffers() { attach(nullptr); }
 

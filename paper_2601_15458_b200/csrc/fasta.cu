@@ -262,7 +262,7 @@ int dm_run_align(dm_ctx* ctx, const char* input_path, const char* output_path, i
                  int gap_extend, int flat, const int16_t* custom_table, const uint8_t* custom_has, uint64_t seed,
                  int input_order, const char* dump_tree_path, const char* dump_dedup_path,
                  dm_align_summary* summary, dm_stats* st) {
-    return dm::guard([&] {
+    return dm::guard(ctx, [&] {
         dm::require(ctx && input_path && output_path, "null argument");
         const std::string in(input_path);
         // pipeline.cpp:162-170: auto parses structurally, a fixed alphabet validates while parsing
@@ -326,7 +326,7 @@ int dm_dump_tree(const dm_node* nodes, uint64_t nnodes, const char* ids, const u
 
 int dm_write_fasta(dm_ctx* ctx, const char* path, const char* ids, const uint64_t* id_off, const char* descs,
                    const uint64_t* desc_off, const char* residues, const uint64_t* res_off, uint64_t n) {
-    return dm::guard([&] {
+    return dm::guard(ctx, [&] {
         dm::require(ctx && path && id_off && desc_off && res_off, "null argument");
         std::vector<std::string> headers(n);
         std::vector<uint64_t> src(n);

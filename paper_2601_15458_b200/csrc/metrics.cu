@@ -246,7 +246,7 @@ extern "C" {
 int dm_evaluate(dm_ctx* ctx, const char* rows, uint64_t nrows, uint64_t width, const uint32_t* row_to_sequence,
                 const char* raw, const uint64_t* raw_offsets, uint32_t nraw, uint64_t sample_size,
                 uint64_t pair_budget, uint64_t seed, dm_metrics* out) {
-    return dm::guard([&] {
+    return dm::guard(ctx, [&] {
         dm::require(ctx && out && (rows || nrows == 0) && (row_to_sequence || nrows == 0) && raw_offsets,
                     "null argument");
         dm::evaluate(ctx, rows, nrows, width, row_to_sequence, raw, raw_offsets, nraw, sample_size, pair_budget,
@@ -255,7 +255,7 @@ int dm_evaluate(dm_ctx* ctx, const char* rows, uint64_t nrows, uint64_t width, c
 }
 
 int dm_gap_percent(dm_ctx* ctx, const char* rows, uint64_t nrows, uint64_t width, double* out) {
-    return dm::guard([&] {
+    return dm::guard(ctx, [&] {
         dm::require(ctx && out, "null argument");
         *out = dm::gap_percent(ctx, rows, nrows, width);
     });
@@ -263,7 +263,7 @@ int dm_gap_percent(dm_ctx* ctx, const char* rows, uint64_t nrows, uint64_t width
 
 int dm_row_pair_stats(dm_ctx* ctx, const char* a, uint64_t na, const char* b, uint64_t nb, uint32_t* considered,
                       uint32_t* mismatched, uint32_t* hamming) {
-    return dm::guard([&] {
+    return dm::guard(ctx, [&] {
         dm::require(ctx && considered && mismatched && hamming, "null argument");
         if (na != nb) throw dm::invalid_argument("rows must have equal length");
         dm::row_pair_stats(ctx, a, b, na, considered, mismatched, hamming);

@@ -173,7 +173,7 @@ int dm_align_sequences(dm_ctx* ctx, const char* data, const uint64_t* offsets, u
                        int gap_open, int gap_extend, int flat, const int16_t* custom_table,
                        const uint8_t* custom_has, uint64_t seed, int input_order, char** rows_out,
                        uint64_t* width_out, dm_align_summary* summary, dm_stats* st) {
-    return dm::guard([&] {
+    return dm::guard(ctx, [&] {
         dm::require(ctx && offsets && rows_out && width_out, "null argument");
         dm::AlignCore res = dm::align_core(ctx, data, offsets, n, nullptr, alphabet, gap_open, gap_extend, flat,
                                            custom_table, custom_has, seed, input_order, st);

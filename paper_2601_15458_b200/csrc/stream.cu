@@ -234,7 +234,7 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
 
 extern "C" int dm_lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint64_t npairs,
                                    uint32_t* out, dm_stats* st) {
-    return dm::guard([&] {
+    return dm::guard(ctx, [&] {
         dm::require(ctx && offsets && (out || npairs == 0), "null argument");
         cudaEvent_t t0, t1;
         DM_CUDA(cudaEventCreate(&t0));

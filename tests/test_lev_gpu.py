@@ -170,3 +170,26 @@ def test_packed_streaming_mixed_chunks(dm, ctx, orc, monkeypatch, chunk):
     assert list(got) == want
     # a second call on the same context reuses the planner slots
     assert list(dm.lev_pairs_packed(data, offs, ctx)) == want
+
+
+def test_context_shared_by_threads(dm, ctx, orc):
+    """The reference's functions are reentrant (called from parallel_for
+    bodies); one context used by 8 host threads at once gives
+    the same answers (ctypes drops the GIL, so the calls overlap in C)."""
+    from concurrent.futures import ThreadPoolExecutor
+    rng = random.Random(99)
+    pairs = [(rand_str(rng, rng.randint(0, 300)), rand_str(rng, rng.randint(0, 300))) for _ in range(64)]
+    want = [orc.levenshtein(a, b) for a, b in pairs]
+
+    def work(k):
+        a, b = pairs[k]
+        d = dm.levenshtein(a, b, ctx)
+        ss = dm.SeqSet([a, b, a], ctx)
+        d2 = int(dm.lev_pairs(ss, [0, 1], [1, 2])[0])
+        r = dm.nw_align(a + "A", b + "C", ctx=ctx)
+        return d, d2, r.score
+
+    with ThreadPoolExecutor(8) as ex:
+        got = list(ex.map(work, range(len(pairs))))
+    assert [g[0] for g in got] == want and [g[1] for g in got] == want
+    assert all(g[2] == dm.nw_align(a + "A", b + "C", ctx=ctx).score for g, (a, b) in zip(got, pairs))
