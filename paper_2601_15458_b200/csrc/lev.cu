@@ -94,24 +94,20 @@ __device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
     return d;
 }
 
-// v = (v << 1) | cin over W words; returns the bit shifted out. Per word one
-// IMAD.WIDE (v * 2: low half = v << 1, high half = the bit leaving the word)
-// plus one IMAD folding in the carry from the word below — all on the FMA
-// pipe, which co-issues with the LOP3 stream (IMAD.HI / SHF.L.W do not;
-// measured in tools/ubench/pipes.cu).
+// v = (v << 1) | cin over W words; returns the bit shifted out. The shift
+// is v + v as ONE carry-chained add over the words (one IADD3.X per word);
+// the carry-in lands in the free bit 0 of word 0. Measured on the bare
+// per-word mix (tools/ubench/mix.cu): 61 TCUPS with both shifts as add
+// chains vs 54 with IMAD.WIDE + IMAD per word on the FMA pipe — fewer
+// instructions issued beats moving work off the ALU pipe here.
 template <int W>
-__device__ __forceinline__ uint32_t shl1(uint32_t (&v)[W], uint32_t cin, uint32_t two, uint32_t one) {
-    uint32_t carry = cin;
+__device__ __forceinline__ uint32_t shl1(uint32_t (&v)[W], uint32_t cin) {
+    uint32_t t[W];
 #pragma unroll
-    for (int w = 0; w < W; ++w) {
-        uint32_t lo, hi;
-        asm("{\n\t.reg .u64 t;\n\tmul.wide.u32 t, %2, %3;\n\tmov.b64 {%0, %1}, t;\n\t}"
-            : "=r"(lo), "=r"(hi)
-            : "r"(v[w]), "r"(two));
-        v[w] = imad(lo, one, carry);
-        carry = hi;
-    }
-    return carry;
+    for (int w = 0; w < W; ++w) t[w] = v[w];
+    Chain<W>::add(v, t, t);
+    v[0] |= cin;
+    return t[W - 1] >> 31;
 }
 
 template <int NP, int W>
@@ -230,8 +226,8 @@ __global__ void __launch_bounds__(256, NP == 2 ? 3 : 1) lev_kernel(const LevArgs
                     // terms are disjoint and the OR is an add -> FMA pipe
                     Ph[w] = w == 0 ? lop3<0xF1>(Mv[w], S[w], T0) : imad(lop3<0x01>(S[w], Pv[w], Xv[w]), a.one, Mv[w]);
                 }
-                const uint32_t hpo = shl1<W>(Ph, hp, two, a.one);
-                const uint32_t hmo = shl1<W>(Mh, hm, two, a.one);
+                const uint32_t hpo = shl1<W>(Ph, hp);
+                const uint32_t hmo = shl1<W>(Mh, hm);
 #pragma unroll
                 for (int w = 0; w < W; ++w) {
                     Pv[w] = lop3<0xF1>(Mh[w], Xv[w], Ph[w]);  // Mh | ~(Xv | Ph)
