@@ -1,7 +1,9 @@
 // Ceiling of the distance kernel's per-word instruction mix on one B200:
 // the K1 word update (LDS match mask, 6 LOP3, carry-chained add, IMAD Ph,
-// two IMAD.WIDE+IMAD shifts) over W = 16 words per column, no shuffles, no
-// text loads, no bounds checks, 24 warps per SM as in lev_kernel<2,16>.
+// two 1-bit shifts) over W = 16 words per column, no shuffles, no text loads,
+// no bounds checks, 24 warps per SM as in lev_kernel<2,16>. Variants compare
+// shift forms (IMAD.WIDE+IMAD, funnel, carry-chained add — the one K1 uses)
+// and Ph as IMAD vs LOP3; results in profiles/r01_ubench_mix.txt.
 // Prints cells/s; the real kernel's number divided by this one is the share
 // of the mix's ceiling it reaches.
 #include <cstdint>
