@@ -11,8 +11,10 @@ A step = one pass of the distance engine over the whole pair batch.
          launching stream), max over ranks, aggregated over all ranks.
   e2e    same metric through the C ABI with HOST buffers: every step hands
          the packed pairs in pinned host memory to dm_lev_pairs_packed, which
-         uploads them in chunks overlapped with the kernels and returns the
-         distances in host memory (wall clock around the call).
+         uploads them in chunks overlapped with the kernels (A/C/G/T chunks
+         packed to 2 bits per residue by host threads first, so a quarter of
+         the bytes cross PCIe; h2d_bytes_per_step counts what was copied) and
+         returns the distances in host memory (wall clock around the call).
   nw     the NW micro-benchmark of SURVEY.md §8(d): the first 65,536 cfg1
          pairs through dm_nw_batch (nucleotide scheme, affine -10/-1, full
          traceback), bit-checked against the C restatement on a sample;
@@ -64,30 +66,44 @@ class ClockSampler:
         self.lines = []
 
     def start(self):
+        """Start nvidia-smi and wait for its first sample, so the timed region
+        (which may last only ~100 ms) is covered from its first step."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t_end = time.time() + 5
+            while not self.lines and time.time() < t_end and self.proc.poll() is None:
+                time.sleep(0.01)
         except FileNotFoundError:
             self.proc = None
+        self.t0 = time.time()
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t1 = time.time()
+        # at least one sample taken after the timed region began
+        t_end = t1 + 1.0
+        while not any(t >= self.t0 for t, _ in self.lines) and time.time() < t_end and self.proc.poll() is None:
+            time.sleep(0.01)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
+        during = [ln for t, ln in self.lines if self.t0 <= t <= t1 + 0.06]
+        if not during:
+            during = [ln for t, ln in self.lines if t >= self.t0][:1]
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in during:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 8:
                 continue
@@ -352,11 +368,14 @@ def main():
     offs_c = np.ascontiguousarray(offs, dtype=np.uint64)
     u32p = C.POINTER(C.c_uint32)
 
+    est = dm.dm_stats()
+
     def e2e_step():
         # host buffers in, host distances out: chunked upload overlapped with the kernels
+        # (nucleotide chunks cross PCIe 2-bit packed; est reports the bytes moved)
         check(lib().dm_lev_pairs_packed(ctx.handle, C.c_void_p(pinned.data_ptr()),
                                         offs_c.ctypes.data_as(C.POINTER(C.c_uint64)), n_pairs,
-                                        out_h.ctypes.data_as(u32p), None))
+                                        out_h.ctypes.data_as(u32p), C.byref(est)))
 
     e2e_step()
     torch.cuda.synchronize()
@@ -374,8 +393,9 @@ def main():
     if not np.array_equal(out_h, got):
         raise SystemExit("bench: e2e distances differ from the device-resident run")
     e2e = {"value": cells_step * world / e2e_s / 1e9, "unit": "GCUPS",
-           "h2d_bytes_per_step": int(len(data) + offs_c.nbytes),
-           "d2h_bytes_per_step": int(4 * n_pairs)}
+           "h2d_bytes_per_step": int(est.h2d_bytes), "d2h_bytes_per_step": int(est.d2h_bytes),
+           "host_input_bytes_per_step": int(len(data) + offs_c.nbytes),
+           "upload": "A/C/G/T chunks packed to 2 bits/residue by host threads; codes built on the device from the packed bytes"}
 
     # ---- roofline: INT32 lane-op peak measured on this box --------------
     peaks = []

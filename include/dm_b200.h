@@ -56,6 +56,7 @@ typedef struct {
     uint64_t launches;       /* kernels launched */
     double tree_ms, align_ms; /* dm_msa: phase times; dm_nw_*: align_ms = forward-pass kernel time */
     uint64_t lev_calls, nw_calls;
+    uint64_t h2d_bytes, d2h_bytes; /* dm_lev_pairs_packed: bytes that crossed PCIe */
 } dm_stats;
 
 const char* dm_last_error(void);
@@ -109,10 +110,19 @@ int dm_lev_pairs_device(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia,
                         const uint32_t* d_ib, uint64_t n, uint32_t* d_out, dm_stats* st);
 /* End-to-end batch from HOST memory: pair i = (sequence 2i, sequence 2i+1)
  * of `data` / `offsets` (2*npairs+1 entries). Uploads and computes in
- * overlapped chunks (copy stream + compute stream); pinned `data` lets the
- * transfer run fully asynchronously. out: host uint32[npairs]. */
+ * overlapped chunks (copy stream + compute stream). Chunks holding only
+ * A/C/G/T bytes cross PCIe as 2-bit codes (packed by host threads into
+ * pinned slots, expanded on the device); others are uploaded as given, where
+ * pinned `data` lets the transfer run fully asynchronously. The results are
+ * the same either way. st->h2d_bytes / d2h_bytes report the bytes copied.
+ * Env: DM_STREAM_PACK=0 disables packing, DM_HOST_THREADS sizes the host
+ * pool. out: host uint32[npairs]. */
 int dm_lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint64_t npairs,
                         uint32_t* out, dm_stats* st);
+/* The packer alone (no device needed): residue j of src -> bits 2(j%4).. of
+ * dst[j/4], codes A0 C1 G2 T3, last byte zero-padded; DM_EINVAL if src holds
+ * any other byte. dst: (n+3)/4 bytes. */
+int dm_pack_nt(const char* src, uint64_t n, uint8_t* dst);
 /* distance_scan: out[i] = levenshtein(seq from, seq members[i]). */
 int dm_lev_one_to_many(dm_ctx* ctx, const dm_seqset* s, uint32_t from, const uint32_t* members,
                        uint64_t n, uint32_t* out, dm_stats* st);

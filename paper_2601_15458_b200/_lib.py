@@ -37,7 +37,8 @@ class dm_metrics(C.Structure):
 class dm_stats(C.Structure):
     _fields_ = [("kernel_ms", C.c_double), ("total_ms", C.c_double), ("cells", C.c_uint64),
                 ("cells_executed", C.c_uint64), ("launches", C.c_uint64), ("tree_ms", C.c_double),
-                ("align_ms", C.c_double), ("lev_calls", C.c_uint64), ("nw_calls", C.c_uint64)]
+                ("align_ms", C.c_double), ("lev_calls", C.c_uint64), ("nw_calls", C.c_uint64),
+                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -76,6 +77,7 @@ SIGNATURES = {
     "dm_lev_pairs": (C.c_int, [_P, _P, _u32p, _u32p, C.c_uint64, _u32p, C.POINTER(dm_stats)]),
     "dm_lev_pairs_device": (C.c_int, [_P, _P, _P, _P, C.c_uint64, _P, C.POINTER(dm_stats)]),
     "dm_lev_pairs_packed": (C.c_int, [_P, C.c_void_p, _u64p, C.c_uint64, _u32p, C.POINTER(dm_stats)]),
+    "dm_pack_nt": (C.c_int, [C.c_char_p, C.c_uint64, C.c_void_p]),
     "dm_lev_one_to_many": (C.c_int, [_P, _P, C.c_uint32, _u32p, C.c_uint64, _u32p, C.POINTER(dm_stats)]),
     "dm_geometric_median": (C.c_int, [_P, _P, _u32p, C.c_uint64, C.c_uint64, C.c_uint64, _u32p]),
     "dm_build_tree": (C.c_int, [_P, _P, C.c_uint64, C.c_uint64, C.POINTER(dm_node), _u64p, _u32p,

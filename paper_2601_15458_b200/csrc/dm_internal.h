@@ -103,6 +103,9 @@ struct dm_ctx {
     cudaStream_t copy_stream = nullptr;  // host->device staging of streamed batches
     static constexpr int kStreamSlots = 4;  // chunks of a streamed batch in flight
     dm::DevBuf stage[kStreamSlots], stream_pairs, stream_out, stream_offs;
+    dm::DevBuf stage_packed[kStreamSlots];  // 2-bit nucleotide chunks as uploaded
+    dm::DevBuf ss_meta, ss_codes, ss_planes;  // planner contexts: the chunk's sequence set (reused)
+    dm::PinnedBuf pin_pack[kStreamSlots];   // host side of the same
     dm_ctx* prep[kStreamSlots] = {};  // planner contexts of the streamed path (own stream + scratch)
     static constexpr int kLevSide = 8;  // side streams the distance buckets fan out on
     cudaStream_t lev_side[kLevSide] = {};
@@ -124,9 +127,11 @@ private:
         for (dm::DevBuf* b : {&items, &out, &counter, &aux, &aux2, &aux3, &lev_all, &lev_items,
                               &stream_pairs, &stream_out, &stream_offs, &nw_in, &nw_table,
                               &nw_jobs, &nw_trace,
-                              &nw_res, &nw_gaps, &rows_a, &rows_b, &colmap, &tree_buf})
+                              &nw_res, &nw_gaps, &rows_a, &rows_b, &colmap, &tree_buf, &ss_meta, &ss_codes,
+                              &ss_planes})
             b->sp = s;
         for (dm::DevBuf& b : stage) b.sp = s;
+        for (dm::DevBuf& b : stage_packed) b.sp = s;
     }
 };
 
@@ -153,6 +158,7 @@ struct dm_seqset {
     uint64_t* d_blk = nullptr;
     uint64_t* d_planes = nullptr; // [block][plane] 64-bit words
     uint64_t total_blocks = 0;
+    bool owns_meta = true;        // false: the arrays above are a context's scratch (streamed chunks)
     ~dm_seqset();
 };
 
@@ -179,6 +185,7 @@ struct LevItem {
 
 struct LevTotals {
     uint64_t cells = 0, cells_exec = 0, launches = 0;
+    uint64_t h2d_bytes = 0, d2h_bytes = 0;  // streamed path: bytes actually copied
     float kernel_ms = 0.f;
 };
 
@@ -189,11 +196,14 @@ void lev_run_host_items(dm_ctx* ctx, const dm_seqset* s, std::vector<LevItem>& i
 // Pairs (2i, 2i+1) of a packed HOST buffer, streamed in chunks (stream.cu).
 void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint64_t npairs, uint32_t* out,
                       LevTotals* tot, bool timing);
-// Streamed path: plan on `prep` (its stream and scratch; host-synchronous),
-// then launch the distance kernels on ctx->stream after `planned`.
+// Streamed path: plan on `prep` (its stream and scratch), then launch the
+// distance kernels on ctx->stream after `planned`. pair_offs (host, 2n+1
+// offsets of pairs (2i, 2i+1)) given: the bucket histogram is counted on the
+// host from the lengths and the planner never synchronises; null: it is read
+// back from the device (one host sync).
 void lev_plan_then_launch(dm_ctx* prep, dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia,
                           const uint32_t* d_ib, uint64_t n, uint32_t* d_out, cudaEvent_t planned,
-                          LevTotals* tot);
+                          LevTotals* tot, const uint64_t* pair_offs = nullptr);
 // Pairs given as device arrays (bench path): builds items on the device.
 void lev_run_device_pairs(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia,
                           const uint32_t* d_ib, uint64_t n, uint32_t* d_out, LevTotals* tot,
@@ -206,9 +216,16 @@ dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets,
 // Sequence set over residues already on the device (d_raw) whose offsets are
 // d_offs[first..first+n] (device, absolute) / h_offs[0..n] (host, same values):
 // no host->device copies, so it never queues behind a bulk upload.
-// Host mirrors (len/off/blk_off/raw_off) are left empty.
+// Host mirrors (len/off/blk_off/raw_off) are left empty. The device arrays
+// live in ctx's ss_* scratch (no allocation per chunk; valid until the next
+// call on ctx, which must be stream-ordered after every use). acgt: the caller
+// knows every byte is A/C/G/T (the streamed packer checked), so the census
+// and its host sync are skipped (codes A0 C1 G2 T3, 2 bit-planes).
+// d_packed (with acgt): the residues as 2-bit codes (host_pack.h layout,
+// relative to h_offs[0]); d_raw is then unused and left null in the set.
 dm_seqset* seqset_create_device(dm_ctx* ctx, const uint8_t* d_raw, const uint64_t* d_offs,
-                                const uint64_t* h_offs, uint32_t n);
+                                const uint64_t* h_offs, uint32_t n, bool acgt = false,
+                                const uint8_t* d_packed = nullptr);
 
 // Guide tree (tree.cu / tree_host.cpp).
 void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_cap,

@@ -32,9 +32,12 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
+#include <vector>
 
 #include "dm_internal.h"
 #include "comm.h"
@@ -287,7 +290,10 @@ void launch_one(const LevArgs& a, int sm_count, cudaStream_t st) {
     // blocks, so blocks turn over during a launch: kernels on other streams
     // (the planners of streamed batches) get SM slots within a fraction of
     // a bucket instead of after it. grid * 8 warps * max_pulls >= tasks.
-    constexpr uint64_t kWaves = 4;
+    static const uint64_t kWaves = [] {
+        const char* e = std::getenv("DM_LEV_WAVES");
+        return e ? (uint64_t)std::max(1, std::atoi(e)) : (uint64_t)4;
+    }();
     const uint64_t tasks = ((uint64_t)a.nitems + (32u >> a.lgG) - 1) / (32u >> a.lgG);
     const uint64_t resident = (uint64_t)occ * sm_count;
     const uint64_t want = (tasks + 7) / 8;  // blocks if every warp pulled once
@@ -398,10 +404,42 @@ struct LevPlan {
     unsigned long long hc[2];
 };
 
+// plan_kernel's histogram and cell counts for pairs (2i, 2i+1) of host
+// offsets, counted on the host (same orientation and bucket rule).
+void plan_hist_host(const uint64_t* offs, uint64_t n, int lg_gpar, int wmax, LevPlan& P) {
+    // lg per pattern word count B (beyond the table: 5); the per-pair body is
+    // branch-free (random orientations would mispredict)
+    const uint32_t bmax = (uint32_t)wmax << 5;
+    std::vector<uint8_t> lgof(bmax + 2);
+    for (uint32_t B = 0; B <= bmax + 1; ++B) {
+        int lg = lg_gpar;
+        while ((uint32_t)(wmax << lg) < B && lg < 5) ++lg;
+        lgof[B] = (uint8_t)lg;
+    }
+    std::vector<unsigned int> h(4 * kBuckets, 0u);  // 4 interleaved copies: no store-forwarding chains
+    unsigned long long c0 = 0, c1 = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint32_t a = (uint32_t)(offs[2 * i + 1] - offs[2 * i]), b = (uint32_t)(offs[2 * i + 2] - offs[2 * i + 1]);
+        const uint32_t m = 0u - (uint32_t)(a < b), lx = (a & m) | (b & ~m), ly = a ^ b ^ lx;
+        const uint32_t B = (lx + 31) >> 5;
+        const int lg = lgof[std::min(B, bmax + 1)];
+        const uint32_t R = std::max((B + (1u << lg) - 1) >> lg, 1u);
+        const uint32_t bucket = R > (uint32_t)wmax ? kBuckets - 1 : (uint32_t)lg * 32 + R;
+        ++h[(i & 3) * kBuckets + bucket];
+        c0 += (unsigned long long)lx * ly;
+        c1 += (unsigned long long)(R << lg) * 32ull * ly;
+    }
+    for (int k = 0; k < kBuckets; ++k) P.h[k] = h[k] + h[kBuckets + k] + h[2 * kBuckets + k] + h[3 * kBuckets + k];
+    P.hc[0] = c0;
+    P.hc[1] = c1;
+}
+
 // Planner phase on `ctx`'s stream (scratch from ctx): orient, bucket, sort,
-// read the histogram back (the one host sync of a batch).
+// read the histogram back (the one host sync of a batch) -- or, given the
+// host offsets of identity pairs (2i, 2i+1), count it on the host and stay
+// asynchronous.
 void plan_batch(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const uint32_t* d_ib,
-                const LevItem* d_in_items, uint64_t n, LevPlan& P) {
+                const LevItem* d_in_items, uint64_t n, LevPlan& P, const uint64_t* pair_offs = nullptr) {
     if (n > 0xffffffffull) throw invalid_argument("too many distance jobs in one batch");
     cudaStream_t st = ctx->stream;
     const int np = s->planes;
@@ -443,9 +481,13 @@ void plan_batch(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const uin
     DM_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_b, k0, k1, i0, i1, (int)n, 0, 40, st));
     gather_items<<<grid, 256, 0, st>>>(it0, i1, n, it1);
     DM_CUDA(cudaGetLastError());
-    DM_CUDA(cudaMemcpyAsync(P.h, hist, sizeof(P.h), cudaMemcpyDeviceToHost, st));
-    DM_CUDA(cudaMemcpyAsync(P.hc, cells, sizeof(P.hc), cudaMemcpyDeviceToHost, st));
-    DM_CUDA(cudaStreamSynchronize(st));
+    if (pair_offs) {
+        plan_hist_host(pair_offs, n, lg_gpar, wmax, P);
+    } else {
+        DM_CUDA(cudaMemcpyAsync(P.h, hist, sizeof(P.h), cudaMemcpyDeviceToHost, st));
+        DM_CUDA(cudaMemcpyAsync(P.hc, cells, sizeof(P.hc), cudaMemcpyDeviceToHost, st));
+        DM_CUDA(cudaStreamSynchronize(st));
+    }
     if (P.h[kBuckets - 1])
         throw invalid_argument("sequence too long for the distance engine (max " +
                                std::to_string(32 * wmax * 32) + " residues for this alphabet)");
@@ -620,14 +662,22 @@ void lev_run_device_pairs(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia,
 
 void lev_plan_then_launch(dm_ctx* prep, dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia,
                           const uint32_t* d_ib, uint64_t n, uint32_t* d_out, cudaEvent_t planned,
-                          LevTotals* tot) {
+                          LevTotals* tot, const uint64_t* pair_offs) {
     if (n == 0) return;
     LevPlan P;
-    plan_batch(prep, s, d_ia, d_ib, nullptr, n, P);
+    const bool tr = std::getenv("DM_TRACE") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
+    plan_batch(prep, s, d_ia, d_ib, nullptr, n, P, pair_offs);
+    auto t1 = std::chrono::steady_clock::now();
     DM_CUDA(cudaEventRecord(planned, prep->stream));
     // the kernels follow the planner directly, not ctx->stream: this batch's
     // buckets start while the previous batch's tails still drain
     const int launches = launch_plan(ctx, P, s, d_out, ctx->stream, planned);
+    auto t2 = std::chrono::steady_clock::now();
+    if (tr)
+        std::fprintf(stderr, "[plan] plan_batch %.2f ms, launch_plan %.2f ms (%d launches)\n",
+                     std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                     std::chrono::duration<double, std::milli>(t2 - t1).count(), launches);
     ctx->launches += launches;
     if (tot) {
         tot->cells += P.hc[0];

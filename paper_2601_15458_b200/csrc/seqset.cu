@@ -82,6 +82,23 @@ __global__ void recode_kernel(const uint8_t* __restrict__ raw, const uint64_t* _
     }
 }
 
+// Same from 2-bit packed residues (streamed A/C/G/T chunks: the packed codes
+// are the codes, A0 C1 G2 T3); also zeroes each sequence's padding, so the
+// code buffer needs no memset.
+__global__ void recode_packed_kernel(const uint8_t* __restrict__ packed, const uint64_t* __restrict__ raw_off,
+                                     const uint64_t* __restrict__ off, uint32_t n, uint8_t* __restrict__ codes) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t s = warp; s < n; s += nw) {
+        const uint64_t a = raw_off[s], e = raw_off[s + 1], o = off[s], span = off[s + 1] - o;
+        for (uint64_t i = lane; i < span; i += 32) {
+            const uint64_t r = a + i;
+            codes[o + i] = r < e ? (uint8_t)((packed[r >> 2] >> ((r & 3) * 2)) & 3u) : (uint8_t)0;
+        }
+    }
+}
+
 template <int NP>
 __global__ void planes_kernel(const uint8_t* __restrict__ codes, const uint64_t* __restrict__ off,
                               const uint32_t* __restrict__ len, const uint64_t* __restrict__ blk,
@@ -154,10 +171,16 @@ __global__ void lut_kernel(const unsigned int* __restrict__ present, uint8_t* __
     lut[c] = (present[c >> 5] >> (c & 31)) & 1u ? (uint8_t)below : 0;
 }
 
+// Fixed code map of an all-A/C/G/T set: A0 C1 G2 T3.
+__global__ void acgt_lut_kernel(uint8_t* __restrict__ lut) {
+    const int c = threadIdx.x;
+    lut[c] = c == 'C' ? 1 : (c == 'G' ? 2 : (c == 'T' ? 3 : 0));
+}
+
 }  // namespace
 
 dm_seqset* seqset_create_device(dm_ctx* ctx, const uint8_t* d_raw, const uint64_t* d_offs,
-                                const uint64_t* h_offs, uint32_t n) {
+                                const uint64_t* h_offs, uint32_t n, bool acgt, const uint8_t* d_packed) {
     auto* s = new dm_seqset;
     s->ctx = ctx;
     s->n = n;
@@ -174,10 +197,14 @@ dm_seqset* seqset_create_device(dm_ctx* ctx, const uint8_t* d_raw, const uint64_
         s->total_blocks = b;
         const uint64_t nbytes = h_offs[n] - h_offs[0];
         cudaStream_t st = ctx->stream;
-        DM_CUDA(cudaMallocAsync(&s->d_raw_off, (n + 1) * sizeof(uint64_t), st));
-        DM_CUDA(cudaMallocAsync(&s->d_off, (n + 1) * sizeof(uint64_t), st));
-        DM_CUDA(cudaMallocAsync(&s->d_len, std::max<size_t>(n, 1) * sizeof(uint32_t), st));
-        DM_CUDA(cudaMallocAsync(&s->d_blk, (n + 1) * sizeof(uint64_t), st));
+        // device arrays from the context's scratch: no pool traffic per chunk
+        s->owns_meta = false;
+        const size_t a8 = ((size_t)(n + 1) * 8 + 255) & ~size_t(255), a4 = ((size_t)n * 4 + 259) & ~size_t(255);
+        char* meta = (char*)ctx->ss_meta.get(3 * a8 + a4);
+        s->d_raw_off = (uint64_t*)meta;
+        s->d_off = (uint64_t*)(meta + a8);
+        s->d_blk = (uint64_t*)(meta + 2 * a8);
+        s->d_len = (uint32_t*)(meta + 3 * a8);
         size_t cub_b = 0;
         DM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, cub_b, (uint64_t*)nullptr, (uint64_t*)nullptr, (int)n + 1, st));
         const size_t sz_b = ((size_t)(n + 1) * 8 + 255) & ~size_t(255);
@@ -191,36 +218,57 @@ dm_seqset* seqset_create_device(dm_ctx* ctx, const uint8_t* d_raw, const uint64_
         DM_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_b, code_sz, s->d_off, (int)n + 1, st));
         DM_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_b, blk_sz, s->d_blk, (int)n + 1, st));
 
-        unsigned int* d_present = ctx->aux.as<unsigned int>(8);
-        DM_CUDA(cudaMemsetAsync(d_present, 0, 32, st));
-        if (nbytes) {
-            const int grid = (int)std::min<uint64_t>((nbytes + 4095) / 4096, (uint64_t)ctx->sm_count * 16);
-            census_kernel<<<std::max(grid, 1), 256, 0, st>>>(d_raw, nbytes,
-                                                             reinterpret_cast<unsigned long long*>(d_present));
-            DM_CUDA(cudaGetLastError());
-        }
         uint8_t* d_lut = (uint8_t*)ctx->aux2.get(256);
-        lut_kernel<<<1, 256, 0, st>>>(d_present, d_lut);
-        DM_CUDA(cudaGetLastError());
-        unsigned int present[8];
-        DM_CUDA(cudaMemcpyAsync(present, d_present, 32, cudaMemcpyDeviceToHost, st));
-        DM_CUDA(cudaStreamSynchronize(st));
-        int nsym = 0;
-        for (int c = 0; c < 256; ++c)
-            if (present[c >> 5] & (1u << (c & 31))) {
-                s->code_of[c] = (uint8_t)nsym++;
+        if (acgt) {
+            acgt_lut_kernel<<<1, 256, 0, st>>>(d_lut);
+            DM_CUDA(cudaGetLastError());
+            int k = 0;
+            for (int c : {'A', 'C', 'G', 'T'}) {
+                s->code_of[c] = (uint8_t)k++;
                 s->present[c] = true;
             }
-        s->nsym = nsym;
-        s->planes = nsym <= 4 ? 2 : (nsym <= 32 ? 5 : 8);
-
-        DM_CUDA(cudaMallocAsync(&s->d_codes, o + 16, st));
-        DM_CUDA(cudaMallocAsync(&s->d_planes, std::max<uint64_t>(b, 1) * s->planes * sizeof(uint64_t), st));
-        DM_CUDA(cudaMemsetAsync(s->d_codes, 0, o + 16, st));
-        if (n) {
-            const int grid = (int)std::min<uint64_t>((n + 7) / 8, (uint64_t)ctx->sm_count * 16);
-            recode_kernel<<<grid, 256, 0, st>>>(d_raw, s->d_raw_off, s->d_off, n, d_lut, s->d_codes);
+            s->nsym = 4;
+            s->planes = 2;
+        } else {
+            unsigned int* d_present = ctx->aux.as<unsigned int>(8);
+            DM_CUDA(cudaMemsetAsync(d_present, 0, 32, st));
+            if (nbytes) {
+                const int grid = (int)std::min<uint64_t>((nbytes + 4095) / 4096, (uint64_t)ctx->sm_count * 16);
+                census_kernel<<<std::max(grid, 1), 256, 0, st>>>(d_raw, nbytes,
+                                                                 reinterpret_cast<unsigned long long*>(d_present));
+                DM_CUDA(cudaGetLastError());
+            }
+            lut_kernel<<<1, 256, 0, st>>>(d_present, d_lut);
             DM_CUDA(cudaGetLastError());
+            unsigned int present[8];
+            DM_CUDA(cudaMemcpyAsync(present, d_present, 32, cudaMemcpyDeviceToHost, st));
+            DM_CUDA(cudaStreamSynchronize(st));
+            int nsym = 0;
+            for (int c = 0; c < 256; ++c)
+                if (present[c >> 5] & (1u << (c & 31))) {
+                    s->code_of[c] = (uint8_t)nsym++;
+                    s->present[c] = true;
+                }
+            s->nsym = nsym;
+            s->planes = nsym <= 4 ? 2 : (nsym <= 32 ? 5 : 8);
+        }
+
+        s->d_codes = (uint8_t*)ctx->ss_codes.get(o + 16);
+        s->d_planes = ctx->ss_planes.as<uint64_t>(std::max<uint64_t>(b, 1) * s->planes);
+        if (d_packed) {
+            s->d_raw = nullptr;  // the residues stay packed; only the codes are built
+            if (n) {
+                const int grid = (int)std::min<uint64_t>((n + 7) / 8, (uint64_t)ctx->sm_count * 16);
+                recode_packed_kernel<<<grid, 256, 0, st>>>(d_packed, s->d_raw_off, s->d_off, n, s->d_codes);
+                DM_CUDA(cudaGetLastError());
+            }
+        } else {
+            DM_CUDA(cudaMemsetAsync(s->d_codes, 0, o + 16, st));
+            if (n) {
+                const int grid = (int)std::min<uint64_t>((n + 7) / 8, (uint64_t)ctx->sm_count * 16);
+                recode_kernel<<<grid, 256, 0, st>>>(d_raw, s->d_raw_off, s->d_off, n, d_lut, s->d_codes);
+                DM_CUDA(cudaGetLastError());
+            }
         }
         if (b) {
             const int grid = (int)std::min<uint64_t>((b + 255) / 256, (uint64_t)ctx->sm_count * 16);
@@ -346,6 +394,7 @@ dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets,
 
 dm_seqset::~dm_seqset() {
     if (d_raw && owns_raw) cudaFreeAsync(d_raw, ctx->stream);
+    if (!owns_meta) return;
     if (d_raw_off) cudaFreeAsync(d_raw_off, ctx->stream);
     if (d_codes) cudaFreeAsync(d_codes, ctx->stream);
     if (d_off) cudaFreeAsync(d_off, ctx->stream);

@@ -75,3 +75,27 @@ def test_synth_shapes_and_determinism(dm):
     d, o = dm.synth(1, scale=0.0005)
     lens = np.diff(o)
     assert len(lens) == 1000 and lens[0::2].min() >= 500 and lens[0::2].max() <= 1500
+
+
+def _np_pack(b):
+    codes = np.frombuffer(b, dtype=np.uint8)
+    k = ((codes >> 1) ^ (codes >> 2)) & 3
+    k = np.concatenate([k, np.zeros((-len(k)) % 4, dtype=np.uint8)]).reshape(-1, 4)
+    return (k[:, 0] | (k[:, 1] << 2) | (k[:, 2] << 4) | (k[:, 3] << 6)).astype(np.uint8).tobytes()
+
+
+def test_pack_nt_host(dm):
+    """The streamed path's 2-bit packer (host only): codes A0 C1 G2 T3, any
+    other byte rejected wherever it sits (SIMD body, 128-residue groups,
+    scalar tail, across the 1 Mi-residue task boundary)."""
+    from paper_2601_15458_b200._lib import lib
+    rng = np.random.default_rng(4)
+    for n in (0, 1, 3, 4, 5, 127, 128, 129, 1000, (1 << 20) - 1, (1 << 20) + 77, 3 * (1 << 20) + 5):
+        src = np.frombuffer(b"ACGT", dtype=np.uint8)[rng.integers(0, 4, n)].tobytes()
+        dst = (C.c_uint8 * max(1, (n + 3) // 4))()
+        assert lib().dm_pack_nt(src, n, dst) == 0
+        assert bytes(dst)[:(n + 3) // 4] == _np_pack(src), n
+        for pos in {0, n // 2, n - 1} if n else ():
+            for badc in (b"N", b"a", b"-", b"\x00", b"\xc1", b"E"):
+                bad = src[:pos] + badc + src[pos + 1:]
+                assert lib().dm_pack_nt(bad, n, dst) != 0, (n, pos, badc)

@@ -193,3 +193,61 @@ def test_context_shared_by_threads(dm, ctx, orc):
         got = list(ex.map(work, range(len(pairs))))
     assert [g[0] for g in got] == want and [g[1] for g in got] == want
     assert all(g[2] == dm.nw_align(a + "A", b + "C", ctx=ctx).score for g, (a, b) in zip(got, pairs))
+
+
+@pytest.mark.parametrize("chunk", ["100000", "5000000"])
+def test_packed_upload_matches_raw_upload(dm, ctx, orc, monkeypatch, chunk):
+    """2-bit upload of A/C/G/T chunks (all of each chunk, or the default
+    packed head + raw tail) == raw upload, bit for bit; a chunk with any
+    other byte (here 'N', lower case) goes up raw. h2d_bytes shows which
+    happened."""
+    monkeypatch.setenv("DM_STREAM_CHUNK_BYTES", chunk)
+    data, offs = dm.synth(1, scale=0.005)  # 5000 pairs, ~10 MB
+    n = (len(offs) - 1) // 2
+    full, sf = dm.lev_pairs_packed(data, offs, ctx, stats=True)
+    monkeypatch.setenv("DM_STREAM_PACK_FRAC", "0.6")
+    split, sp = dm.lev_pairs_packed(data, offs, ctx, stats=True)
+    monkeypatch.setenv("DM_STREAM_PACK", "0")
+    raw, sr = dm.lev_pairs_packed(data, offs, ctx, stats=True)
+    monkeypatch.delenv("DM_STREAM_PACK")
+    monkeypatch.delenv("DM_STREAM_PACK_FRAC")
+    assert np.array_equal(split, raw) and np.array_equal(full, raw)
+    # the host-counted bucket histogram (fully packed chunks) == the device one
+    assert (sf["cells"], sf["cells_executed"], sf["launches"]) == (sr["cells"], sr["cells_executed"], sr["launches"])
+    assert sr["h2d_bytes"] >= len(data) + 8 * (len(offs) - 1)
+    assert sf["h2d_bytes"] < 0.3 * len(data) + 8 * len(offs) + 64 * 1000
+    assert sf["h2d_bytes"] < sp["h2d_bytes"] < sr["h2d_bytes"]
+    assert sp["d2h_bytes"] == 4 * n
+    # dirty bytes in the middle and near the end: those chunks go up raw
+    dirty = bytearray(data)
+    for p in (len(dirty) // 2, len(dirty) - 3):
+        dirty[p] = ord("N")
+    dirty[int(offs[10])] = ord("a")
+    dirty = bytes(dirty)
+    got, sd = dm.lev_pairs_packed(dirty, offs, ctx, stats=True)
+    assert sf["h2d_bytes"] < sd["h2d_bytes"] < sr["h2d_bytes"] or chunk == "5000000"
+    for i in list(range(0, 40)) + list(range(n // 2 - 30, n // 2 + 30)) + list(range(n - 20, n)):
+        a = dirty[offs[2 * i]:offs[2 * i + 1]]
+        b = dirty[offs[2 * i + 1]:offs[2 * i + 2]]
+        assert got[i] == orc.levenshtein(a, b), i
+    assert np.array_equal(got[np.r_[100:n // 2 - 100]], raw[100:n // 2 - 100])
+
+
+@pytest.mark.parametrize("frac", ["1", "0.5"])
+@pytest.mark.parametrize("alphabet", ["ACGT", "GT"])
+@pytest.mark.parametrize("n", [1, 15, 16, 17, 63, 64, 65, 1000, 5000])
+def test_packed_upload_odd_lengths(dm, ctx, orc, monkeypatch, n, alphabet, frac):
+    """Chunk residue counts around the unpacker's 16-residue groups, chunks
+    missing some of A/C/G/T, fully and partly packed chunks."""
+    monkeypatch.setenv("DM_STREAM_CHUNK_BYTES", "1")  # one pair per chunk
+    monkeypatch.setenv("DM_STREAM_PACK_FRAC", frac)
+    rng = random.Random(n)
+    seqs = []
+    for k in range(6):
+        la = max(0, n + k - 3)
+        seqs += [rand_str(rng, la, alphabet), rand_str(rng, max(0, n - k), alphabet)]
+    data = "".join(seqs).encode()
+    offs = np.zeros(len(seqs) + 1, dtype=np.uint64)
+    offs[1:] = np.cumsum([len(x) for x in seqs])
+    got = dm.lev_pairs_packed(data, offs, ctx)
+    assert list(got) == [orc.levenshtein(seqs[2 * i], seqs[2 * i + 1]) for i in range(6)]
