@@ -123,6 +123,12 @@ int dm_lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, 
  * dst[j/4], codes A0 C1 G2 T3, last byte zero-padded; DM_EINVAL if src holds
  * any other byte. dst: (n+3)/4 bytes. */
 int dm_pack_nt(const char* src, uint64_t n, uint8_t* dst);
+/* Per-sequence form, the streamed path's upload layout: sequence i of
+ * data[offsets[i], offsets[i+1]) (n sequences) takes 32*ceil(L/128) bytes
+ * (residue j at bits 2(j%16) of little-endian 32-bit word j/16, zero pad),
+ * back to back; *bytes = total. dst: 32-B aligned, sum of L/4 + 32 bytes
+ * suffices. */
+int dm_pack_nt_seqs(const char* data, const uint64_t* offsets, uint64_t n, uint8_t* dst, uint64_t* bytes);
 /* distance_scan: out[i] = levenshtein(seq from, seq members[i]). */
 int dm_lev_one_to_many(dm_ctx* ctx, const dm_seqset* s, uint32_t from, const uint32_t* members,
                        uint64_t n, uint32_t* out, dm_stats* st);

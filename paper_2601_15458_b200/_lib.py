@@ -78,6 +78,7 @@ SIGNATURES = {
     "dm_lev_pairs_device": (C.c_int, [_P, _P, _P, _P, C.c_uint64, _P, C.POINTER(dm_stats)]),
     "dm_lev_pairs_packed": (C.c_int, [_P, C.c_void_p, _u64p, C.c_uint64, _u32p, C.POINTER(dm_stats)]),
     "dm_pack_nt": (C.c_int, [C.c_char_p, C.c_uint64, C.c_void_p]),
+    "dm_pack_nt_seqs": (C.c_int, [C.c_char_p, _u64p, C.c_uint64, C.c_void_p, C.POINTER(C.c_uint64)]),
     "dm_lev_one_to_many": (C.c_int, [_P, _P, C.c_uint32, _u32p, C.c_uint64, _u32p, C.POINTER(dm_stats)]),
     "dm_geometric_median": (C.c_int, [_P, _P, _u32p, C.c_uint64, C.c_uint64, C.c_uint64, _u32p]),
     "dm_build_tree": (C.c_int, [_P, _P, C.c_uint64, C.c_uint64, C.POINTER(dm_node), _u64p, _u32p,

@@ -135,6 +135,22 @@ private:
     }
 };
 
+namespace dm {
+// Bytes sequence i of length L occupies in a set's code buffer: with 2
+// bit-planes (<= 4 symbols) the codes are stored 2 bits per residue, residue
+// j at bits 2(j%16) of 32-bit word j/16, in whole 32-B blocks of 128 residues
+// (zero past the end; the host packer writes each block with one aligned
+// streaming store); otherwise one byte per residue in 16-B aligned runs with
+// >= 1 pad byte. Host packer (host_pack.cpp), seqset builders and the
+// distance kernel share this.
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+inline uint64_t code_bytes(uint64_t L, int planes) {
+    return planes == 2 ? ((L + 127) >> 7) << 5 : (L + 16) & ~uint64_t(15);
+}
+}  // namespace dm
+
 // Device-resident sequence store.
 struct dm_seqset {
     dm_ctx* ctx = nullptr;
@@ -152,7 +168,7 @@ struct dm_seqset {
     uint8_t* d_raw = nullptr;      // raw residue bytes (what NW scores and the MSA prints)
     bool owns_raw = true;
     uint64_t* d_raw_off = nullptr;
-    uint8_t* d_codes = nullptr;    // dense codes 0..nsym-1, 16-B aligned per sequence
+    uint8_t* d_codes = nullptr;    // dense codes 0..nsym-1, laid out by code_bytes()
     uint64_t* d_off = nullptr;
     uint32_t* d_len = nullptr;
     uint64_t* d_blk = nullptr;
@@ -221,11 +237,12 @@ dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets,
 // call on ctx, which must be stream-ordered after every use). acgt: the caller
 // knows every byte is A/C/G/T (the streamed packer checked), so the census
 // and its host sync are skipped (codes A0 C1 G2 T3, 2 bit-planes).
-// d_packed (with acgt): the residues as 2-bit codes (host_pack.h layout,
-// relative to h_offs[0]); d_raw is then unused and left null in the set.
+// d_codes_given (with acgt): the code buffer itself, already on the device
+// in the code_bytes() layout (the streamed packer writes it on the host);
+// d_raw is then unused and left null in the set.
 dm_seqset* seqset_create_device(dm_ctx* ctx, const uint8_t* d_raw, const uint64_t* d_offs,
                                 const uint64_t* h_offs, uint32_t n, bool acgt = false,
-                                const uint8_t* d_packed = nullptr);
+                                const uint8_t* d_codes_given = nullptr);
 
 // Guide tree (tree.cu / tree_host.cpp).
 void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_cap,

@@ -109,41 +109,109 @@ inline bool pack_scalar(const uint8_t* s, uint64_t n, uint8_t* d) {
     return true;
 }
 
-// 128 residues -> 32 bytes per step: per 32-residue vector, codes by
-// shift/xor, validity by PSHUFB lookup, 4 codes per byte by two
-// multiply-adds; four vectors are narrowed with PACKUS and put back in order
-// by one lane permute, and the 32 bytes go out with a streaming store (the
-// copy engine reads them next, not this core).
-__attribute__((target("avx2"))) bool pack_avx2(const uint8_t* s, uint64_t n, uint8_t* d) {
+// 128 residues -> 32 bytes: per 32-residue vector, codes by shift/xor,
+// validity by PSHUFB lookup, 4 codes per byte by two multiply-adds; four
+// vectors are narrowed with PACKUS and put back in order by one lane
+// permute. Streaming store when the caller's destination allows it (the copy
+// engine reads the bytes next, not this core).
+__attribute__((target("avx2"))) inline bool block128_avx2(const uint8_t* s, uint8_t* d, bool stream) {
     const __m256i three = _mm256_set1_epi8(3);
     const __m256i lut = _mm256_setr_epi8('A', 'C', 'G', 'T', 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0,
                                          'A', 'C', 'G', 'T', 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0);
     const __m256i w14 = _mm256_set1_epi16(0x0401);       // k0 + 4 k1
     const __m256i w116 = _mm256_set1_epi32(0x00100001);  // p0 + 16 p1
     const __m256i order = _mm256_setr_epi32(0, 4, 1, 5, 2, 6, 3, 7);
+    __m256i bad = _mm256_setzero_si256(), p[4];
+#pragma GCC unroll 4
+    for (int u = 0; u < 4; ++u) {
+        const __m256i x = _mm256_loadu_si256((const __m256i*)(s + 32 * u));
+        const __m256i k = _mm256_and_si256(_mm256_xor_si256(_mm256_srli_epi16(x, 1), _mm256_srli_epi16(x, 2)), three);
+        bad = _mm256_or_si256(bad, _mm256_xor_si256(_mm256_shuffle_epi8(lut, k), x));
+        p[u] = _mm256_madd_epi16(_mm256_maddubs_epi16(k, w14), w116);  // one byte per dword
+    }
+    const __m256i q = _mm256_packus_epi16(_mm256_packus_epi32(p[0], p[1]), _mm256_packus_epi32(p[2], p[3]));
+    const __m256i r = _mm256_permutevar8x32_epi32(q, order);
+    if (stream) _mm256_stream_si256((__m256i*)d, r);
+    else _mm256_storeu_si256((__m256i*)d, r);
+    return _mm256_testz_si256(bad, bad);
+}
+
+// The last < 128 residues of a sequence in place: 128 bytes are read from s
+// (the caller guarantees they are readable), those at rem and beyond count
+// as 'A'; 32 bytes are written.
+__attribute__((target("avx2"))) inline bool tail_avx2(const uint8_t* s, uint64_t rem, uint8_t* d) {
+    alignas(32) uint8_t buf[128];
+    const __m256i A = _mm256_set1_epi8('A');
+    const __m256i idx0 = _mm256_setr_epi8(0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21,
+                                          22, 23, 24, 25, 26, 27, 28, 29, 30, 31);
+    const __m256i lim = _mm256_set1_epi8((char)rem);  // rem < 128: signed compare is exact
+#pragma GCC unroll 4
+    for (int u = 0; u < 4; ++u) {
+        const __m256i idx = _mm256_add_epi8(idx0, _mm256_set1_epi8((char)(32 * u)));
+        const __m256i keep = _mm256_cmpgt_epi8(lim, idx);  // idx < rem
+        const __m256i x = _mm256_loadu_si256((const __m256i*)(s + 32 * u));
+        _mm256_store_si256((__m256i*)(buf + 32 * u), _mm256_blendv_epi8(A, x, keep));
+    }
+    return block128_avx2(buf, d, true);
+}
+
+__attribute__((target("avx2"))) bool pack_avx2(const uint8_t* s, uint64_t n, uint8_t* d) {
     const bool aligned = ((uintptr_t)d & 31) == 0;
     uint64_t i = 0;
-    for (; i + 128 <= n; i += 128) {
-        __m256i bad = _mm256_setzero_si256(), p[4];
-#pragma GCC unroll 4
-        for (int u = 0; u < 4; ++u) {
-            const __m256i x = _mm256_loadu_si256((const __m256i*)(s + i + 32 * u));
-            const __m256i k =
-                _mm256_and_si256(_mm256_xor_si256(_mm256_srli_epi16(x, 1), _mm256_srli_epi16(x, 2)), three);
-            bad = _mm256_or_si256(bad, _mm256_xor_si256(_mm256_shuffle_epi8(lut, k), x));
-            p[u] = _mm256_madd_epi16(_mm256_maddubs_epi16(k, w14), w116);  // one byte per dword
-        }
-        if (!_mm256_testz_si256(bad, bad)) {
+    for (; i + 128 <= n; i += 128)
+        if (!block128_avx2(s + i, d + i / 4, aligned)) {
             _mm_sfence();
             return false;
         }
-        const __m256i q = _mm256_packus_epi16(_mm256_packus_epi32(p[0], p[1]), _mm256_packus_epi32(p[2], p[3]));
-        const __m256i r = _mm256_permutevar8x32_epi32(q, order);
-        if (aligned) _mm256_stream_si256((__m256i*)(d + i / 4), r);
-        else _mm256_storeu_si256((__m256i*)(d + i / 4), r);
-    }
     _mm_sfence();
     return pack_scalar(s + i, n - i, d + i / 4);
+}
+
+// One sequence into its code_bytes(L, 2) region (32 B per started block of
+// 128 residues, zero past the end), every block with one aligned streaming
+// store. The tail block reads 128 bytes in place (past the sequence, into
+// the next one) unless that would cross src_end; then it goes through a
+// buffer, so nothing past the input is read.
+template <bool AVX>
+inline bool pack_seq(const uint8_t* s, uint64_t L, uint8_t* d, const uint8_t* src_end) {
+    uint64_t i = 0;
+    for (; i + 128 <= L; i += 128) {
+        bool ok;
+        if constexpr (AVX) ok = block128_avx2(s + i, d + i / 4, true);
+        else ok = pack_scalar(s + i, 128, d + i / 4);
+        if (!ok) return false;
+    }
+    const uint64_t rem = L - i;
+    if (rem == 0) return true;
+    if constexpr (AVX) {
+        if (s + i + 128 <= src_end) return tail_avx2(s + i, rem, d + i / 4);
+    }
+    alignas(32) uint8_t tail[128];
+    std::memset(tail, 'A', sizeof(tail));
+    std::memcpy(tail, s + i, rem);
+    if constexpr (AVX) return block128_avx2(tail, d + i / 4, true);
+    else return pack_scalar(tail, 128, d + i / 4);
+}
+
+__attribute__((target("avx2"))) bool pack_seqs_avx2(const uint8_t* data, const uint64_t* offs, uint64_t lo,
+                                                      uint64_t hi, uint8_t* d, const uint8_t* src_end) {
+    bool ok = true;
+    for (uint64_t k = lo; k < hi && ok; ++k) {
+        const uint64_t L = offs[k + 1] - offs[k];
+        ok = pack_seq<true>(data + offs[k], L, d, src_end);
+        d += ((L + 127) >> 7) << 5;
+    }
+    _mm_sfence();
+    return ok;
+}
+
+bool pack_seqs_scalar(const uint8_t* data, const uint64_t* offs, uint64_t lo, uint64_t hi, uint8_t* d) {
+    for (uint64_t k = lo; k < hi; ++k) {
+        const uint64_t L = offs[k + 1] - offs[k];
+        if (!pack_seq<false>(data + offs[k], L, d, nullptr)) return false;
+        d += ((L + 127) >> 7) << 5;
+    }
+    return true;
 }
 
 bool have_avx2() {
@@ -158,6 +226,31 @@ unsigned host_pool_threads() { return pool().threads(); }
 
 bool pack_acgt_serial(const uint8_t* src, uint64_t n, uint8_t* dst) {
     return have_avx2() ? pack_avx2(src, n, dst) : pack_scalar(src, n, dst);
+}
+
+bool pack_acgt_seqs(const char* data, const uint64_t* offs, uint64_t n, uint8_t* dst, uint64_t* bytes) {
+    // sequences per task: >= 4 tasks per pool thread (balance), >= 256 (overhead)
+    const uint64_t per = std::max<uint64_t>(256, (n + 4 * host_pool_threads() - 1) / (4 * host_pool_threads()));
+    const uint64_t ntasks = (n + per - 1) / per;
+    std::vector<uint64_t> base(ntasks + 1, 0);
+    host_pool_run(ntasks, [&](uint64_t t) {
+        uint64_t sum = 0;
+        for (uint64_t k = t * per, e = std::min(n, k + per); k < e; ++k) sum += ((offs[k + 1] - offs[k] + 127) >> 7) << 5;
+        base[t + 1] = sum;
+    });
+    for (uint64_t t = 0; t < ntasks; ++t) base[t + 1] += base[t];
+    *bytes = base[ntasks];
+    std::atomic<bool> bad{false};
+    const uint8_t* d8 = reinterpret_cast<const uint8_t*>(data);
+    const bool avx = have_avx2();
+    host_pool_run(ntasks, [&](uint64_t t) {
+        if (bad.load(std::memory_order_relaxed)) return;
+        const uint64_t lo = t * per, hi = std::min(n, lo + per);
+        const bool ok = avx ? pack_seqs_avx2(d8, offs, lo, hi, dst + base[t], d8 + offs[n])
+                            : pack_seqs_scalar(d8, offs, lo, hi, dst + base[t]);
+        if (!ok) bad.store(true, std::memory_order_relaxed);
+    });
+    return !bad.load();
 }
 
 bool pack_acgt(const uint8_t* src, uint64_t n, uint8_t* dst) {

@@ -19,6 +19,13 @@ unsigned host_pool_threads();
 // byte other than 'A', 'C', 'G', 'T' is seen. Multithreaded.
 bool pack_acgt(const uint8_t* src, uint64_t n, uint8_t* dst);
 
+// Sequences offs[0..n] of data (absolute offsets) packed one by one into the
+// 2-bit code layout of a sequence set (code_bytes(L, 2) bytes each: 32 B per
+// started 128-residue block, zero-padded), i.e. the device code buffer
+// itself; dst must be 32-B aligned; *bytes = its size. False (dst
+// unspecified) if a byte is not A/C/G/T. Multithreaded.
+bool pack_acgt_seqs(const char* data, const uint64_t* offs, uint64_t n, uint8_t* dst, uint64_t* bytes);
+
 // Single-threaded kernel of pack_acgt over [src, src+n) (n % 4 == 0 except
 // for the last piece); exposed for tests.
 bool pack_acgt_serial(const uint8_t* src, uint64_t n, uint8_t* dst);

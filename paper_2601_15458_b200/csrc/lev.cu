@@ -179,12 +179,13 @@ __global__ void __launch_bounds__(256, NP == 2 ? 3 : 1) lev_kernel(const LevArgs
         // One text column through the lane pipeline. CHK: some lane of the
         // warp may be outside its text (pipeline fill/drain, shorter texts of
         // other groups, the final column); the steady state skips the checks.
-        auto column = [&](uint32_t s, auto chk, uint32_t own) {
+        // ownw: lane 0's own word for this column, code << 2 | 1 (h_in = +1)
+        auto column = [&](uint32_t s, auto chk, uint32_t ownw) {
             constexpr bool CHK = decltype(chk)::value;
             // word = code << 2 | h_minus << 1 | h_plus; lane 0 synthesises its
-            // own (text code `own`, h_in = +1). Branch-free select on a mask.
+            // own (text code, h_in = +1). Branch-free select on a mask.
             const uint32_t recv = __shfl_up_sync(FULL, word, 1, G);
-            const uint32_t r = lop3<0xCA>(leadmask, imad(own, four, a.one), recv);  // lead ? own word : recv
+            const uint32_t r = lop3<0xCA>(leadmask, ownw, recv);  // lead ? own word : recv
             const uint32_t c = r >> 2;
             uint32_t hm = (r >> 1) & 1u;
             uint32_t hp = r & 1u;
@@ -256,17 +257,53 @@ __global__ void __launch_bounds__(256, NP == 2 ? 3 : 1) lev_kernel(const LevArgs
         uint32_t nmin = __reduce_min_sync(FULL, valid ? n : 0xffffffffu);
         const uint32_t s1 = nmin == 0xffffffffu || nmin == 0 ? 0u : nmin - 1u;
         const uint32_t s0 = min((uint32_t)G - 1u, s1);
-        auto code_at = [&](uint32_t s) -> uint32_t { return (lead && s < n) ? (uint32_t)__ldg(tp + s) : 0u; };
+        // text codes: 2 bits per residue (16 per word) when TAB, else bytes (code_bytes())
+        const uint32_t* tw = reinterpret_cast<const uint32_t*>(tp);
+        auto code_at = [&](uint32_t s) -> uint32_t {  // as a lane-0 word (code << 2 | 1)
+            uint32_t c = 0u;
+            if (lead && s < n) {
+                if constexpr (TAB) c = (__ldg(tw + (s >> 4)) >> ((s & 15u) * 2u)) & 3u;
+                else c = (uint32_t)__ldg(tp + s);
+            }
+            return imad(c, four, a.one);
+        };
         uint32_t s = 0;
         for (; s < s0; ++s) column(s, std::true_type{}, code_at(s));
-        // steady state, four columns per text load (16-B aligned code runs)
+        if constexpr (TAB) {
+            // steady state, 16 columns per text word (2-bit codes), taken 4 at a
+            // time from a register (the 4-column body is not unrolled further:
+            // instruction cache)
+            for (; s < s1 && (s & 15u); ++s) column(s, std::false_type{}, code_at(s));
+            for (; s + 16 <= s1; s += 16) {
+                uint32_t w16 = lead ? __ldg(tw + (s >> 4)) : 0u;
+#pragma unroll 1
+                for (uint32_t q = 0; q < 16; q += 4) {
+                    // word k = (code_k << 2) | 1, one or two ops each
+                    column(s + q, std::false_type{}, lop3<0xEA>(w16 << 2, 0xcu, 1u));
+                    column(s + q + 1, std::false_type{}, lop3<0xEA>(w16, 0xcu, 1u));
+                    column(s + q + 2, std::false_type{}, lop3<0xEA>(w16 >> 2, 0xcu, 1u));
+                    column(s + q + 3, std::false_type{}, lop3<0xEA>(w16 >> 4, 0xcu, 1u));
+                    w16 >>= 8;
+                }
+            }
+        }
+        // steady state, four columns per text load (4-aligned code runs)
         for (; s < s1 && (s & 3u); ++s) column(s, std::false_type{}, code_at(s));
         for (; s + 4 <= s1; s += 4) {
-            const uint32_t t4 = lead ? __ldg(reinterpret_cast<const uint32_t*>(tp + s)) : 0u;
-            column(s, std::false_type{}, t4 & 0xffu);
-            column(s + 1, std::false_type{}, __byte_perm(t4, 0u, 0x4441u));
-            column(s + 2, std::false_type{}, __byte_perm(t4, 0u, 0x4442u));
-            column(s + 3, std::false_type{}, t4 >> 24);
+            if constexpr (TAB) {
+                // 4 codes in bits 0..7 of t4; word k = (code_k << 2) | 1, one or two ops each
+                const uint32_t t4 = lead ? __ldg(tw + (s >> 4)) >> ((s & 12u) * 2u) : 0u;
+                column(s, std::false_type{}, lop3<0xEA>(t4 << 2, 0xcu, 1u));
+                column(s + 1, std::false_type{}, lop3<0xEA>(t4, 0xcu, 1u));
+                column(s + 2, std::false_type{}, lop3<0xEA>(t4 >> 2, 0xcu, 1u));
+                column(s + 3, std::false_type{}, lop3<0xEA>(t4 >> 4, 0xcu, 1u));
+            } else {
+                const uint32_t t4 = lead ? __ldg(reinterpret_cast<const uint32_t*>(tp + s)) : 0u;
+                column(s, std::false_type{}, imad(t4 & 0xffu, four, a.one));
+                column(s + 1, std::false_type{}, imad(__byte_perm(t4, 0u, 0x4441u), four, a.one));
+                column(s + 2, std::false_type{}, imad(__byte_perm(t4, 0u, 0x4442u), four, a.one));
+                column(s + 3, std::false_type{}, imad(t4 >> 24, four, a.one));
+            }
         }
         for (; s < s1; ++s) column(s, std::false_type{}, code_at(s));
         for (; s < steps; ++s) column(s, std::true_type{}, code_at(s));

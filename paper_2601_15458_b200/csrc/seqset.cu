@@ -1,6 +1,7 @@
 // Device-resident sequence store: raw residues, a dense
-// re-coding of the residues for the distance engine, and per-sequence
-// bit-plane profiles.
+// re-coding of the residues for the distance engine (2 bits per residue when
+// at most 4 symbols occur, else a byte; layout code_bytes()), and
+// per-sequence bit-plane profiles.
 //
 // Levenshtein compares raw bytes (distance.cpp:40 `ai != b[j]`),
 // so the code map is a bijection over the bytes that actually occur: S
@@ -82,21 +83,39 @@ __global__ void recode_kernel(const uint8_t* __restrict__ raw, const uint64_t* _
     }
 }
 
-// Same from 2-bit packed residues (streamed A/C/G/T chunks: the packed codes
-// are the codes, A0 C1 G2 T3); also zeroes each sequence's padding, so the
-// code buffer needs no memset.
-__global__ void recode_packed_kernel(const uint8_t* __restrict__ packed, const uint64_t* __restrict__ raw_off,
-                                     const uint64_t* __restrict__ off, uint32_t n, uint8_t* __restrict__ codes) {
+// 2-bit code layout (<= 4 symbols, code_bytes()): one warp per sequence,
+// one lane per 16-residue word; the padding words come out zero, so the code
+// buffer needs no memset.
+__global__ void recode2_kernel(const uint8_t* __restrict__ raw, const uint64_t* __restrict__ raw_off,
+                               const uint64_t* __restrict__ off, uint32_t n,
+                               const uint8_t* __restrict__ lut, uint32_t* __restrict__ codes) {
+    __shared__ uint8_t slut[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) slut[i] = lut[i];
+    __syncthreads();
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t s = warp; s < n; s += nw) {
-        const uint64_t a = raw_off[s], e = raw_off[s + 1], o = off[s], span = off[s + 1] - o;
-        for (uint64_t i = lane; i < span; i += 32) {
-            const uint64_t r = a + i;
-            codes[o + i] = r < e ? (uint8_t)((packed[r >> 2] >> ((r & 3) * 2)) & 3u) : (uint8_t)0;
+        const uint64_t a = raw_off[s], e = raw_off[s + 1], o = off[s] >> 2, words = (off[s + 1] >> 2) - o;
+        for (uint64_t w = lane; w < words; w += 32) {
+            uint32_t v = 0;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const uint64_t r = a + w * 16 + k;
+                if (r < e) v |= (uint32_t)slut[raw[r]] << (2 * k);
+            }
+            codes[o + w] = v;
         }
     }
+}
+
+// Even bits of x (bits 0, 2, .., 30) gathered into the low 16 bits.
+__device__ __forceinline__ uint32_t even_bits(uint32_t x) {
+    x &= 0x55555555u;
+    x = (x | (x >> 1)) & 0x33333333u;
+    x = (x | (x >> 2)) & 0x0f0f0f0fu;
+    x = (x | (x >> 4)) & 0x00ff00ffu;
+    return (x | (x >> 8)) & 0x0000ffffu;
 }
 
 template <int NP>
@@ -123,6 +142,20 @@ __global__ void planes_kernel(const uint8_t* __restrict__ codes, const uint64_t*
         uint64_t w[NP];
 #pragma unroll
         for (int k = 0; k < NP; ++k) w[k] = 0;
+        if constexpr (NP == 2) {
+            // 2-bit codes: 64 residues = 4 words; plane k = bit k of every code
+            const uint32_t* pw = reinterpret_cast<const uint32_t*>(codes + off[s]) + local * 4;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t x = q * 16 < cnt ? pw[q] : 0u;
+                w[0] |= (uint64_t)even_bits(x) << (16 * q);
+                w[1] |= (uint64_t)even_bits(x >> 1) << (16 * q);
+            }
+            const uint64_t keep = cnt >= 64 ? ~0ull : ((1ull << cnt) - 1ull);
+            planes[b * 2] = w[0] & keep;
+            planes[b * 2 + 1] = w[1] & keep;
+            continue;
+        }
         // codes are 16-B aligned per sequence and zero-padded past the end
         const uint4* pv = reinterpret_cast<const uint4*>(p);
         for (int q = 0; q < (cnt + 15) / 16; ++q) {
@@ -143,8 +176,8 @@ __global__ void planes_kernel(const uint8_t* __restrict__ codes, const uint64_t*
 
 // Per-sequence metadata from absolute device offsets (streamed batches):
 // relative raw offsets, lengths and the padded sizes the two scans turn into
-// code offsets (16-B aligned, >= 1 pad byte) and first plane block.
-__global__ void meta_kernel(const uint64_t* __restrict__ offs, uint32_t n, uint64_t* __restrict__ raw_off,
+// code offsets (code_bytes() layout) and first plane block.
+__global__ void meta_kernel(const uint64_t* __restrict__ offs, uint32_t n, int planes, uint64_t* __restrict__ raw_off,
                             uint32_t* __restrict__ len, uint64_t* __restrict__ code_sz,
                             uint64_t* __restrict__ blk_sz) {
     const uint64_t base = offs[0];
@@ -153,7 +186,7 @@ __global__ void meta_kernel(const uint64_t* __restrict__ offs, uint32_t n, uint6
         if (i < n) {
             const uint64_t L = offs[i + 1] - offs[i];
             len[i] = (uint32_t)L;
-            code_sz[i] = (L + 16) & ~uint64_t(15);
+            code_sz[i] = code_bytes(L, planes);
             blk_sz[i] = (L + 63) / 64;
         } else {
             code_sz[i] = 0;
@@ -180,44 +213,17 @@ __global__ void acgt_lut_kernel(uint8_t* __restrict__ lut) {
 }  // namespace
 
 dm_seqset* seqset_create_device(dm_ctx* ctx, const uint8_t* d_raw, const uint64_t* d_offs,
-                                const uint64_t* h_offs, uint32_t n, bool acgt, const uint8_t* d_packed) {
+                                const uint64_t* h_offs, uint32_t n, bool acgt, const uint8_t* d_codes_given) {
     auto* s = new dm_seqset;
     s->ctx = ctx;
     s->n = n;
     s->owns_raw = false;
     s->d_raw = const_cast<uint8_t*>(d_raw);
     try {
-        uint64_t o = 0, b = 0;
-        for (uint32_t i = 0; i < n; ++i) {
-            const uint64_t L = h_offs[i + 1] - h_offs[i];
-            if (L > 0xffffffffull) throw invalid_argument("sequence longer than 2^32-1 residues");
-            o += (L + 16) & ~uint64_t(15);
-            b += (L + 63) / 64;
-        }
-        s->total_blocks = b;
+        if (d_codes_given && !acgt) throw invalid_argument("given codes need a known A/C/G/T alphabet");
         const uint64_t nbytes = h_offs[n] - h_offs[0];
         cudaStream_t st = ctx->stream;
-        // device arrays from the context's scratch: no pool traffic per chunk
-        s->owns_meta = false;
-        const size_t a8 = ((size_t)(n + 1) * 8 + 255) & ~size_t(255), a4 = ((size_t)n * 4 + 259) & ~size_t(255);
-        char* meta = (char*)ctx->ss_meta.get(3 * a8 + a4);
-        s->d_raw_off = (uint64_t*)meta;
-        s->d_off = (uint64_t*)(meta + a8);
-        s->d_blk = (uint64_t*)(meta + 2 * a8);
-        s->d_len = (uint32_t*)(meta + 3 * a8);
-        size_t cub_b = 0;
-        DM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, cub_b, (uint64_t*)nullptr, (uint64_t*)nullptr, (int)n + 1, st));
-        const size_t sz_b = ((size_t)(n + 1) * 8 + 255) & ~size_t(255);
-        char* scratch = (char*)ctx->aux3.get(2 * sz_b + cub_b + 256);
-        uint64_t* code_sz = (uint64_t*)scratch;
-        uint64_t* blk_sz = (uint64_t*)(scratch + sz_b);
-        void* cub_tmp = scratch + 2 * sz_b;
-        const int mgrid = (int)std::min<uint64_t>((n + 256) / 256, (uint64_t)ctx->sm_count * 8);
-        meta_kernel<<<std::max(mgrid, 1), 256, 0, st>>>(d_offs, n, s->d_raw_off, s->d_len, code_sz, blk_sz);
-        DM_CUDA(cudaGetLastError());
-        DM_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_b, code_sz, s->d_off, (int)n + 1, st));
-        DM_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_b, blk_sz, s->d_blk, (int)n + 1, st));
-
+        // alphabet: known (packed A/C/G/T chunk) or from the device census (one host sync)
         uint8_t* d_lut = (uint8_t*)ctx->aux2.get(256);
         if (acgt) {
             acgt_lut_kernel<<<1, 256, 0, st>>>(d_lut);
@@ -252,23 +258,51 @@ dm_seqset* seqset_create_device(dm_ctx* ctx, const uint8_t* d_raw, const uint64_
             s->nsym = nsym;
             s->planes = nsym <= 4 ? 2 : (nsym <= 32 ? 5 : 8);
         }
+        uint64_t o = 0, b = 0;
+        for (uint32_t i = 0; i < n; ++i) {
+            const uint64_t L = h_offs[i + 1] - h_offs[i];
+            if (L > 0xffffffffull) throw invalid_argument("sequence longer than 2^32-1 residues");
+            o += code_bytes(L, s->planes);
+            b += (L + 63) / 64;
+        }
+        s->total_blocks = b;
+        // device arrays from the context's scratch: no pool traffic per chunk
+        s->owns_meta = false;
+        const size_t a8 = ((size_t)(n + 1) * 8 + 255) & ~size_t(255), a4 = ((size_t)n * 4 + 259) & ~size_t(255);
+        char* meta = (char*)ctx->ss_meta.get(3 * a8 + a4);
+        s->d_raw_off = (uint64_t*)meta;
+        s->d_off = (uint64_t*)(meta + a8);
+        s->d_blk = (uint64_t*)(meta + 2 * a8);
+        s->d_len = (uint32_t*)(meta + 3 * a8);
+        size_t cub_b = 0;
+        DM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, cub_b, (uint64_t*)nullptr, (uint64_t*)nullptr, (int)n + 1, st));
+        const size_t sz_b = ((size_t)(n + 1) * 8 + 255) & ~size_t(255);
+        char* scratch = (char*)ctx->aux3.get(2 * sz_b + cub_b + 256);
+        uint64_t* code_sz = (uint64_t*)scratch;
+        uint64_t* blk_sz = (uint64_t*)(scratch + sz_b);
+        void* cub_tmp = scratch + 2 * sz_b;
+        const int mgrid = (int)std::min<uint64_t>((n + 256) / 256, (uint64_t)ctx->sm_count * 8);
+        meta_kernel<<<std::max(mgrid, 1), 256, 0, st>>>(d_offs, n, s->planes, s->d_raw_off, s->d_len, code_sz, blk_sz);
+        DM_CUDA(cudaGetLastError());
+        DM_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_b, code_sz, s->d_off, (int)n + 1, st));
+        DM_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_b, blk_sz, s->d_blk, (int)n + 1, st));
 
-        s->d_codes = (uint8_t*)ctx->ss_codes.get(o + 16);
         s->d_planes = ctx->ss_planes.as<uint64_t>(std::max<uint64_t>(b, 1) * s->planes);
-        if (d_packed) {
-            s->d_raw = nullptr;  // the residues stay packed; only the codes are built
-            if (n) {
-                const int grid = (int)std::min<uint64_t>((n + 7) / 8, (uint64_t)ctx->sm_count * 16);
-                recode_packed_kernel<<<grid, 256, 0, st>>>(d_packed, s->d_raw_off, s->d_off, n, s->d_codes);
-                DM_CUDA(cudaGetLastError());
-            }
+        if (d_codes_given) {
+            s->d_raw = nullptr;  // the residues arrived as codes; there are no raw bytes
+            s->d_codes = const_cast<uint8_t*>(d_codes_given);
         } else {
-            DM_CUDA(cudaMemsetAsync(s->d_codes, 0, o + 16, st));
-            if (n) {
-                const int grid = (int)std::min<uint64_t>((n + 7) / 8, (uint64_t)ctx->sm_count * 16);
-                recode_kernel<<<grid, 256, 0, st>>>(d_raw, s->d_raw_off, s->d_off, n, d_lut, s->d_codes);
-                DM_CUDA(cudaGetLastError());
+            s->d_codes = (uint8_t*)ctx->ss_codes.get(o + 16);
+            const int grid = (int)std::min<uint64_t>((n + 7) / 8, (uint64_t)ctx->sm_count * 16);
+            if (s->planes == 2) {
+                if (n)
+                    recode2_kernel<<<grid, 256, 0, st>>>(d_raw, s->d_raw_off, s->d_off, n, d_lut,
+                                                         reinterpret_cast<uint32_t*>(s->d_codes));
+            } else {
+                DM_CUDA(cudaMemsetAsync(s->d_codes, 0, o + 16, st));
+                if (n) recode_kernel<<<grid, 256, 0, st>>>(d_raw, s->d_raw_off, s->d_off, n, d_lut, s->d_codes);
             }
+            DM_CUDA(cudaGetLastError());
         }
         if (b) {
             const int grid = (int)std::min<uint64_t>((b + 255) / 256, (uint64_t)ctx->sm_count * 16);
@@ -303,12 +337,9 @@ dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets,
             const uint64_t L = offsets[i + 1] - offsets[i];
             if (L > 0xffffffffull) throw invalid_argument("sequence longer than 2^32-1 residues");
             s->len[i] = (uint32_t)L;
-            s->off[i] = o;
             s->blk_off[i] = b;
-            o += (L + 16) & ~uint64_t(15);  // >= 1 pad byte, 16-B aligned starts
             b += (L + 63) / 64;
         }
-        s->off[n] = o;
         s->blk_off[n] = b;
         s->total_blocks = b;
         s->raw_off.assign(offsets, offsets + n + 1);
@@ -354,13 +385,18 @@ dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets,
         std::memcpy(s->code_of, lut, 256);
         s->nsym = nsym;
         s->planes = nsym <= 4 ? 2 : (nsym <= 32 ? 5 : 8);
+        for (uint32_t i = 0; i < n; ++i) {
+            s->off[i] = o;
+            o += code_bytes(s->len[i], s->planes);
+        }
+        s->off[n] = o;
 
         DM_CUDA(cudaMallocAsync(&s->d_codes, o + 16, st));
         DM_CUDA(cudaMallocAsync(&s->d_off, (n + 1) * sizeof(uint64_t), st));
         DM_CUDA(cudaMallocAsync(&s->d_len, std::max<size_t>(n, 1) * sizeof(uint32_t), st));
         DM_CUDA(cudaMallocAsync(&s->d_blk, (n + 1) * sizeof(uint64_t), st));
         DM_CUDA(cudaMallocAsync(&s->d_planes, std::max<uint64_t>(b, 1) * s->planes * sizeof(uint64_t), st));
-        DM_CUDA(cudaMemsetAsync(s->d_codes, 0, o + 16, st));
+        if (s->planes != 2) DM_CUDA(cudaMemsetAsync(s->d_codes, 0, o + 16, st));
         DM_CUDA(cudaMemcpyAsync(s->d_off, s->off.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st));
         if (n) DM_CUDA(cudaMemcpyAsync(s->d_len, s->len.data(), n * 4, cudaMemcpyHostToDevice, st));
         DM_CUDA(cudaMemcpyAsync(s->d_blk, s->blk_off.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st));
@@ -368,7 +404,11 @@ dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets,
         DM_CUDA(cudaMemcpyAsync(d_lut, lut, 256, cudaMemcpyHostToDevice, st));
         if (n) {
             const int grid = (int)std::min<uint64_t>((n + 7) / 8, (uint64_t)ctx->sm_count * 16);
-            recode_kernel<<<grid, 256, 0, st>>>(d_raw, d_raw_off, s->d_off, n, d_lut, s->d_codes);
+            if (s->planes == 2)
+                recode2_kernel<<<grid, 256, 0, st>>>(d_raw, d_raw_off, s->d_off, n, d_lut,
+                                                     reinterpret_cast<uint32_t*>(s->d_codes));
+            else
+                recode_kernel<<<grid, 256, 0, st>>>(d_raw, d_raw_off, s->d_off, n, d_lut, s->d_codes);
             DM_CUDA(cudaGetLastError());
         }
         if (b) {

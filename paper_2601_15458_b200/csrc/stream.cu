@@ -12,14 +12,15 @@
 //
 // PCIe is the end-to-end bound of the raw bytes (2 GB per cfg1 batch), so a
 // packer thread feeds the copy stream: a chunk that holds only A/C/G/T bytes
-// is packed to 2-bit codes by the host pool into a pinned slot (a quarter of
-// the bytes cross the bus). For such a chunk the planner builds the codes
-// straight from the packed bytes (recode_packed_kernel) and, knowing the
-// alphabet and the lengths, skips both host syncs: codes are A0 C1 G2 T3 and
-// the bucket histogram is counted on the host (plan_hist_host). Any other
-// chunk is uploaded as given and planned as before. DM_STREAM_PACK_FRAC < 1
-// packs only the head of each chunk (expanded by unpack_acgt next to the raw
-// tail), for hosts whose packing rate is below the bus rate.
+// is packed by the host pool, sequence by sequence, straight into the
+// sequence set's 2-bit code layout (code_bytes()) in a pinned slot; a quarter
+// of the bytes cross the bus and the uploaded buffer IS the chunk's code
+// buffer. Knowing the alphabet and the lengths, that chunk's planner skips
+// both host syncs (codes A0 C1 G2 T3; bucket histogram counted on the host,
+// plan_hist_host) and has no recode pass. Any other chunk is uploaded as
+// given and planned as before. DM_STREAM_PACK_FRAC < 1 packs only the head
+// of each chunk (flat, expanded by unpack_acgt next to the raw tail), for
+// hosts whose packing rate is below the bus rate.
 #include <algorithm>
 #include <chrono>
 #include <condition_variable>
@@ -97,16 +98,16 @@ dm_ctx* prep_context(dm_ctx* ctx, int k) {
 constexpr int NB = dm_ctx::kStreamSlots;  // chunks in flight: uploading (NB-1), planning/computing
 
 struct ChunkEvents {
-    cudaEvent_t copied[NB] = {}, recoded[NB] = {}, planned[NB] = {}, done[NB] = {}, ready = nullptr;
+    cudaEvent_t copied[NB] = {}, planned[NB] = {}, done[NB] = {}, ready = nullptr;
     ChunkEvents() {
         for (int b = 0; b < NB; ++b)
-            for (cudaEvent_t* e : {&copied[b], &recoded[b], &planned[b], &done[b]})
+            for (cudaEvent_t* e : {&copied[b], &planned[b], &done[b]})
                 DM_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         DM_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
     }
     ~ChunkEvents() {
         for (int b = 0; b < NB; ++b)
-            for (cudaEvent_t e : {copied[b], recoded[b], planned[b], done[b]})
+            for (cudaEvent_t e : {copied[b], planned[b], done[b]})
                 if (e) cudaEventDestroy(e);
         if (ready) cudaEventDestroy(ready);
     }
@@ -128,6 +129,8 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
     uint64_t big = 256ull << 20, small = 32ull << 20;
     if (const char* env = std::getenv("DM_STREAM_CHUNK_BYTES"))
         big = small = std::max<uint64_t>(1, std::strtoull(env, nullptr, 10));
+    if (const char* env = std::getenv("DM_STREAM_BIG_MB")) big = std::max<uint64_t>(1, std::strtoull(env, nullptr, 10)) << 20;
+    if (const char* env = std::getenv("DM_STREAM_SMALL_MB")) small = std::max<uint64_t>(1, std::strtoull(env, nullptr, 10)) << 20;
     std::vector<uint64_t> cb{0};
     for (uint64_t lo = 0, k = 0; lo < npairs; ++k) {
         const uint64_t rem = offsets[2 * npairs] - offsets[2 * lo];
@@ -182,11 +185,12 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
     };
     // Hand-off between the packer thread (uploads) and this thread (planning,
     // kernels): chunk c may be planned once issued > c; chunk c + NB may be
-    // uploaded into slot c % NB once recoded > c (its staging buffer is free).
+    // uploaded into slot c % NB once launched > c, behind ev.done of chunk c
+    // (a packed chunk's upload buffer is its code buffer, read by its kernels).
     struct Handoff {
         std::mutex mu;
         std::condition_variable cv;
-        uint64_t issued = 0, recoded = 0, h2d = 0;
+        uint64_t issued = 0, launched = 0;
         bool abort = false;
         std::exception_ptr err;
     } hs;
@@ -211,7 +215,8 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
         uint32_t* h_res = ctx->pin_out.as<uint32_t>(npairs);
         const char* pk = std::getenv("DM_STREAM_PACK");
         const bool pack = !(pk && pk[0] == '0');
-        const uint64_t packed_cap = (maxbytes + 3) / 4 + 16;
+        // per-sequence 2-bit layout (code_bytes): < L / 4 + 32 bytes per sequence
+        const uint64_t packed_cap = maxbytes / 4 + 32 * (2 * per) + 64;
         uint8_t* d_pack[NB] = {};
         uint8_t* h_pack[NB] = {};
         if (pack)
@@ -249,11 +254,11 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
             // chunk offsets go up from a pinned slot (a pageable copy would block
             // the host behind the bulk upload already queued)
             std::memcpy(h_offs + b * oslot, offsets + 2 * lo, (2 * (hi - lo) + 1) * 8);
-            if (c >= NB) {  // staging b is free once chunk c - NB is recoded
+            if (c >= NB) {  // slot b's device buffers are free once chunk c - NB's kernels are done
                 std::unique_lock<std::mutex> g(hs.mu);
-                hs.cv.wait(g, [&] { return hs.abort || hs.recoded > c - NB; });
+                hs.cv.wait(g, [&] { return hs.abort || hs.launched > c - NB; });
                 if (hs.abort) return false;
-                DM_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ev.recoded[b], 0));
+                DM_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ev.done[b], 0));
             }
             DM_CUDA(cudaMemcpyAsync(d_offs + b * oslot, h_offs + b * oslot, (2 * (hi - lo) + 1) * 8,
                                     cudaMemcpyHostToDevice, ctx->copy_stream));
@@ -265,13 +270,21 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
                 h2d_bytes += n - m;
             }
             const double tp0 = trace ? now_ms() : 0.0;
-            bool packed = m > 0 && pack_acgt((const uint8_t*)data + a0, m, h_pack[b]);
+            uint64_t pb = 0;  // packed bytes to upload
+            bool packed = false;
+            if (m == n && m > 0) {  // whole chunk: straight into the set's 2-bit code layout
+                // (one upload per chunk: uploading pieces while packing measured slower,
+                // the copy engine's host reads compete with the packers)
+                packed = pack_acgt_seqs(data, offsets + 2 * lo, 2 * (hi - lo), h_pack[b], &pb);
+            } else if (m > 0) {     // head only: flat 2-bit stream, expanded next to the raw tail
+                packed = pack_acgt((const uint8_t*)data + a0, m, h_pack[b]);
+                pb = (m + 15) / 16 * 4;
+            }
             if (trace)
                 std::fprintf(stderr, "[pack] chunk %llu: %.1f MB packed %.2f..%.2f ms\n", (unsigned long long)c, m / 1e6,
                              tp0, now_ms());
             acgt[c] = packed && m == n;
             if (packed) {
-                const uint64_t pb = (m + 15) / 16 * 4;
                 DM_CUDA(cudaMemcpyAsync(d_pack[b], h_pack[b], pb, cudaMemcpyHostToDevice, ctx->copy_stream));
                 DM_CUDA(cudaEventRecord(h2d_done[b], ctx->copy_stream));
                 if (trace) {
@@ -280,11 +293,11 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
                     cudaEventRecord(e, ctx->copy_stream);
                     th.push_back(e);
                 }
-                if (m < n) {  // head packed, tail raw: expand the head next to the tail
+                if (m < n) {
                     const int ug = (int)std::min<uint64_t>((m / 16 + 255) / 256 + 1, (uint64_t)ctx->sm_count * 8);
                     unpack_acgt<<<ug, 256, 0, ctx->copy_stream>>>((const uint32_t*)d_pack[b], m, stage[b]);
                     DM_CUDA(cudaGetLastError());
-                }  // else the planner builds the codes from the packed bytes directly
+                }  // else d_pack[b] is the chunk's code buffer as it stands
                 h2d_bytes += pb;
             } else {
                 if (m) DM_CUDA(cudaMemcpyAsync(stage[b], data + a0, m, cudaMemcpyHostToDevice, ctx->copy_stream));
@@ -296,7 +309,7 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
                 cudaEvent_t e;
                 cudaEventCreate(&e);
                 cudaEventRecord(e, ctx->copy_stream);
-                tc.push_back({e, packed ? (m + 3) / 4 + (n - m) : n});
+                tc.push_back({e, packed ? pb + (n - m) : n});
             }
             return true;
         };
@@ -336,17 +349,16 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
             const double t0 = trace ? now_ms() : 0.0;
             live[b] = seqset_create_device(P, stage[b], d_offs + b * oslot, offsets + 2 * lo, (uint32_t)(2 * cnt),
                                            acgt[c] != 0, acgt[c] ? d_pack[b] : nullptr);
-            DM_CUDA(cudaEventRecord(ev.recoded[b], P->stream));  // staging b free again
-            {
-                std::lock_guard<std::mutex> g(hs.mu);
-                hs.recoded = c + 1;
-            }
-            hs.cv.notify_all();
             const double t1 = trace ? now_ms() : 0.0;
             // plan on the planner stream, kernels on ctx->stream
             lev_plan_then_launch(P, ctx, live[b], d_ab, d_ab + per, cnt, d_res + lo, ev.planned[b], tot,
                                  acgt[c] ? offsets + 2 * lo : nullptr);
             DM_CUDA(cudaEventRecord(ev.done[b], ctx->stream));
+            {
+                std::lock_guard<std::mutex> g(hs.mu);
+                hs.launched = c + 1;
+            }
+            hs.cv.notify_all();
             if (trace) {  // GPU-side timeline: when chunk c's planning and kernels finished
                 cudaEvent_t a, k;
                 cudaEventCreate(&a);
@@ -427,6 +439,18 @@ extern "C" int dm_lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t
             st->h2d_bytes = tot.h2d_bytes;
             st->d2h_bytes = tot.d2h_bytes;
         }
+    });
+}
+
+extern "C" int dm_pack_nt_seqs(const char* data, const uint64_t* offsets, uint64_t n, uint8_t* dst,
+                               uint64_t* bytes) {
+    return dm::guard([&] {
+        dm::require(offsets && bytes && (data || n == 0) && (dst || n == 0), "null argument");
+        dm::require(((uintptr_t)dst & 31) == 0, "dst must be 32-byte aligned");
+        for (uint64_t i = 0; i < n; ++i)
+            if (offsets[i + 1] < offsets[i]) throw dm::invalid_argument("sequence offsets must be non-decreasing");
+        if (!dm::pack_acgt_seqs(data, offsets, n, dst, bytes))
+            throw dm::invalid_argument("not a nucleotide (A/C/G/T) buffer");
     });
 }
 

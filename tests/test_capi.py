@@ -99,3 +99,41 @@ def test_pack_nt_host(dm):
             for badc in (b"N", b"a", b"-", b"\x00", b"\xc1", b"E"):
                 bad = src[:pos] + badc + src[pos + 1:]
                 assert lib().dm_pack_nt(bad, n, dst) != 0, (n, pos, badc)
+
+
+def test_pack_nt_seqs_layout(dm):
+    """Per-sequence 2-bit layout of the streamed upload (= the device code
+    buffer of a <= 4-symbol set): 32 bytes per started 128-residue block,
+    residue j at bits 2(j%16) of 32-bit word j/16, zero padding."""
+    for lens in ([0, 1, 15, 16, 17, 31, 32, 127, 128, 129, 255, 256, 1000, 3]
+                 + list(np.random.default_rng(7).integers(0, 3000, 9000)),
+                 list(np.random.default_rng(8).integers(0, 40, 20000)) + [5, 0, 2]):
+        _check_pack_seqs(lens)
+
+
+def _check_pack_seqs(lens):
+    from paper_2601_15458_b200._lib import lib
+    rng = np.random.default_rng(len(lens))
+    seqs = [np.frombuffer(b"ACGT", dtype=np.uint8)[rng.integers(0, 4, L)].tobytes() for L in lens]
+    data = b"".join(seqs)
+    offs = np.zeros(len(seqs) + 1, dtype=np.uint64)
+    offs[1:] = np.cumsum(lens)
+    want = []
+    for s_ in seqs:
+        words = 8 * ((len(s_) + 127) // 128)
+        k = ((np.frombuffer(s_, dtype=np.uint8) >> 1) ^ (np.frombuffer(s_, dtype=np.uint8) >> 2)) & 3
+        k = np.concatenate([k, np.zeros(16 * words - len(k), dtype=np.uint8)]).astype(np.uint32).reshape(words, 16)
+        want.append((k << (2 * np.arange(16, dtype=np.uint32))).sum(axis=1).astype("<u4").tobytes())
+    want = b"".join(want)
+    raw = np.zeros(len(data) // 4 + 32 * len(seqs) + 128, dtype=np.uint8)
+    dst = raw[(-raw.ctypes.data) % 32:]  # 32-byte aligned view
+    nb = C.c_uint64()
+    u64p = C.POINTER(C.c_uint64)
+    assert lib().dm_pack_nt_seqs(data, offs.ctypes.data_as(u64p), len(seqs), dst.ctypes.data, C.byref(nb)) == 0
+    assert nb.value == len(want) and dst[:nb.value].tobytes() == want
+    for pos in (len(data) - 1, len(data) // 2, 0):  # buffer end (tail through the buffer), middle, start
+        bad = bytearray(data)
+        bad[pos] = ord("N")
+        assert lib().dm_pack_nt_seqs(bytes(bad), offs.ctypes.data_as(u64p), len(seqs), dst.ctypes.data,
+                                     C.byref(nb)) != 0
+    assert lib().dm_pack_nt_seqs(data, offs.ctypes.data_as(u64p), len(seqs), dst[1:].ctypes.data, C.byref(nb)) != 0
