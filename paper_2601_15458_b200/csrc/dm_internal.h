@@ -113,7 +113,7 @@ struct dm_ctx {
     cudaEvent_t lev_fork = nullptr, lev_join[kLevSide] = {};
     dm::PinnedBuf pin_items, pin_out;
     // scratch for the aligner / merge scheduler
-    dm::DevBuf nw_in, nw_table, nw_jobs, nw_trace, nw_res, nw_gaps, rows_a, rows_b, colmap, tree_buf;
+    dm::DevBuf nw_in, nw_table, nw_jobs, nw_trace, nw_res, nw_gaps, nw_wrap, rows_a, rows_b, colmap, tree_buf;
     uint64_t launches = 0;
     // Every C ABI call on a context holds this lock (capi_guard.h), so one
     // context may be shared by host threads (the reference's functions are
@@ -126,7 +126,7 @@ private:
     void attach(cudaStream_t* s) {
         for (dm::DevBuf* b : {&items, &out, &counter, &aux, &aux2, &aux3, &lev_all, &lev_items,
                               &stream_pairs, &stream_out, &stream_offs, &nw_in, &nw_table,
-                              &nw_jobs, &nw_trace,
+                              &nw_jobs, &nw_trace, &nw_wrap,
                               &nw_res, &nw_gaps, &rows_a, &rows_b, &colmap, &tree_buf, &ss_meta, &ss_codes,
                               &ss_planes})
             b->sp = s;

@@ -1,7 +1,7 @@
 // Pairwise aligner: batched Gotoh Needleman-Wunsch
 // with device-side traceback, bit-exact with nw_align (pairwise.cpp:301-415).
 //
-// Forward (K5, nw_fwd.cuh): one alignment per CTA of 1, 4 or 8 warps. Lane g
+// Forward (K5, nw_fwd.cuh): one alignment per CTA of 1-4 or 8 warps. Lane g
 // owns RR = 16 consecutive rows of its warp's 512-row band and sweeps the
 // columns of b as a diagonal pipeline (lane g is on column s-g+1 at step s);
 // the bottom row of lane g-1 arrives by __shfl_up each step, and each band
@@ -127,8 +127,10 @@ __global__ void __launch_bounds__(128) nw_traceback_kernel(const TbArgs a) {
     }
 }
 
+// wrap_m: largest width of an alignment with more bands than NWW (0: none);
+// such launches get a per-CTA global row for the round-to-round hand-off.
 template <class V, int NWW>
-void launch_fwd(dm_ctx* ctx, const nwk::FwdArgs& fa, size_t smem) {
+void launch_fwd(dm_ctx* ctx, const nwk::FwdArgs& fa, size_t smem, uint32_t wrap_m) {
     static int occ = -1;
     if (occ < 0) {
         DM_CUDA(cudaFuncSetAttribute(nwk::nw_fwd_kernel<V, NWW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -137,20 +139,29 @@ void launch_fwd(dm_ctx* ctx, const nwk::FwdArgs& fa, size_t smem) {
         occ = std::max(occ, 1);
     }
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(fa.njobs, (uint64_t)occ * ctx->sm_count));
-    nwk::nw_fwd_kernel<V, NWW><<<grid, NWW * 32, smem, ctx->stream>>>(fa);
+    nwk::FwdArgs f = fa;
+    if (NWW > 1 && wrap_m) {
+        f.wrap_stride = ((uint64_t)wrap_m + 1) * 3;
+        f.wrap = ctx->nw_wrap.get((uint64_t)grid * f.wrap_stride * sizeof(V));
+    }
+    nwk::nw_fwd_kernel<V, NWW><<<grid, NWW * 32, smem, ctx->stream>>>(f);
 }
 
 template <class V>
-void launch_group(dm_ctx* ctx, int nww, const nwk::FwdArgs& fa, size_t smem) {
-    if (nww == 1) launch_fwd<V, 1>(ctx, fa, smem);
-    else if (nww == 4) launch_fwd<V, 4>(ctx, fa, smem);
-    else launch_fwd<V, 8>(ctx, fa, smem);
+void launch_group(dm_ctx* ctx, int nww, const nwk::FwdArgs& fa, size_t smem, uint32_t wrap_m) {
+    if (nww == 1) launch_fwd<V, 1>(ctx, fa, smem, 0);
+    else if (nww == 2) launch_fwd<V, 2>(ctx, fa, smem, wrap_m);
+    else if (nww == 3) launch_fwd<V, 3>(ctx, fa, smem, wrap_m);
+    else if (nww == 4) launch_fwd<V, 4>(ctx, fa, smem, wrap_m);
+    else launch_fwd<V, 8>(ctx, fa, smem, wrap_m);
 }
 
-// warps per alignment: one band per warp up to 8 bands
+// warps per alignment: one band per warp up to 4 bands (a CTA's warps wait
+// for each other between alignments, so no idle warps there), then 8
+constexpr int kGroups = 5;
 int group_of(uint32_t n) {
     const uint32_t nb = (n + nwk::BAND - 1) / nwk::BAND;
-    return nb <= 1 ? 1 : (nb <= 4 ? 4 : 8);
+    return nb <= 4 ? (int)std::max<uint32_t>(nb, 1) : 8;
 }
 
 }  // namespace
@@ -158,9 +169,13 @@ int group_of(uint32_t n) {
 void nw_warm() {
     cudaFuncAttributes fa;
     DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int32_t, 1>));
+    DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int32_t, 2>));
+    DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int32_t, 3>));
     DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int32_t, 4>));
     DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int32_t, 8>));
     DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int64_t, 1>));
+    DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int64_t, 2>));
+    DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int64_t, 3>));
     DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int64_t, 4>));
     DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int64_t, 8>));
     DM_CUDA(cudaFuncGetAttributes(&fa, nw_traceback_kernel));
@@ -261,8 +276,8 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
         uint8_t* d_trace = (uint8_t*)ctx->nw_trace.get(tb + 64);
         NwJob* d_jobs = ctx->nw_jobs.as<NwJob>(cnt);
         DM_CUDA(cudaMemcpyAsync(d_jobs, sj.data() + c0, cnt * sizeof(NwJob), cudaMemcpyHostToDevice, ctx->stream));
-        uint32_t* d_cnt = ctx->counter.as<uint32_t>(4);
-        DM_CUDA(cudaMemsetAsync(d_cnt, 0, 16, ctx->stream));
+        uint32_t* d_cnt = ctx->counter.as<uint32_t>(kGroups + 1);  // one per group launch + the traceback
+        DM_CUDA(cudaMemsetAsync(d_cnt, 0, (kGroups + 1) * sizeof(uint32_t), ctx->stream));
         if (time_kernels) DM_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
         size_t g0 = c0;
         int gi = 0;
@@ -272,8 +287,11 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
             while (g1 < c1 && group_of(sj[g1].n) == grp) ++g1;
             nwk::FwdArgs fa{d_chars, d_jobs + (g0 - c0), (uint32_t)(g1 - g0), d_lut, d_table, sc.K, sc.Kp,
                             4 * sc.open, 4 * sc.extend, d_trace, out.d_res, d_cnt + gi, 1};
-            if (wide) launch_group<int64_t>(ctx, grp, fa, smem);
-            else launch_group<int32_t>(ctx, grp, fa, smem);
+            uint32_t wrap_m = 0;  // widest alignment with more bands than warps
+            for (size_t q = g0; q < g1; ++q)
+                if ((sj[q].n + nwk::BAND - 1) / nwk::BAND > (uint32_t)grp) wrap_m = std::max(wrap_m, sj[q].m);
+            if (wide) launch_group<int64_t>(ctx, grp, fa, smem, wrap_m);
+            else launch_group<int32_t>(ctx, grp, fa, smem, wrap_m);
             DM_CUDA(cudaGetLastError());
             out.launches += 1;
             ctx->launches += 1;
@@ -288,7 +306,7 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
             out.fwd_ms += ms;
             DM_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
         }
-        TbArgs ta{d_jobs, cnt, d_trace, out.d_res, out.d_gaps, d_cnt + 3};
+        TbArgs ta{d_jobs, cnt, d_trace, out.d_res, out.d_gaps, d_cnt + kGroups};
         const int tgrid = (int)std::max<uint64_t>(1, std::min<uint64_t>((cnt + 3) / 4, (uint64_t)ctx->sm_count * 8));
         nw_traceback_kernel<<<tgrid, 128, 0, ctx->stream>>>(ta);
         DM_CUDA(cudaGetLastError());

@@ -12,7 +12,27 @@
 // merge drops from 5 sequential passes to ~1. Flow control is two monotonic
 // sequence counters per ring (published / consumed), checked once per
 // CHUNK columns. NWW = 1 is the plain warp-per-alignment kernel for
-// single-band alignments.
+// single-band alignments. With more bands than warps, warp w sweeps bands
+// w, w+NWW, ...; the row from the last band of a round to the first band of
+// the next (ring 0) cannot be a bounded ring (band NWW starts only when band
+// 0 has finished the whole width, which a 128-column ring would stall
+// through back-pressure), so it goes through a full-width row in global
+// memory: the producer never waits, the consumer waits on the same
+// publication counter and reads L2 (ld.cg: the row is rewritten in place
+// by the next round, never read from a stale L1 line).
+//
+// State convention (fewer ALU ops per cell, the kernel is ALU-bound): a row
+// keeps PM = M + O4, PGB = GapB + O4, PGA = GapA + O4 (tags survive: O4 is a
+// multiple of 4). Then per cell
+//   diag   = max3(PM, PGB, PGA) of the row above, previous column  (= max + O4)
+//   M + O4 = diag + s                                    -> retag 2 = new PM
+//   GA + O4 = max3(PM, PGB, PGA - O4) (own row, prev col) + E4 + O4 -> & ~3 = new PGA
+//   GB     = max3(PM, GB, PGA) (row above, this column) + E4   -> retag 1; +O4 = new PGB
+// i.e. 6 ALU (3 max3, 3 retags) + 6 FMA (adds incl. the score-table address),
+// where the max3-of-sums form needed 4 ALU VIADDMNMX + 3 retags + 1 max3 +
+// an ALU address add. The vertical-gap chain down the 16 rows of a lane is
+// max3 -> add -> retag (13 cycles a row instead of 30 with two dependent
+// VIADDMNMX). Lanes and the band ring pass (PM, GB, PGA) of their bottom row.
 #pragma once
 
 #include <type_traits>
@@ -55,6 +75,16 @@ __device__ __forceinline__ int32_t add_fma(int32_t x, int32_t y, int32_t one) {
 }
 __device__ __forceinline__ int64_t add_fma(int64_t x, int64_t y, int32_t) { return x + y; }
 
+__device__ __forceinline__ int32_t ldcg(const int32_t* p) { return __ldcg(p); }
+__device__ __forceinline__ int64_t ldcg(const int64_t* p) { return (int64_t)__ldcg(reinterpret_cast<const long long*>(p)); }
+
+// x * y on the FMA pipe (y opaque: no strength reduction to a shift)
+__device__ __forceinline__ uint32_t umul(uint32_t x, uint32_t y) {
+    uint32_t d;
+    asm("mul.lo.u32 %0, %1, %2;" : "=r"(d) : "r"(x), "r"(y));
+    return d;
+}
+
 // low bytes of four values -> one word (byte k = low byte of value k)
 __device__ __forceinline__ uint32_t gather_lo(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     const uint32_t ab = __byte_perm(a, b, 0x0040);
@@ -91,6 +121,11 @@ struct FwdArgs {
     NwRes* res;
     uint32_t* counter;
     int32_t one;  // == 1 (opaque to ptxas)
+    // alignments with more bands than warps: the row passed from band NWW-1
+    // of one round to band NWW of the next (ring 0) goes through this
+    // per-CTA global row (wrap_stride V per CTA, columns 0..m) instead
+    void* wrap;
+    uint64_t wrap_stride;
 };
 
 template <class V, int NWW>
@@ -114,6 +149,8 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
     const char* tbytes = reinterpret_cast<const char*>(s_table);
     // opaque ~3 / tag constants (from the runtime 1) for the one-LOP3 retags
     const uint32_t tag1 = (uint32_t)a.one, tag2 = tag1 + tag1, keep = ~(tag2 + tag1);
+    const uint32_t four = tag2 + tag2, sixteen = four * four;
+    const V NO4 = -O4, EO4 = E4 + O4;
     for (;;) {
         __syncthreads();  // previous job fully done; table/lut loaded
         if (threadIdx.x == 0) sm.jid = atomicAdd(a.counter, 1u);
@@ -126,6 +163,7 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
         if (jid >= a.njobs) break;
         const NwJob job = a.jobs[jid];
         const uint32_t n = job.n, m = job.m;
+
         const uint8_t* A = a.chars + job.a_off;
         const uint8_t* B = a.chars + job.b_off;
         const uint32_t pa = (n + 15) & ~15u;
@@ -134,35 +172,36 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
         for (uint32_t band = w; band < nbands; band += NWW) {
             const uint32_t i0 = band * BAND + (uint32_t)g * RR + 1;
             int rowoff[RR];  // byte offset of the score-table row of a[i]
-            V LM[RR], LGB[RR], LGA[RR];
+            V LM[RR], LGB[RR], LGA[RR];  // PM, PGB, PGA (offset by O4, see above)
 #pragma unroll
             for (int r = 0; r < RR; ++r) {
                 const uint32_t i = i0 + r;
                 rowoff[r] = (i <= n ? (int)sm.lut[A[i - 1] & 127] : 0) * a.Kp * 4;
-                LM[r] = (V)(NEG | 2);
-                LGA[r] = NEG;
-                LGB[r] = (V)((a.O4 + (int64_t)i * a.E4) | 1);  // column 0: GB = open + i*extend
+                LM[r] = (V)(NEG | 2) + O4;
+                LGA[r] = NEG + O4;
+                LGB[r] = (V)((a.O4 + (int64_t)i * a.E4) | 1) + O4;  // column 0: GB = open + i*extend
             }
             // row i0-1 at column 0: the first row's diagonal at column 1
-            // (as the max over its three states: all the M recurrence needs)
-            V pmax = i0 == 1 ? (V)2 /* M[0][0] = 0 */ : (V)((a.O4 + (int64_t)(i0 - 1) * a.E4) | 1);
+            // (as the max over its three states: all the M recurrence needs), + O4
+            V pmax = (i0 == 1 ? (V)2 /* M[0][0] = 0 */ : (V)((a.O4 + (int64_t)(i0 - 1) * a.E4) | 1)) + O4;
             // ring in (from band-1) and out (to band+1); sequence = gen*(m+1)+j
             const int rin = (int)(band % NWW), rout = (int)((band + 1) % NWW);
             const uint32_t seq_in = (band / NWW) * (m + 1), seq_out = ((band + 1) / NWW) * (m + 1);
             const bool has_in = NWW > 1 && band > 0;
             const bool has_out = NWW > 1 && band + 1 < nbands;
+            V* wrapbuf = NWW > 1 ? reinterpret_cast<V*>(a.wrap) + (uint64_t)blockIdx.x * a.wrap_stride : nullptr;
             V sM = 0, sGB = 0, sGA = 0;
             // One column step of the band's lane pipeline. CHK: generic step
             // (pipeline fill/drain: lanes may be outside 1..m; ring flow
-            // control decided from s). Steady steps (every lane inside, s in
-            // whole 16-column chunks, k = s mod 16) drop the range checks and
-            // take the flow-control points from k alone (warp-uniform).
-            auto step = [&](uint32_t s, auto chk, int k) {
+            // control decided from s, per step). Steady steps (every lane
+            // inside, s in whole 16-column chunks) drop the range checks and
+            // all flow control: the steady loop does it once per chunk.
+            auto step = [&](uint32_t s, auto chk) {
                 constexpr bool CHK = decltype(chk)::value;
                 const V rM = shfl_up1(sM), rGB = shfl_up1(sGB), rGA = shfl_up1(sGA);
-                if constexpr (NWW > 1) {
+                if constexpr (NWW > 1 && CHK) {
                     // consumer side (lane 0 reads column s+1 this step)
-                    if (CHK ? (has_in && (s % CHUNK) == 0 && s < m) : (has_in && k == 0)) {
+                    if (has_in && (s % CHUNK) == 0 && s < m) {
                         if (g == 0) {
                             const uint32_t need = seq_in + min(s + CHUNK, m);
                             while (sm.pub[rin] < need) {
@@ -171,8 +210,7 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
                         __syncwarp();
                     }
                     // producer side (lane 31 writes column s-30 this step)
-                    if (CHK ? (has_out && s >= 31 && ((s - 31) % CHUNK) == 0 && s - 31 < m)
-                            : (has_out && k == CHUNK - 1)) {
+                    if (has_out && rout != 0 && s >= 31 && ((s - 31) % CHUNK) == 0 && s - 31 < m) {
                         if (g == 31) {
                             const uint32_t jj = s - 30;  // first column of the chunk
                             const uint32_t last = seq_out + min(jj + CHUNK - 1, m);
@@ -187,11 +225,16 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
                     // lane 0's input row (band 0: row 0, pairwise.cpp:322-330;
                     // else the band above via the ring), read at lane 0's
                     // column s+1 by every lane (one broadcast, no divergence)
-                    V iM, iGB, iGA;
+                    V iM, iGB, iGA;  // (PM, GB, PGA) of the row above lane 0
                     if (band == 0) {
-                        iM = (V)(NEG | 2);
+                        iM = (V)(NEG | 2) + O4;
                         iGB = (V)(NEG | 1);
-                        iGA = (V)(a.O4 + (int64_t)(s + 1) * a.E4);
+                        iGA = (V)(a.O4 + (int64_t)(s + 1) * a.E4) + O4;
+                    } else if (NWW > 1 && rin == 0) {
+                        const V* e = wrapbuf + (uint64_t)(s + 1) * 3;
+                        iM = ldcg(e);
+                        iGB = ldcg(e + 1);
+                        iGA = ldcg(e + 2);
                     } else {
                         const V* e = sm.ring[rin][(seq_in + s + 1) % RING];
                         iM = e[0];
@@ -205,33 +248,35 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
                     // pre-reduced to their max before row r-1 is overwritten, so
                     // every state updates in place (no register rotation)
                     V dmax = pmax;
-                    pmax = vmax3(uM, uGB, uGA);
+                    pmax = vmax3(uM, add_fma(uGB, O4, a.one), uGA);
                     const int cb4 = (int)sm.lut[B[j - 1] & 127] * 4;
                     uint32_t tw[RR / 4];
                     uint32_t tm[4], tgb[4], tga[4];
 #pragma unroll
                     for (int r = 0; r < RR; ++r) {
-                        const int32_t sc = *reinterpret_cast<const int32_t*>(tbytes + rowoff[r] + cb4);
-                        const V mraw = add_fma(dmax, (V)sc, a.one);
-                        dmax = vmax3(LM[r], LGB[r], LGA[r]);
-                        const V gbraw = add_fma(addmax(uGA, O4, addmax(uM, O4, uGB)), E4, a.one);
-                        const V garaw = add_fma(addmax(LGB[r], O4, addmax(LM[r], O4, LGA[r])), E4, a.one);
-                        tm[r & 3] = (uint32_t)mraw;
+                        const int32_t sc = *reinterpret_cast<const int32_t*>(tbytes + add_fma(rowoff[r], cb4, a.one));
+                        const V mo = add_fma(dmax, (V)sc, a.one);                  // M + O4
+                        dmax = vmax3(LM[r], LGB[r], LGA[r]);                       // old row r, + O4
+                        const V gao = add_fma(vmax3(LM[r], LGB[r], add_fma(LGA[r], NO4, a.one)), EO4, a.one);
+                        const V gbraw = add_fma(vmax3(uM, uGB, uGA), E4, a.one);   // the row chain
+                        tm[r & 3] = (uint32_t)mo;
                         tgb[r & 3] = (uint32_t)gbraw;
-                        tga[r & 3] = (uint32_t)garaw;
+                        tga[r & 3] = (uint32_t)gao;
                         if ((r & 3) == 3) {  // four rows of codes -> one trace word
                             const uint32_t wm = gather_lo(tm[0], tm[1], tm[2], tm[3]);
                             const uint32_t wb = gather_lo(tgb[0], tgb[1], tgb[2], tgb[3]);
                             const uint32_t wa = gather_lo(tga[0], tga[1], tga[2], tga[3]);
                             // byte = tagM | tagGB << 2 | tagGA << 4 (bits 6-7 are
-                            // don't-care: the traceback masks every field)
-                            tw[r >> 2] = bitsel(bitsel(wm, wb << 2, 0x03030303u), wa << 4, 0x0F0F0F0Fu);
+                            // don't-care: the traceback masks every field); the
+                            // shifts as multiplies by opaque 4 / 16 (FMA pipe)
+                            tw[r >> 2] = bitsel(bitsel(wm, umul(wb, four), 0x03030303u), umul(wa, sixteen), 0x0F0F0F0Fu);
                         }
-                        LM[r] = retag(mraw, keep, tag2);
-                        LGB[r] = retag(gbraw, keep, tag1);
-                        LGA[r] = garaw & ~(V)3;
+                        LM[r] = retag(mo, keep, tag2);
+                        const V lgb = retag(gbraw, keep, tag1);
+                        LGB[r] = add_fma(lgb, O4, a.one);
+                        LGA[r] = retag(gao, keep, 0u);
                         uM = LM[r];
-                        uGB = LGB[r];
+                        uGB = lgb;
                         uGA = LGA[r];
                     }
                     sM = uM;
@@ -242,16 +287,16 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
                             make_uint4(tw[0], tw[1], tw[2], tw[3]);
                     if constexpr (NWW > 1) {
                         if (has_out && g == 31) {
-                            V* e = sm.ring[rout][(seq_out + j) % RING];
+                            V* e = rout == 0 ? wrapbuf + (uint64_t)j * 3 : sm.ring[rout][(seq_out + j) % RING];
                             e[0] = uM;
                             e[1] = uGB;
                             e[2] = uGA;
-                            if (CHK ? ((j % CHUNK) == 0 || j == m) : (k == CHUNK - 2)) {
+                            if (CHK && ((j % CHUNK) == 0 || j == m)) {
                                 __threadfence_block();
                                 sm.pub[rout] = seq_out + j;
                             }
                         }
-                        if (has_in && g == 0 && (CHK ? ((j % CHUNK) == 0 || j == m) : (k == CHUNK - 1))) {
+                        if (CHK && has_in && g == 0 && ((j % CHUNK) == 0 || j == m)) {
                             __threadfence_block();  // ring reads complete before the slot is released
                             sm.con[rin] = seq_in + j;
                         }
@@ -260,16 +305,55 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
             };
             const uint32_t steps = m + 31;
             uint32_t s = 0;
-            for (; s < min(32u, steps); ++s) step(s, std::true_type{}, 0);
-            // steady state: s in [32, m), whole chunks of CHUNK columns
+            for (; s < min(32u, steps); ++s) step(s, std::true_type{});
+            // steady state: s in [32, s_end), whole chunks of CHUNK columns;
+            // flow control once per chunk, around the chunk:
+            //  - consumer (lane 0 reads columns s+1 .. s+16): wait until the
+            //    band above published them; release them after the chunk;
+            //  - producer (lane 31 writes columns s-30 .. s-15): wait for ring
+            //    space through column s (this chunk plus the next 15 writes,
+            //    which the drain steps' own checks do not cover); publish
+            //    through s-15 after the chunk.
+            // The producer then runs 31..143 columns ahead of its consumer.
             if (m > 32) {
                 const uint32_t s_end = 32 + ((m - 32) & ~(uint32_t)(CHUNK - 1));
-                // not unrolled: one step is ~300 instructions, a chunk of them
-                // would not fit the instruction cache
 #pragma unroll 1
-                for (; s < s_end; ++s) step(s, std::false_type{}, (int)(s % CHUNK));
+                for (; s < s_end; s += CHUNK) {
+                    if constexpr (NWW > 1) {
+                        if (has_in) {
+                            if (g == 0) {
+                                const uint32_t need = seq_in + min(s + CHUNK, m);
+                                while (sm.pub[rin] < need) {
+                                }
+                            }
+                            __syncwarp();
+                        }
+                        if (has_out && rout != 0) {
+                            if (g == 31) {
+                                const uint32_t last = seq_out + min(s, m);
+                                while (sm.con[rout] + RING < last + 1) {
+                                }
+                            }
+                            __syncwarp();
+                        }
+                    }
+                    // not unrolled: one step is ~300 instructions, a chunk of
+                    // them would not fit the instruction cache
+#pragma unroll 1
+                    for (uint32_t q = 0; q < CHUNK; ++q) step(s + q, std::false_type{});
+                    if constexpr (NWW > 1) {
+                        if (has_out && g == 31) {
+                            __threadfence_block();
+                            sm.pub[rout] = seq_out + (s + CHUNK - 1 - 30);
+                        }
+                        if (has_in && g == 0) {
+                            __threadfence_block();  // ring reads complete before the slots are released
+                            sm.con[rin] = seq_in + s + CHUNK;
+                        }
+                    }
+                }
             }
-            for (; s < steps; ++s) step(s, std::true_type{}, 0);
+            for (; s < steps; ++s) step(s, std::true_type{});
             // final state at (n, m) (pairwise.cpp:374-375): the lane owning row n
             if (n >= i0 && n < i0 + RR) {
                 V fM = LM[0], fGB = LGB[0], fGA = LGA[0];
@@ -280,7 +364,7 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
                         fGB = LGB[r];
                         fGA = LGA[r];
                     }
-                const V fin = vmax3(fM, fGB, fGA);
+                const V fin = vmax3(fM, fGB, fGA) - O4;
                 a.res[job.slot].score = (int64_t)(fin >> 2);
                 a.res[job.slot].final_tag = (uint32_t)(fin & 3);
             }

@@ -166,3 +166,29 @@ def test_cfg1_nw_sample_vs_reference(dm, ctx, ref):
     assert st["cells"] == sum(len(a) * len(b) for a, b in pairs)
     for (a, b), r in zip(pairs, got):
         assert as_tuple(r) == as_tuple(ref.nw_align(a, b))
+
+
+@pytest.mark.timeout(600)
+def test_more_bands_than_warps_vs_reference(dm, ctx, ref):
+    """Alignments of 2..19 bands (512 rows each; more than 8 bands = several
+    rounds of the 8-warp CTA, the round-to-round row going through global
+    memory) and every warps-per-alignment group, including int64 scores."""
+    rng = random.Random(12)
+    pairs = []
+    for la, lb in ((1000, 900), (1500, 1600), (2000, 1900), (4100, 600), (4700, 4800), (5200, 300),
+                   (9000, 8800), (9700, 2500)):
+        a = rand_str(rng, la)
+        b = list(a[:lb]) + [rng.choice("ACGT") for _ in range(max(0, lb - la))]
+        for _ in range(lb // 15):
+            b[rng.randrange(len(b))] = rng.choice("ACGT")
+        pairs.append((a, "".join(b)))
+    got = dm.nw_batch(pairs, dm.ScoringScheme.nucleotide(), ctx)
+    for (a, b), r in zip(pairs, got):
+        assert as_tuple(r) == as_tuple(ref.nw_align(a, b)), (len(a), len(b))
+    syms = "ACGT"
+    flatm = [30000 if i == j else -29000 for i in range(4) for j in range(4)]
+    sc = dm.ScoringScheme.custom(syms, flatm, -32000, -20000)
+    big = [pairs[4], pairs[6]]
+    for (a, b), r in zip(big, dm.nw_batch(big, sc, ctx)):
+        want = ref.nw_align(a, b, "custom", -32000, -20000, False, symbols=syms, matrix=flatm)
+        assert as_tuple(r) == as_tuple(want)
