@@ -191,6 +191,9 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
             const bool has_out = NWW > 1 && band + 1 < nbands;
             V* wrapbuf = NWW > 1 ? reinterpret_cast<V*>(a.wrap) + (uint64_t)blockIdx.x * a.wrap_stride : nullptr;
             V sM = 0, sGB = 0, sGA = 0;
+            // b's residue for the lane's next column, loaded one step ahead
+            // (the global load's latency was the top stall of the step)
+            uint32_t bnext = (g == 0 && m > 0) ? (uint32_t)B[0] : 0u;
             // One column step of the band's lane pipeline. CHK: generic step
             // (pipeline fill/drain: lanes may be outside 1..m; ring flow
             // control decided from s, per step). Steady steps (every lane
@@ -221,6 +224,8 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
                     }
                 }
                 const uint32_t j = s - (uint32_t)g + 1;  // 1..m when active
+                const uint32_t bcur = bnext;
+                bnext = j < m ? (uint32_t)B[j] : 0u;  // column j + 1 next step
                 if (!CHK || j - 1 < m) {
                     // lane 0's input row (band 0: row 0, pairwise.cpp:322-330;
                     // else the band above via the ring), read at lane 0's
@@ -249,7 +254,7 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
                     // every state updates in place (no register rotation)
                     V dmax = pmax;
                     pmax = vmax3(uM, add_fma(uGB, O4, a.one), uGA);
-                    const int cb4 = (int)sm.lut[B[j - 1] & 127] * 4;
+                    const int cb4 = (int)sm.lut[bcur & 127] * 4;
                     uint32_t tw[RR / 4];
                     uint32_t tm[4], tgb[4], tga[4];
 #pragma unroll
