@@ -103,14 +103,17 @@ __device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
 // per-word mix (tools/ubench/mix.cu): 61 TCUPS with both shifts as add
 // chains vs 54 with IMAD.WIDE + IMAD per word on the FMA pipe — fewer
 // instructions issued beats moving work off the ALU pipe here.
+// Two of its ops go to the FMA pipe (the kernel is ALU-bound, the FMA pipe
+// has room): word 0 = t0 * 2 + cin as an IMAD (the chain's own word 0 only
+// feeds the carry), and the bit shifted out = hi(t * 2) as an IMAD.HI.
 template <int W>
-__device__ __forceinline__ uint32_t shl1(uint32_t (&v)[W], uint32_t cin) {
+__device__ __forceinline__ uint32_t shl1(uint32_t (&v)[W], uint32_t cin, uint32_t two) {
     uint32_t t[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) t[w] = v[w];
     Chain<W>::add(v, t, t);
-    v[0] |= cin;
-    return t[W - 1] >> 31;
+    v[0] = imad(t[0], two, cin);
+    return __umulhi(t[W - 1], two);
 }
 
 template <int NP, int W>
@@ -230,8 +233,8 @@ __global__ void __launch_bounds__(256, NP == 2 ? 3 : 1) lev_kernel(const LevArgs
                     // terms are disjoint and the OR is an add -> FMA pipe
                     Ph[w] = w == 0 ? lop3<0xF1>(Mv[w], S[w], T0) : imad(lop3<0x01>(S[w], Pv[w], Xv[w]), a.one, Mv[w]);
                 }
-                const uint32_t hpo = shl1<W>(Ph, hp);
-                const uint32_t hmo = shl1<W>(Mh, hm);
+                const uint32_t hpo = shl1<W>(Ph, hp, two);
+                const uint32_t hmo = shl1<W>(Mh, hm, two);
 #pragma unroll
                 for (int w = 0; w < W; ++w) {
                     Pv[w] = lop3<0xF1>(Mh[w], Xv[w], Ph[w]);  // Mh | ~(Xv | Ph)
