@@ -13,8 +13,10 @@ A step = one pass of the distance engine over the whole pair batch.
          the packed pairs in pinned host memory to dm_lev_pairs_packed, which
          uploads them in chunks overlapped with the kernels (A/C/G/T chunks
          packed to 2 bits per residue by host threads first, so a quarter of
-         the bytes cross PCIe; h2d_bytes_per_step counts what was copied) and
-         returns the distances in host memory (wall clock around the call).
+         their bytes cross PCIe, while ~30% of the chunks go up raw on the copy
+         engine and are checked on the device; h2d_bytes_per_step counts what
+         was copied) and returns the distances in host memory (wall clock
+         around the call).
   nw     the NW micro-benchmark of SURVEY.md §8(d): the first 65,536 cfg1
          pairs through dm_nw_batch (nucleotide scheme, affine -10/-1, full
          traceback), bit-checked against the C restatement on a sample;
@@ -395,7 +397,8 @@ def main():
     e2e = {"value": cells_step * world / e2e_s / 1e9, "unit": "GCUPS",
            "h2d_bytes_per_step": int(est.h2d_bytes), "d2h_bytes_per_step": int(est.d2h_bytes),
            "host_input_bytes_per_step": int(len(data) + offs_c.nbytes),
-           "upload": "A/C/G/T chunks packed to 2 bits/residue by host threads; codes built on the device from the packed bytes"}
+           "upload": ("~70% of the residue bytes packed to 2 bits/residue by host threads (the upload is the "
+                      "device code buffer), ~30% sent raw by the copy engine and checked on the device")}
 
     # ---- roofline: INT32 lane-op peak measured on this box --------------
     peaks = []

@@ -112,11 +112,12 @@ int dm_lev_pairs_device(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia,
  * of `data` / `offsets` (2*npairs+1 entries). Uploads and computes in
  * overlapped chunks (copy stream + compute stream). Chunks holding only
  * A/C/G/T bytes cross PCIe as 2-bit codes (packed by host threads into
- * pinned slots, expanded on the device); others are uploaded as given, where
- * pinned `data` lets the transfer run fully asynchronously. The results are
- * the same either way. st->h2d_bytes / d2h_bytes report the bytes copied.
- * Env: DM_STREAM_PACK=0 disables packing, DM_HOST_THREADS sizes the host
- * pool. out: host uint32[npairs]. */
+ * pinned slots); with a pinned `data`, part of the chunks go up raw while
+ * the host packs the rest (planned as A/C/G/T, verified on the device,
+ * recomputed exactly if the check fails). Results are identical either way.
+ * st->h2d_bytes / d2h_bytes report the bytes copied. Env: DM_STREAM_PACK=0
+ * disables packing, DM_STREAM_RAW_FRAC sets the raw share, DM_HOST_THREADS
+ * sizes the host pool. out: host uint32[npairs]. */
 int dm_lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint64_t npairs,
                         uint32_t* out, dm_stats* st);
 /* The packer alone (no device needed): residue j of src -> bits 2(j%4).. of

@@ -102,7 +102,7 @@ struct dm_ctx {
     dm::DevBuf items, out, counter, aux, aux2, aux3, lev_all, lev_items;
     cudaStream_t copy_stream = nullptr;  // host->device staging of streamed batches
     static constexpr int kStreamSlots = 4;  // chunks of a streamed batch in flight
-    dm::DevBuf stage[kStreamSlots], stream_pairs, stream_out, stream_offs;
+    dm::DevBuf stage[kStreamSlots], stream_pairs, stream_out, stream_offs, stream_flags;
     dm::DevBuf stage_packed[kStreamSlots];  // 2-bit nucleotide chunks as uploaded
     dm::DevBuf ss_meta, ss_codes, ss_planes;  // planner contexts: the chunk's sequence set (reused)
     dm::PinnedBuf pin_pack[kStreamSlots];   // host side of the same
@@ -125,7 +125,7 @@ struct dm_ctx {
 private:
     void attach(cudaStream_t* s) {
         for (dm::DevBuf* b : {&items, &out, &counter, &aux, &aux2, &aux3, &lev_all, &lev_items,
-                              &stream_pairs, &stream_out, &stream_offs, &nw_in, &nw_table,
+                              &stream_pairs, &stream_out, &stream_offs, &stream_flags, &nw_in, &nw_table,
                               &nw_jobs, &nw_trace, &nw_wrap,
                               &nw_res, &nw_gaps, &rows_a, &rows_b, &colmap, &tree_buf, &ss_meta, &ss_codes,
                               &ss_planes})
@@ -210,8 +210,11 @@ struct LevTotals {
 void lev_run_host_items(dm_ctx* ctx, const dm_seqset* s, std::vector<LevItem>& items,
                         uint32_t* d_out, LevTotals* tot, bool time_kernels);
 // Pairs (2i, 2i+1) of a packed HOST buffer, streamed in chunks (stream.cu).
+// speculate: chunks may be sent raw and planned as A/C/G/T, verified on the
+// device; the pair ranges of chunks that failed go to *redo (the caller runs
+// them again with speculate = false).
 void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint64_t npairs, uint32_t* out,
-                      LevTotals* tot, bool timing);
+                      LevTotals* tot, bool speculate, std::vector<std::pair<uint64_t, uint64_t>>* redo);
 // Streamed path: plan on `prep` (its stream and scratch), then launch the
 // distance kernels on ctx->stream after `planned`. pair_offs (host, 2n+1
 // offsets of pairs (2i, 2i+1)) given: the bucket histogram is counted on the

@@ -17,10 +17,13 @@
 // of the bytes cross the bus and the uploaded buffer IS the chunk's code
 // buffer. Knowing the alphabet and the lengths, that chunk's planner skips
 // both host syncs (codes A0 C1 G2 T3; bucket histogram counted on the host,
-// plan_hist_host) and has no recode pass. Any other chunk is uploaded as
-// given and planned as before. DM_STREAM_PACK_FRAC < 1 packs only the head
-// of each chunk (flat, expanded by unpack_acgt next to the raw tail), for
-// hosts whose packing rate is below the bus rate.
+// plan_hist_host) and has no recode pass. Packing is bound by host memory
+// bandwidth, which the copy engine can add to: with a pinned caller buffer,
+// ~30 % of the bytes go up raw instead ("speculative" chunks), planned as
+// A/C/G/T like packed ones and checked on the device (verify_acgt_kernel);
+// a chunk that fails is recomputed on the exact path before the call
+// returns. Any other chunk is uploaded as given and planned with the device
+// census. DM_STREAM_PACK=0 / DM_STREAM_RAW_FRAC=x override the mix.
 #include <algorithm>
 #include <chrono>
 #include <condition_variable>
@@ -47,27 +50,24 @@ __global__ void iota_pairs(uint32_t* ia, uint32_t* ib, uint64_t n) {
     }
 }
 
-// 4 codes (one packed byte) -> 4 residue bytes: the codes are PRMT selectors
-// into the word "ACGT".
-__device__ __forceinline__ uint32_t expand4(uint32_t b) {
-    const uint32_t sel = (b & 3u) | ((b & 0xcu) << 2) | ((b & 0x30u) << 4) | ((b & 0xc0u) << 6);
-    return __byte_perm(0x54474341u, 0u, sel);
-}
-
-// n residues from 2-bit codes (host_pack.h layout) back to bytes; 16
-// residues (one 32-bit load, one 16-byte store) per thread.
-__global__ void unpack_acgt(const uint32_t* __restrict__ src, uint64_t n, uint8_t* __restrict__ dst) {
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x, groups = n / 16;
-    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += stride) {
-        const uint32_t w = src[g];
-        reinterpret_cast<uint4*>(dst)[g] =
-            make_uint4(expand4(w & 0xffu), expand4((w >> 8) & 0xffu), expand4((w >> 16) & 0xffu), expand4(w >> 24));
+// Speculative chunks: flag = 1 if any of the n bytes is not A, C, G or T.
+__global__ void verify_acgt_kernel(const uint8_t* __restrict__ raw, uint64_t n, uint32_t* __restrict__ flag) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x, words = n / 16;
+    bool bad = false;
+    auto check4 = [](uint32_t x) {
+        const uint32_t ok = __vcmpeq4(x, 0x41414141u) | __vcmpeq4(x, 0x43434343u) | __vcmpeq4(x, 0x47474747u) |
+                            __vcmpeq4(x, 0x54545454u);
+        return ok != 0xffffffffu;
+    };
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += stride) {
+        const uint4 v = reinterpret_cast<const uint4*>(raw)[i];
+        bad |= check4(v.x) | check4(v.y) | check4(v.z) | check4(v.w);
     }
     if (blockIdx.x == 0 && threadIdx.x < n % 16) {
-        const uint64_t j = groups * 16 + threadIdx.x;
-        const uint32_t b = reinterpret_cast<const uint8_t*>(src)[j / 4];
-        dst[j] = (uint8_t)(0x54474341u >> (8 * ((b >> (2 * (j % 4))) & 3u)));
+        const uint8_t c = raw[words * 16 + threadIdx.x];
+        bad |= !(c == 'A' || c == 'C' || c == 'G' || c == 'T');
     }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
 }
 
 }  // namespace
@@ -116,8 +116,7 @@ struct ChunkEvents {
 }  // namespace
 
 void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint64_t npairs, uint32_t* out,
-                      LevTotals* tot, bool timing) {
-    (void)timing;
+                      LevTotals* tot, bool speculate, std::vector<std::pair<uint64_t, uint64_t>>* redo) {
     if (npairs == 0) return;
     if (2 * npairs > 0xffffffffull) throw invalid_argument("too many sequences in one streamed batch");
     for (uint64_t i = 0; i < 2 * npairs; ++i)
@@ -152,7 +151,7 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
         maxbytes = std::max(maxbytes, offsets[2 * cb[c + 1]] - offsets[2 * cb[c]]);
     }
     const uint64_t oslot = 2 * per + 1;  // offsets per staging slot
-    if (!ctx->copy_stream) {  // high priority: the unpack kernels take the first SM slots the distance kernels free
+    if (!ctx->copy_stream) {  // high priority, like the planners
         int least = 0, greatest = 0;
         DM_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
         DM_CUDA(cudaStreamCreateWithPriority(&ctx->copy_stream, cudaStreamNonBlocking, greatest));
@@ -165,7 +164,7 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
     const auto t_start = std::chrono::steady_clock::now();
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tl;
     std::vector<std::pair<cudaEvent_t, uint64_t>> tc;
-    std::vector<cudaEvent_t> th;  // trace: residue bytes landed (before the unpack)
+    std::vector<cudaEvent_t> th;  // trace: residue bytes landed
     cudaEvent_t tl0 = nullptr;
     if (trace) {
         cudaEventCreate(&tl0);
@@ -213,6 +212,8 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
         uint32_t* d_ab = ctx->stream_pairs.as<uint32_t>(2 * per + 2);
         uint32_t* d_res = ctx->stream_out.as<uint32_t>(npairs);
         uint32_t* h_res = ctx->pin_out.as<uint32_t>(npairs);
+        uint32_t* d_flags = ctx->stream_flags.as<uint32_t>(nchunks);  // speculative chunk c held a non-ACGT byte
+        DM_CUDA(cudaMemsetAsync(d_flags, 0, nchunks * 4, ctx->stream));
         const char* pk = std::getenv("DM_STREAM_PACK");
         const bool pack = !(pk && pk[0] == '0');
         // per-sequence 2-bit layout (code_bytes): < L / 4 + 32 bytes per sequence
@@ -238,14 +239,26 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
             }
         } evg{h2d_done};
         uint64_t h2d_bytes = 0;
-        std::vector<char> acgt(nchunks, 0);  // chunk c went up fully packed (set before issued > c)
-        // Share of each chunk that is packed on the host (default all of it);
-        // with f < 1 the rest goes up raw while the host packs (pack rate P,
-        // bus rate B: f/P = (1 - 3f/4)/B balances them). Only a fully packed
-        // chunk is known to be A/C/G/T, which lets its planner skip both host
-        // syncs (census and bucket histogram).
-        double frac = 1.0;
-        if (const char* e = std::getenv("DM_STREAM_PACK_FRAC")) frac = std::min(1.0, std::max(0.0, std::atof(e)));
+        // Chunk kinds (set before issued > c): kPacked — packed on the host,
+        // the upload is its code buffer; kSpec — uploaded raw from the
+        // caller's pinned buffer and planned as A/C/G/T, verified on the
+        // device (a failed chunk is recomputed by the caller, see `redo`);
+        // kRaw — uploaded raw, alphabet from the device census.
+        enum : char { kRaw = 0, kPacked = 1, kSpec = 2 };
+        std::vector<char> kind(nchunks, kRaw);
+        // Share of the residue bytes sent raw: the copy engine reads them from
+        // host memory while the host threads pack the rest, which uses host
+        // memory bandwidth better than packing everything (measured on the
+        // box: pack alone ~100 GB/s; pack + raw copy 82 + 54 GB/s); at ~0.3
+        // the bus and the packers finish together. Needs a pinned `data`.
+        double raw_frac = 0.0;
+        if (speculate && pack) {
+            cudaPointerAttributes pa{};
+            if (cudaPointerGetAttributes(&pa, data) == cudaSuccess && pa.type == cudaMemoryTypeHost) raw_frac = 0.3;
+            cudaGetLastError();
+            if (const char* e = std::getenv("DM_STREAM_RAW_FRAC")) raw_frac = std::min(1.0, std::max(0.0, std::atof(e)));
+        }
+        uint64_t raw_sofar = 0, all_sofar = 0;  // packer thread only
         auto issue_copy = [&](uint64_t c) {
             const int b = (int)(c % NB);
             const uint64_t lo = cb[c], hi = cb[c + 1];
@@ -263,53 +276,38 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
             DM_CUDA(cudaMemcpyAsync(d_offs + b * oslot, h_offs + b * oslot, (2 * (hi - lo) + 1) * 8,
                                     cudaMemcpyHostToDevice, ctx->copy_stream));
             h2d_bytes += (2 * (hi - lo) + 1) * 8;
-            // head [0, m) packed, tail [m, n) raw; the tail's upload runs while the head is packed
-            uint64_t m = !pack || n < 256 ? 0 : (frac >= 1.0 ? n : (uint64_t)(frac * (double)n) / 128 * 128);
-            if (m < n) {
-                DM_CUDA(cudaMemcpyAsync(stage[b] + m, data + a0 + m, n - m, cudaMemcpyHostToDevice, ctx->copy_stream));
-                h2d_bytes += n - m;
-            }
+            all_sofar += n;
             const double tp0 = trace ? now_ms() : 0.0;
-            uint64_t pb = 0;  // packed bytes to upload
-            bool packed = false;
-            if (m == n && m > 0) {  // whole chunk: straight into the set's 2-bit code layout
-                // (one upload per chunk: uploading pieces while packing measured slower,
-                // the copy engine's host reads compete with the packers)
-                packed = pack_acgt_seqs(data, offsets + 2 * lo, 2 * (hi - lo), h_pack[b], &pb);
-            } else if (m > 0) {     // head only: flat 2-bit stream, expanded next to the raw tail
-                packed = pack_acgt((const uint8_t*)data + a0, m, h_pack[b]);
-                pb = (m + 15) / 16 * 4;
+            uint64_t pb = 0;  // packed bytes
+            if (n > 0 && (double)raw_sofar < raw_frac * (double)all_sofar) {
+                kind[c] = kSpec;
+                raw_sofar += n;
+            } else if (pack && n >= 256 && pack_acgt_seqs(data, offsets + 2 * lo, 2 * (hi - lo), h_pack[b], &pb)) {
+                kind[c] = kPacked;  // straight into the set's 2-bit code layout
             }
             if (trace)
-                std::fprintf(stderr, "[pack] chunk %llu: %.1f MB packed %.2f..%.2f ms\n", (unsigned long long)c, m / 1e6,
-                             tp0, now_ms());
-            acgt[c] = packed && m == n;
-            if (packed) {
+                std::fprintf(stderr, "[pack] chunk %llu: %.1f MB kind %d %.2f..%.2f ms\n", (unsigned long long)c, n / 1e6,
+                             (int)kind[c], tp0, now_ms());
+            if (kind[c] == kPacked) {  // one upload per chunk: uploading pieces while packing measured slower
                 DM_CUDA(cudaMemcpyAsync(d_pack[b], h_pack[b], pb, cudaMemcpyHostToDevice, ctx->copy_stream));
-                DM_CUDA(cudaEventRecord(h2d_done[b], ctx->copy_stream));
-                if (trace) {
-                    cudaEvent_t e;
-                    cudaEventCreate(&e);
-                    cudaEventRecord(e, ctx->copy_stream);
-                    th.push_back(e);
-                }
-                if (m < n) {
-                    const int ug = (int)std::min<uint64_t>((m / 16 + 255) / 256 + 1, (uint64_t)ctx->sm_count * 8);
-                    unpack_acgt<<<ug, 256, 0, ctx->copy_stream>>>((const uint32_t*)d_pack[b], m, stage[b]);
-                    DM_CUDA(cudaGetLastError());
-                }  // else d_pack[b] is the chunk's code buffer as it stands
                 h2d_bytes += pb;
             } else {
-                if (m) DM_CUDA(cudaMemcpyAsync(stage[b], data + a0, m, cudaMemcpyHostToDevice, ctx->copy_stream));
-                DM_CUDA(cudaEventRecord(h2d_done[b], ctx->copy_stream));
-                h2d_bytes += m;
+                if (n) DM_CUDA(cudaMemcpyAsync(stage[b], data + a0, n, cudaMemcpyHostToDevice, ctx->copy_stream));
+                h2d_bytes += n;
+            }
+            DM_CUDA(cudaEventRecord(h2d_done[b], ctx->copy_stream));
+            if (trace) {
+                cudaEvent_t e;
+                cudaEventCreate(&e);
+                cudaEventRecord(e, ctx->copy_stream);
+                th.push_back(e);
             }
             DM_CUDA(cudaEventRecord(ev.copied[b], ctx->copy_stream));
             if (trace) {
                 cudaEvent_t e;
                 cudaEventCreate(&e);
                 cudaEventRecord(e, ctx->copy_stream);
-                tc.push_back({e, packed ? pb + (n - m) : n});
+                tc.push_back({e, kind[c] == kPacked ? pb : n});
             }
             return true;
         };
@@ -347,12 +345,19 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
             live[b] = nullptr;
             // census + recode + bit-planes on the planner stream (one host sync)
             const double t0 = trace ? now_ms() : 0.0;
+            const bool known = kind[c] != kRaw;  // alphabet known (packed) or assumed (speculative)
             live[b] = seqset_create_device(P, stage[b], d_offs + b * oslot, offsets + 2 * lo, (uint32_t)(2 * cnt),
-                                           acgt[c] != 0, acgt[c] ? d_pack[b] : nullptr);
+                                           known, kind[c] == kPacked ? d_pack[b] : nullptr);
+            if (kind[c] == kSpec) {  // the assumption, checked on the device
+                const uint64_t nb = offsets[2 * hi] - offsets[2 * lo];
+                const int vg = (int)std::min<uint64_t>((nb + 4095) / 4096 + 1, (uint64_t)ctx->sm_count * 8);
+                verify_acgt_kernel<<<vg, 256, 0, P->stream>>>(stage[b], nb, d_flags + c);
+                DM_CUDA(cudaGetLastError());
+            }
             const double t1 = trace ? now_ms() : 0.0;
             // plan on the planner stream, kernels on ctx->stream
             lev_plan_then_launch(P, ctx, live[b], d_ab, d_ab + per, cnt, d_res + lo, ev.planned[b], tot,
-                                 acgt[c] ? offsets + 2 * lo : nullptr);
+                                 known ? offsets + 2 * lo : nullptr);
             DM_CUDA(cudaEventRecord(ev.done[b], ctx->stream));
             {
                 std::lock_guard<std::mutex> g(hs.mu);
@@ -374,7 +379,14 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
         packer.join();
         if (hs.err) std::rethrow_exception(hs.err);
         DM_CUDA(cudaMemcpyAsync(h_res, d_res, npairs * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        std::vector<uint32_t> flags(nchunks);
+        DM_CUDA(cudaMemcpyAsync(flags.data(), d_flags, nchunks * 4, cudaMemcpyDeviceToHost, ctx->stream));
         DM_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (uint64_t c = 0; c < nchunks; ++c)
+            if (flags[c]) {
+                if (!redo) throw cuda_error("internal error: unverified chunk without a redo list");
+                redo->push_back({cb[c], cb[c + 1]});
+            }
         if (tot) {
             tot->h2d_bytes += h2d_bytes;
             tot->d2h_bytes += npairs * 4;
@@ -423,7 +435,13 @@ extern "C" int dm_lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t
         DM_CUDA(cudaEventCreate(&t1));
         DM_CUDA(cudaEventRecord(t0, ctx->stream));
         dm::LevTotals tot;
-        dm::lev_pairs_packed(ctx, data, offsets, npairs, out, &tot, false);
+        std::vector<std::pair<uint64_t, uint64_t>> redo;
+        dm::lev_pairs_packed(ctx, data, offsets, npairs, out, &tot, true, &redo);
+        // speculative chunks that turned out not to be A/C/G/T only: again,
+        // on the exact path (rare; results overwritten in place)
+        for (const auto& r : redo)
+            dm::lev_pairs_packed(ctx, data, offsets + 2 * r.first, r.second - r.first, out + r.first, &tot, false,
+                                 nullptr);
         DM_CUDA(cudaEventRecord(t1, ctx->stream));
         DM_CUDA(cudaEventSynchronize(t1));
         float ms = 0;

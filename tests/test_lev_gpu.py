@@ -197,20 +197,22 @@ def test_context_shared_by_threads(dm, ctx, orc):
 
 @pytest.mark.parametrize("chunk", ["100000", "5000000"])
 def test_packed_upload_matches_raw_upload(dm, ctx, orc, monkeypatch, chunk):
-    """2-bit upload of A/C/G/T chunks (all of each chunk, or the default
-    packed head + raw tail) == raw upload, bit for bit; a chunk with any
-    other byte (here 'N', lower case) goes up raw. h2d_bytes shows which
+    """2-bit upload of A/C/G/T chunks (all chunks packed, or a mix with
+    speculative raw chunks) == raw upload, bit for bit; a chunk with any
+    other byte (here 'N', lower case) goes up raw, or, sent speculatively,
+    fails the device check and is recomputed. h2d_bytes shows which
     happened."""
     monkeypatch.setenv("DM_STREAM_CHUNK_BYTES", chunk)
     data, offs = dm.synth(1, scale=0.005)  # 5000 pairs, ~10 MB
     n = (len(offs) - 1) // 2
+    monkeypatch.setenv("DM_STREAM_RAW_FRAC", "0")
     full, sf = dm.lev_pairs_packed(data, offs, ctx, stats=True)
-    monkeypatch.setenv("DM_STREAM_PACK_FRAC", "0.6")
+    monkeypatch.setenv("DM_STREAM_RAW_FRAC", "0.5")
     split, sp = dm.lev_pairs_packed(data, offs, ctx, stats=True)
     monkeypatch.setenv("DM_STREAM_PACK", "0")
     raw, sr = dm.lev_pairs_packed(data, offs, ctx, stats=True)
     monkeypatch.delenv("DM_STREAM_PACK")
-    monkeypatch.delenv("DM_STREAM_PACK_FRAC")
+    monkeypatch.setenv("DM_STREAM_RAW_FRAC", "0")
     assert np.array_equal(split, raw) and np.array_equal(full, raw)
     # the host-counted bucket histogram (fully packed chunks) == the device one
     assert (sf["cells"], sf["cells_executed"], sf["launches"]) == (sr["cells"], sr["cells_executed"], sr["launches"])
@@ -231,16 +233,20 @@ def test_packed_upload_matches_raw_upload(dm, ctx, orc, monkeypatch, chunk):
         b = dirty[offs[2 * i + 1]:offs[2 * i + 2]]
         assert got[i] == orc.levenshtein(a, b), i
     assert np.array_equal(got[np.r_[100:n // 2 - 100]], raw[100:n // 2 - 100])
+    # every chunk speculative: the dirty ones fail the device check and are redone
+    monkeypatch.setenv("DM_STREAM_RAW_FRAC", "1")
+    spec = dm.lev_pairs_packed(dirty, offs, ctx)
+    assert np.array_equal(spec, got)
 
 
-@pytest.mark.parametrize("frac", ["1", "0.5"])
-@pytest.mark.parametrize("alphabet", ["ACGT", "GT"])
+@pytest.mark.parametrize("frac", ["0", "0.5", "1"])
+@pytest.mark.parametrize("alphabet", ["ACGT", "GT", "ACGTN"])
 @pytest.mark.parametrize("n", [1, 15, 16, 17, 63, 64, 65, 1000, 5000])
 def test_packed_upload_odd_lengths(dm, ctx, orc, monkeypatch, n, alphabet, frac):
-    """Chunk residue counts around the unpacker's 16-residue groups, chunks
-    missing some of A/C/G/T, fully and partly packed chunks."""
+    """Chunk residue counts around the verifier's 16-byte groups, chunks
+    missing some of A/C/G/T or holding an N, packed / speculative / mixed."""
     monkeypatch.setenv("DM_STREAM_CHUNK_BYTES", "1")  # one pair per chunk
-    monkeypatch.setenv("DM_STREAM_PACK_FRAC", frac)
+    monkeypatch.setenv("DM_STREAM_RAW_FRAC", frac)
     rng = random.Random(n)
     seqs = []
     for k in range(6):
