@@ -86,6 +86,8 @@ int dm_ctx_destroy(dm_ctx* ctx) {
         ctx->detach_buffers();  // scratch is freed synchronously once the stream is gone
         dm::comm_destroy(ctx);
         cudaEventDestroy(ctx->ev0);
+        for (cudaEvent_t e : ctx->stage_ev)
+            if (e) cudaEventDestroy(e);
         cudaEventDestroy(ctx->ev1);
         if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
         if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);

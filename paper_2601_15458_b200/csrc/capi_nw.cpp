@@ -5,7 +5,11 @@
 
 #include "capi_guard.h"
 #include "host_par.h"
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include "nw.h"
+#include "host_copy.h"
 
 // One batch of PairwiseResults (pairwise.hpp:78-84).
 struct dm_pw {
@@ -30,18 +34,22 @@ void check_symbols(const char* s, uint64_t n, const dm::NwScheme& sc, const char
     }
 }
 
+// s with a '-' inserted before residue asc[p] for each p (asc ascending; a
+// value n appends at the end), as runs of memcpy between the gaps
 std::string with_gaps(const char* s, uint64_t n, const std::vector<uint32_t>& asc) {
-    std::string out;
-    out.reserve(n + asc.size());
-    size_t p = 0;
-    for (uint64_t c = 0; c < n; ++c) {
-        while (p < asc.size() && asc[p] == c) {
-            out.push_back('-');
-            ++p;
+    std::string out(n + asc.size(), '-');
+    char* o = out.data();
+    uint64_t c = 0;
+    for (const uint32_t g : asc) {
+        const uint64_t upto = std::min<uint64_t>(g, n);
+        if (upto > c) {
+            std::memcpy(o, s + c, upto - c);
+            o += upto - c;
+            c = upto;
         }
-        out.push_back(s[c]);
+        ++o;  // the gap (already '-')
     }
-    for (; p < asc.size(); ++p) out.push_back('-');
+    if (n > c) std::memcpy(o, s + c, n - c);
     return out;
 }
 
@@ -74,17 +82,37 @@ void validate_tree(const std::vector<dm_node>& nodes, const std::vector<uint32_t
 
 void run_batch(dm_ctx* ctx, const char* A, const uint64_t* a_off, const char* B, const uint64_t* b_off,
                uint32_t njobs, const dm::NwScheme& sc, dm_pw* pw, dm_stats* st) {
+    const bool trace = std::getenv("DM_TRACE") != nullptr;
+    const auto t_start = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!trace) return;
+        DM_CUDA(cudaStreamSynchronize(ctx->stream));
+        std::fprintf(stderr, "[dm nw_batch] %s %.2f ms\n", what,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
+    };
     for (uint32_t k = 0; k < njobs; ++k)
         if (a_off[k + 1] == a_off[k] || b_off[k + 1] == b_off[k])
             throw dm::invalid_argument("nw_align requires non-empty inputs");
-    dm::host_parallel_for(njobs, 256, [&](uint64_t k) {
-        check_symbols(A + a_off[k], a_off[k + 1] - a_off[k], sc, "a");
-        check_symbols(B + b_off[k], b_off[k + 1] - b_off[k], sc, "b");
-    });
     const uint64_t abytes = a_off[njobs] - a_off[0], bbytes = b_off[njobs] - b_off[0];
     uint8_t* d_in = (uint8_t*)ctx->rows_b.get(abytes + bbytes + 16);
-    if (abytes) DM_CUDA(cudaMemcpyAsync(d_in, A + a_off[0], abytes, cudaMemcpyHostToDevice, ctx->stream));
-    if (bbytes) DM_CUDA(cudaMemcpyAsync(d_in + abytes, B + b_off[0], bbytes, cudaMemcpyHostToDevice, ctx->stream));
+    dm::upload_host(ctx, d_in, A + a_off[0], abytes, ctx->stream);
+    dm::upload_host(ctx, d_in + abytes, B + b_off[0], bbytes, ctx->stream);
+    mark("uploaded");
+    // symbols (pairwise.cpp:288-297), checked on the uploaded bytes: the first
+    // pair in batch order with a bad symbol reports it, a before b
+    const uint64_t bad_a = dm::nw_first_bad_symbol(ctx, d_in, abytes, sc.has);
+    const uint64_t bad_b = dm::nw_first_bad_symbol(ctx, d_in + abytes, bbytes, sc.has);
+    if (bad_a != UINT64_MAX || bad_b != UINT64_MAX) {
+        auto job_of = [](const uint64_t* off, uint32_t nj, uint64_t pos) {  // pair holding byte off[0] + pos
+            return (uint32_t)(std::upper_bound(off, off + nj + 1, off[0] + pos) - off - 1);
+        };
+        const uint32_t ka = bad_a != UINT64_MAX ? job_of(a_off, njobs, bad_a) : UINT32_MAX;
+        const uint32_t kb = bad_b != UINT64_MAX ? job_of(b_off, njobs, bad_b) : UINT32_MAX;
+        if (ka <= kb) check_symbols(A + a_off[ka], a_off[ka + 1] - a_off[ka], sc, "a");
+        else check_symbols(B + b_off[kb], b_off[kb + 1] - b_off[kb], sc, "b");
+        throw dm::cuda_error("internal error: symbol check disagrees with the host");
+    }
+    mark("checked");
     std::vector<dm::NwJob> jobs(njobs);
     for (uint32_t k = 0; k < njobs; ++k) {
         jobs[k].a_off = a_off[k] - a_off[0];
@@ -94,6 +122,7 @@ void run_batch(dm_ctx* ctx, const char* A, const uint64_t* a_off, const char* B,
     }
     dm::NwOut no;
     dm::nw_run(ctx, d_in, jobs, sc, no, st != nullptr);
+    mark("aligned");
     std::vector<dm::NwRes> res(njobs);
     if (njobs)
         DM_CUDA(cudaMemcpyAsync(res.data(), no.d_res, njobs * sizeof(dm::NwRes), cudaMemcpyDeviceToHost, ctx->stream));
@@ -102,6 +131,7 @@ void run_batch(dm_ctx* ctx, const char* A, const uint64_t* a_off, const char* B,
     std::vector<uint32_t> gaps;
     std::vector<uint64_t> goff;
     dm::nw_compact_gaps(ctx, no.d_gaps, jobs, res, gaps, goff);
+    mark("gaps back");
     pw->r.resize(njobs);
     dm::host_parallel_for(njobs, 64, [&](uint64_t k) {
         auto& o = pw->r[k];
@@ -114,6 +144,7 @@ void run_batch(dm_ctx* ctx, const char* A, const uint64_t* a_off, const char* B,
         o.a = with_gaps(A + a_off[k], jobs[k].n, o.gaps_a);
         o.b = with_gaps(B + b_off[k], jobs[k].m, o.gaps_b);
     });
+    mark("results assembled");
     if (st) {
         std::memset(st, 0, sizeof(*st));
         st->kernel_ms = no.fwd_ms + no.tb_ms;

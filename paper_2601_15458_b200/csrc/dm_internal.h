@@ -112,6 +112,8 @@ struct dm_ctx {
     int lev_rr = 0;
     cudaEvent_t lev_fork = nullptr, lev_join[kLevSide] = {};
     dm::PinnedBuf pin_items, pin_out;
+    dm::PinnedBuf pin_stage;                 // host_copy.cpp: double buffer for pageable uploads
+    cudaEvent_t stage_ev[2] = {};
     // scratch for the aligner / merge scheduler
     dm::DevBuf nw_in, nw_table, nw_jobs, nw_trace, nw_res, nw_gaps, nw_wrap, rows_a, rows_b, colmap, tree_buf;
     uint64_t launches = 0;

@@ -342,6 +342,38 @@ __global__ void compact_gaps_kernel(const uint32_t* __restrict__ gaps, const Com
 }
 }  // namespace
 
+namespace {
+__global__ void bad_symbol_kernel(const uint8_t* __restrict__ b, uint64_t n, uint32_t hasmask0, uint32_t hasmask1,
+                                  uint32_t hasmask2, uint32_t hasmask3, unsigned long long* __restrict__ first) {
+    const uint32_t m[4] = {hasmask0, hasmask1, hasmask2, hasmask3};
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint32_t c = b[i];
+        if (c >= 128 || !((m[c >> 5] >> (c & 31)) & 1u)) {
+            atomicMin(first, (unsigned long long)i);
+            return;  // later bytes of this thread are larger indices
+        }
+    }
+}
+}  // namespace
+
+uint64_t nw_first_bad_symbol(dm_ctx* ctx, const uint8_t* d_bytes, uint64_t n, const bool* has) {
+    if (n == 0) return UINT64_MAX;
+    uint32_t m[4] = {0, 0, 0, 0};
+    for (int c = 0; c < 128; ++c)
+        if (has[c]) m[c >> 5] |= 1u << (c & 31);
+    unsigned long long* d_first = ctx->aux.as<unsigned long long>(1);
+    DM_CUDA(cudaMemsetAsync(d_first, 0xff, 8, ctx->stream));
+    const int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)ctx->sm_count * 8);
+    bad_symbol_kernel<<<std::max(grid, 1), 256, 0, ctx->stream>>>(d_bytes, n, m[0], m[1], m[2], m[3], d_first);
+    DM_CUDA(cudaGetLastError());
+    ctx->launches += 1;
+    unsigned long long first = 0;
+    DM_CUDA(cudaMemcpyAsync(&first, d_first, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    DM_CUDA(cudaStreamSynchronize(ctx->stream));
+    return first;
+}
+
 void nw_compact_gaps(dm_ctx* ctx, const uint32_t* d_gaps, const std::vector<NwJob>& jobs,
                      const std::vector<NwRes>& res, std::vector<uint32_t>& out, std::vector<uint64_t>& off) {
     const uint64_t n = jobs.size();

@@ -67,4 +67,10 @@ void nw_run_sharded(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& job
 void nw_compact_gaps(dm_ctx* ctx, const uint32_t* d_gaps, const std::vector<NwJob>& jobs,
                      const std::vector<NwRes>& res, std::vector<uint32_t>& out, std::vector<uint64_t>& off);
 
+// Index of the first byte of d_bytes[0, n) that is not a symbol of the
+// scheme (>= 128 or has[c] false), or UINT64_MAX; one scan on ctx->stream
+// and one host sync. (pairwise.cpp:288-297 checks on the host; the batch
+// checks the uploaded bytes instead.)
+uint64_t nw_first_bad_symbol(dm_ctx* ctx, const uint8_t* d_bytes, uint64_t n, const bool* has);
+
 }  // namespace dm

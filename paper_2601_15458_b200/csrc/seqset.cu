@@ -18,6 +18,7 @@
 #include <cub/cub.cuh>
 
 #include "dm_internal.h"
+#include "host_copy.h"
 
 namespace dm {
 namespace {
@@ -360,7 +361,7 @@ dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets,
         s->d_raw_off = d_raw_off;
         std::vector<uint64_t> rel(n + 1);
         for (uint32_t i = 0; i <= n; ++i) rel[i] = offsets[i] - base;
-        if (nbytes && !d_raw_given) DM_CUDA(cudaMemcpyAsync(d_raw, data + base, nbytes, cudaMemcpyHostToDevice, st));
+        if (nbytes && !d_raw_given) upload_host(ctx, d_raw, data + base, nbytes, st);
         DM_CUDA(cudaMemcpyAsync(d_raw_off, rel.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st));
         s->raw_off = rel;
 
