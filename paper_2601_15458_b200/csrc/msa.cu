@@ -232,15 +232,20 @@ dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node
                     sides.push_back(SideDesc{rc.begin, rc.end, (uint32_t)W[nd.right], (uint32_t)w, 0,
                                              jobs[k].gb_off, res[k].ngb, 0});
             }
+            if (trace) DM_CUDA(cudaEventRecord(ctx->ev0, stream));
             grow_rows(ctx, rowsbuf, pitch, n, wmax);
             apply_sides(ctx, sides, no.d_gaps, (uint8_t*)rowsbuf.p, pitch, wold);
             launches += 2;
             if (trace) {
+                DM_CUDA(cudaEventRecord(ctx->ev1, stream));
                 DM_CUDA(cudaStreamSynchronize(stream));
+                float ins = 0;
+                cudaEventElapsedTime(&ins, ctx->ev0, ctx->ev1);
                 const double ms =
                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
-                std::fprintf(stderr, "[dm align] depth %d merges %zu cells %.3e fwd %.3f ms tb %.3f ms level %.3f ms\n",
-                             d, jobs.size(), (double)no.cells, no.fwd_ms, no.tb_ms, ms);
+                std::fprintf(stderr,
+                             "[dm align] depth %d merges %zu cells %.3e fwd %.3f ms tb %.3f ms insert %.3f ms level %.3f ms\n",
+                             d, jobs.size(), (double)no.cells, no.fwd_ms, no.tb_ms, ins, ms);
             }
         }
         const uint64_t width = W[0];
