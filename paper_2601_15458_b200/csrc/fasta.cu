@@ -22,6 +22,7 @@
 #include <string_view>
 #include <vector>
 
+#include "host_copy.h"
 #include "capi_guard.h"
 #include "pipeline.h"
 
@@ -181,7 +182,7 @@ std::string format_on_device(dm_ctx* ctx, const uint8_t* d_res, const std::vecto
     fasta_format_kernel<<<grid, 256, 0, ctx->stream>>>(d_res, d_hdr, d_recs, n, d_out);
     DM_CUDA(cudaGetLastError());
     ++ctx->launches;
-    DM_CUDA(cudaMemcpyAsync(text.data(), d_out, total, cudaMemcpyDeviceToHost, ctx->stream));
+    download_host(ctx, text.data(), d_out, total, ctx->stream);
     DM_CUDA(cudaStreamSynchronize(ctx->stream));
     return text;
 }

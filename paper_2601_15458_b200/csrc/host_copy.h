@@ -17,4 +17,13 @@ namespace dm {
 // executed the copy.
 void upload_host(dm_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st);
 
+// The reverse for `rows` rows of `width` bytes at device pitch `pitch` into a
+// dense host buffer; synchronous (returns with `dst` filled). Large copies
+// into pageable memory go through the pinned double buffer, each half's
+// spill to `dst` (host pool) overlapping the next half's download.
+void download_rows(dm_ctx* ctx, void* dst, const void* src, size_t width, size_t pitch, size_t rows,
+                   cudaStream_t st);
+// Dense device -> host copy of `bytes` (same staging), synchronous.
+void download_host(dm_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st);
+
 }  // namespace dm

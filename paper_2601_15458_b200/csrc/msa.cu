@@ -25,6 +25,7 @@
 #include <numeric>
 
 #include "dm_internal.h"
+#include "host_copy.h"
 #include "nw.h"
 
 namespace dm {
@@ -252,9 +253,7 @@ dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node
         out->width = width;
         out->dev_pitch = pitch;
         out->rows.resize((uint64_t)n * width);
-        if (width)
-            DM_CUDA(cudaMemcpy2DAsync(out->rows.data(), width, rowsbuf.p, pitch, width, n, cudaMemcpyDeviceToHost,
-                                      stream));
+        if (width) download_rows(ctx, out->rows.data(), rowsbuf.p, width, pitch, n, stream);
         DM_CUDA(cudaStreamSynchronize(stream));
         out->row_seq = order;
         out->nodes = nodes;
