@@ -290,6 +290,11 @@ def main():
         return run_reference(args)
 
     rank, world, local = dist_env()
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    if local_world > 1 and "DM_HOST_THREADS" not in os.environ:
+        # one process per GPU on this node: split the host cores between the
+        # ranks' packing pools instead of oversubscribing them
+        os.environ["DM_HOST_THREADS"] = str(max(1, (os.cpu_count() or 1) // local_world))
     import torch
     torch.cuda.set_device(local)
     if world > 1:
