@@ -66,7 +66,7 @@ def _sha_rows(rows):
     return h.hexdigest()
 
 
-@pytest.mark.parametrize("key", ["cfg0@1.0", "cfg3@1.0", "cfg2@0.1", "cfg2@1.0"])
+@pytest.mark.parametrize("key", ["cfg0@1.0", "cfg3@1.0", "cfg2@0.1", "cfg2@1.0", "cfg4@1.0"])
 def test_config_msa_golden(dm, ctx, key):
     """Full-size BASELINE configs: tree and MSA bytes equal the reference's (by SHA-256)."""
     big = load("msa_configs.json")
