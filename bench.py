@@ -278,7 +278,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scale", type=float, default=1.0, help="fraction of cfg1's 10^6 pairs per GPU")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--ref-step-s", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -384,7 +384,8 @@ def main():
                                         offs_c.ctypes.data_as(C.POINTER(C.c_uint64)), n_pairs,
                                         out_h.ctypes.data_as(u32p), C.byref(est)))
 
-    e2e_step()
+    for _ in range(2):  # warm-up: pinned slots, host pool, chunk buffers
+        e2e_step()
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
