@@ -130,17 +130,43 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
         big = small = std::max<uint64_t>(1, std::strtoull(env, nullptr, 10));
     if (const char* env = std::getenv("DM_STREAM_BIG_MB")) big = std::max<uint64_t>(1, std::strtoull(env, nullptr, 10)) << 20;
     if (const char* env = std::getenv("DM_STREAM_SMALL_MB")) small = std::max<uint64_t>(1, std::strtoull(env, nullptr, 10)) << 20;
+    const char* pk = std::getenv("DM_STREAM_PACK");
+    const bool pack = !(pk && pk[0] == '0');
+    // Share of the residue bytes sent raw (speculative chunks, see the top):
+    // the copy engine reads them from host memory while the host threads
+    // pack the rest, which uses host memory bandwidth better than packing
+    // everything (measured on the box: pack alone ~100 GB/s; pack + raw copy
+    // 82 + 54 GB/s); at ~0.3 the bus and the packers finish together. Needs
+    // a pinned `data`.
+    double raw_frac = 0.0;
+    if (speculate && pack) {
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, data) == cudaSuccess && pa.type == cudaMemoryTypeHost) raw_frac = 0.3;
+        cudaGetLastError();
+        if (const char* e = std::getenv("DM_STREAM_RAW_FRAC")) raw_frac = std::min(1.0, std::max(0.0, std::atof(e)));
+    }
+    // Raw chunks are at most half the big size: a raw chunk's upload (4x the
+    // bytes of a packed one) should not outlast the kernels of the chunk
+    // before it.
     std::vector<uint64_t> cb{0};
+    std::vector<char> spec;  // chunk k goes up raw (speculative)
+    uint64_t raw_sofar = 0, all_sofar = 0;
     for (uint64_t lo = 0, k = 0; lo < npairs; ++k) {
         const uint64_t rem = offsets[2 * npairs] - offsets[2 * lo];
         uint64_t t = std::min(big, small << std::min<uint64_t>(k, 20));
         if (rem < 2 * t) t = std::max(small, rem / 2);
+        const bool raw = (double)raw_sofar < raw_frac * (double)(all_sofar + t);
+        if (raw) t = std::max<uint64_t>(std::min(t, big / 2), 1);
         // smallest hi > lo with offsets[2hi] - offsets[2lo] >= t
         uint64_t a = lo + 1, z = npairs;
         while (a < z) {
             const uint64_t mid = (a + z) / 2;
             if (offsets[2 * mid] - offsets[2 * lo] >= t) z = mid; else a = mid + 1;
         }
+        const uint64_t n = offsets[2 * a] - offsets[2 * lo];
+        all_sofar += n;
+        if (raw && n > 0) raw_sofar += n;
+        spec.push_back(raw && n > 0);
         lo = a;
         cb.push_back(lo);
     }
@@ -214,8 +240,6 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
         uint32_t* h_res = ctx->pin_out.as<uint32_t>(npairs);
         uint32_t* d_flags = ctx->stream_flags.as<uint32_t>(nchunks);  // speculative chunk c held a non-ACGT byte
         DM_CUDA(cudaMemsetAsync(d_flags, 0, nchunks * 4, ctx->stream));
-        const char* pk = std::getenv("DM_STREAM_PACK");
-        const bool pack = !(pk && pk[0] == '0');
         // per-sequence 2-bit layout (code_bytes): < L / 4 + 32 bytes per sequence
         const uint64_t packed_cap = maxbytes / 4 + 32 * (2 * per) + 64;
         uint8_t* d_pack[NB] = {};
@@ -246,19 +270,6 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
         // kRaw — uploaded raw, alphabet from the device census.
         enum : char { kRaw = 0, kPacked = 1, kSpec = 2 };
         std::vector<char> kind(nchunks, kRaw);
-        // Share of the residue bytes sent raw: the copy engine reads them from
-        // host memory while the host threads pack the rest, which uses host
-        // memory bandwidth better than packing everything (measured on the
-        // box: pack alone ~100 GB/s; pack + raw copy 82 + 54 GB/s); at ~0.3
-        // the bus and the packers finish together. Needs a pinned `data`.
-        double raw_frac = 0.0;
-        if (speculate && pack) {
-            cudaPointerAttributes pa{};
-            if (cudaPointerGetAttributes(&pa, data) == cudaSuccess && pa.type == cudaMemoryTypeHost) raw_frac = 0.3;
-            cudaGetLastError();
-            if (const char* e = std::getenv("DM_STREAM_RAW_FRAC")) raw_frac = std::min(1.0, std::max(0.0, std::atof(e)));
-        }
-        uint64_t raw_sofar = 0, all_sofar = 0;  // packer thread only
         auto issue_copy = [&](uint64_t c) {
             const int b = (int)(c % NB);
             const uint64_t lo = cb[c], hi = cb[c + 1];
@@ -276,12 +287,10 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
             DM_CUDA(cudaMemcpyAsync(d_offs + b * oslot, h_offs + b * oslot, (2 * (hi - lo) + 1) * 8,
                                     cudaMemcpyHostToDevice, ctx->copy_stream));
             h2d_bytes += (2 * (hi - lo) + 1) * 8;
-            all_sofar += n;
             const double tp0 = trace ? now_ms() : 0.0;
             uint64_t pb = 0;  // packed bytes
-            if (n > 0 && (double)raw_sofar < raw_frac * (double)all_sofar) {
+            if (spec[c]) {
                 kind[c] = kSpec;
-                raw_sofar += n;
             } else if (pack && n >= 256 && pack_acgt_seqs(data, offsets + 2 * lo, 2 * (hi - lo), h_pack[b], &pb)) {
                 kind[c] = kPacked;  // straight into the set's 2-bit code layout
             }
