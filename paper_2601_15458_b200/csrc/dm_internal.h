@@ -107,6 +107,12 @@ struct dm_ctx {
     dm::DevBuf ss_meta, ss_codes, ss_planes;  // planner contexts: the chunk's sequence set (reused)
     dm::PinnedBuf pin_pack[kStreamSlots];   // host side of the same
     dm_ctx* prep[kStreamSlots] = {};  // planner contexts of the streamed path (own stream + scratch)
+    // words per lane the lane count per pair is chosen for on this context
+    // (0: the alphabet's maximum; patterns too long for it still use up to
+    // the maximum); the streamed path's planners use 20 -- its chunks share
+    // the SMs with planning and uploads, where the 2-block-per-SM kernels of
+    // 21-24 words measured slower end to end
+    int lev_wmax_cap = 0;
     static constexpr int kLevSide = 8;  // side streams the distance buckets fan out on
     cudaStream_t lev_side[kLevSide] = {};
     int lev_rr = 0;

@@ -52,7 +52,7 @@ constexpr unsigned FULL = 0xffffffffu;
 template <int NP>
 struct WMax;
 template <>
-struct WMax<2> { static constexpr int value = 16; };
+struct WMax<2> { static constexpr int value = 24; };
 template <>
 struct WMax<5> { static constexpr int value = 10; };
 template <>
@@ -117,7 +117,7 @@ __device__ __forceinline__ uint32_t shl1(uint32_t (&v)[W], uint32_t cin, uint32_
 }
 
 template <int NP, int W>
-__global__ void __launch_bounds__(256, NP == 2 ? 3 : 1) lev_kernel(const LevArgs a) {
+__global__ void __launch_bounds__(256, NP == 2 ? (W <= 16 ? 3 : 2) : 1) lev_kernel(const LevArgs a) {
     constexpr bool TAB = NP == 2;
     extern __shared__ uint32_t s_tab[];  // TAB: 4 codes x W words x 256 threads
     // opaque constants (derived from the runtime 1) keep the bit arithmetic on IMAD
@@ -378,7 +378,7 @@ constexpr int kLevSide = dm_ctx::kLevSide;
 // radix key (bucket << 32 | ~n) so one sort groups buckets and balances warps.
 __global__ void plan_kernel(const uint32_t* __restrict__ ia, const uint32_t* __restrict__ ib,
                             const LevItem* __restrict__ in_items, uint64_t n,
-                            const uint32_t* __restrict__ len, int lg_gpar, int wmax,
+                            const uint32_t* __restrict__ len, int lg_gpar, int wsel, int wmax,
                             LevItem* __restrict__ items, uint64_t* __restrict__ keys,
                             uint32_t* __restrict__ idx, unsigned int* __restrict__ hist,
                             unsigned long long* __restrict__ cells) {
@@ -407,7 +407,7 @@ __global__ void plan_kernel(const uint32_t* __restrict__ ia, const uint32_t* __r
         }
         const uint32_t B = (lx + 31) >> 5;  // 32-row words of the pattern
         int lg = lg_gpar;
-        while ((uint32_t)(wmax << lg) < B && lg < 5) ++lg;
+        while ((uint32_t)(wsel << lg) < B && lg < 5) ++lg;
         uint32_t R = (B + (1u << lg) - 1) >> lg;  // words per lane
         if (R < 1) R = 1;
         uint32_t bucket = (uint32_t)lg * 32 + R;
@@ -446,14 +446,14 @@ struct LevPlan {
 
 // plan_kernel's histogram and cell counts for pairs (2i, 2i+1) of host
 // offsets, counted on the host (same orientation and bucket rule).
-void plan_hist_host(const uint64_t* offs, uint64_t n, int lg_gpar, int wmax, LevPlan& P) {
+void plan_hist_host(const uint64_t* offs, uint64_t n, int lg_gpar, int wsel, int wmax, LevPlan& P) {
     // lg per pattern word count B (beyond the table: 5); the per-pair body is
     // branch-free (random orientations would mispredict)
-    const uint32_t bmax = (uint32_t)wmax << 5;
+    const uint32_t bmax = (uint32_t)wsel << 5;
     std::vector<uint8_t> lgof(bmax + 2);
     for (uint32_t B = 0; B <= bmax + 1; ++B) {
         int lg = lg_gpar;
-        while ((uint32_t)(wmax << lg) < B && lg < 5) ++lg;
+        while ((uint32_t)(wsel << lg) < B && lg < 5) ++lg;
         lgof[B] = (uint8_t)lg;
     }
     std::vector<unsigned int> h(4 * kBuckets, 0u);  // 4 interleaved copies: no store-forwarding chains
@@ -488,6 +488,9 @@ void plan_batch(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const uin
         const int v = std::atoi(e);
         if (v >= 1 && v < wmax) wmax = v;
     }
+    // lanes per pair are chosen for at most `wsel` words per lane; longer
+    // patterns (lanes per pair maxed out) still go up to wmax
+    const int wsel = ctx->lev_wmax_cap > 0 ? std::min(wmax, ctx->lev_wmax_cap) : wmax;
     const uint64_t target = (uint64_t)ctx->sm_count * 512;  // lanes wanted in flight
     int lg_gpar = 0;
     while (lg_gpar < 5 && (n << lg_gpar) < target) ++lg_gpar;
@@ -515,14 +518,14 @@ void plan_batch(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const uin
 
     DM_CUDA(cudaMemsetAsync(hist, 0, hist_b, st));
     const int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)ctx->sm_count * 8);
-    plan_kernel<<<grid, 256, 0, st>>>(d_ia, d_ib, d_in_items, n, s->d_len, lg_gpar, wmax, it0, k0, i0,
+    plan_kernel<<<grid, 256, 0, st>>>(d_ia, d_ib, d_in_items, n, s->d_len, lg_gpar, wsel, wmax, it0, k0, i0,
                                       hist, cells);
     DM_CUDA(cudaGetLastError());
     DM_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_b, k0, k1, i0, i1, (int)n, 0, 40, st));
     gather_items<<<grid, 256, 0, st>>>(it0, i1, n, it1);
     DM_CUDA(cudaGetLastError());
     if (pair_offs) {
-        plan_hist_host(pair_offs, n, lg_gpar, wmax, P);
+        plan_hist_host(pair_offs, n, lg_gpar, wsel, wmax, P);
     } else {
         DM_CUDA(cudaMemcpyAsync(P.h, hist, sizeof(P.h), cudaMemcpyDeviceToHost, st));
         DM_CUDA(cudaMemcpyAsync(P.hc, cells, sizeof(P.hc), cudaMemcpyDeviceToHost, st));
