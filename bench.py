@@ -416,11 +416,11 @@ def main():
     roof_gcups = p_int32 / C_LEV / 1e9
     roofline = {"bound": "int32", "achieved": kernel_gcups, "peak": roof_gcups, "unit": "GCUPS",
                 "frac": kernel_gcups / roof_gcups,
-                # DRAM bytes of one captured launch (profiles/r01_ncu_lev_r5_full.txt,
-                # lev_kernel<2,15>: 501 blocks, 1.20 ms): 64.1 MB read + 1.2 MB
+                # DRAM bytes of one captured launch (profiles/r01_ncu_lev_r6_full.txt,
+                # lev_kernel<2,16>: 503 blocks, 1.37 ms): 65.8 MB read + 1.5 MB
                 # written, ~0.7 % of HBM bandwidth -- the kernel is INT32-bound
-                "traffic": 65317888,
-                "traffic_source": "ncu --set full, one lev_kernel<2,15> launch of bench.py (cold L2)",
+                "traffic": 67267072,
+                "traffic_source": "ncu --set full, one lev_kernel<2,16> launch of bench.py (cold L2)",
                 "peak_source": (f"measured INT32 lane-op/s {p_int32:.3e} (max of LOP3 {peaks[0]:.3e}, "
                                 f"IMAD {peaks[1]:.3e}, LOP3+IMAD {peaks[2]:.3e}) / c_lev=10/32 ops per cell"),
                 "kernel": "lev_kernel<NP=2,R> (all buckets)",
