@@ -109,9 +109,10 @@ struct dm_ctx {
     dm_ctx* prep[kStreamSlots] = {};  // planner contexts of the streamed path (own stream + scratch)
     // words per lane the lane count per pair is chosen for on this context
     // (0: the alphabet's maximum; patterns too long for it still use up to
-    // the maximum); the streamed path's planners use 20 -- its chunks share
-    // the SMs with planning and uploads, where the 2-block-per-SM kernels of
-    // 21-24 words measured slower end to end
+    // the maximum); the streamed path's planners use 16 (DM_STREAM_WSEL) --
+    // its chunks share the SMs with planning and uploads, where the
+    // 2-block-per-SM kernels of 17-24 words measured slower end to end
+    // (32.5 / 32.9 / 34.1 ms per cfg1 step at 16 / 20 / 24)
     int lev_wmax_cap = 0;
     static constexpr int kLevSide = 8;  // side streams the distance buckets fan out on
     cudaStream_t lev_side[kLevSide] = {};

@@ -79,7 +79,8 @@ dm_ctx* prep_context(dm_ctx* ctx, int k) {
         auto* p = new dm_ctx;
         p->device = ctx->device;
         p->sm_count = ctx->sm_count;
-        p->lev_wmax_cap = 20;
+        p->lev_wmax_cap = 16;
+        if (const char* e = std::getenv("DM_STREAM_WSEL")) p->lev_wmax_cap = std::max(1, std::atoi(e));
         // planners run at high priority: their blocks take the first SM slots
         // the distance kernels free (the host waits on them)
         int least = 0, greatest = 0;
