@@ -6,6 +6,9 @@
 #include <string>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "capi_guard.h"
 #include "comm.h"
@@ -14,6 +17,30 @@ namespace dm {
 std::string& last_error() {
     thread_local std::string e;
     return e;
+}
+
+int occupancy(const void* kern, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, int, size_t>, int> occ;
+    static std::map<std::pair<const void*, int>, size_t> optin;  // smem limit set per (kernel, device)
+    int dev = 0;
+    DM_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_tuple(kern, dev, threads, smem);
+    auto it = occ.find(key);
+    if (it != occ.end()) return it->second;
+    if (smem > 48 * 1024) {
+        size_t& lim = optin[{kern, dev}];
+        if (smem > lim) {
+            DM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            lim = smem;
+        }
+    }
+    int o = 0;
+    DM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem));
+    if (o < 1) throw runtime_error("kernel does not fit on an SM (" + std::to_string(smem) + " B shared memory)");
+    occ[key] = o;
+    return o;
 }
 }  // namespace dm
 

@@ -31,12 +31,18 @@ int guard(F&& f) {
     }
 }
 
-// guard() holding the context's lock (null ctx: no lock; the body reports it)
+// guard() holding the context's lock (null ctx: no lock; the body reports it),
+// with the context's device current on this host thread (a process may hold
+// contexts on several GPUs, and the calling thread's current device is the
+// caller's business).
 template <class F>
 int guard(dm_ctx* ctx, F&& f) {
     if (!ctx) return guard(std::forward<F>(f));
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
-    return guard(std::forward<F>(f));
+    return guard([&] {
+        DM_CUDA(cudaSetDevice(ctx->device));
+        f();
+    });
 }
 
 inline void require(bool ok, const char* msg) {

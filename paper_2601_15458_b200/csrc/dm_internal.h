@@ -100,6 +100,10 @@ struct dm_ctx {
     void* nccl = nullptr;      // ncclComm_t
     // scratch for the distance engine
     dm::DevBuf items, out, counter, aux, aux2, aux3, lev_all, lev_items;
+    // multi-pass distance jobs (lev.cu run_long): plain cudaMalloc (not
+    // stream-ordered: they are used on the side streams)
+    dm::DevBuf lev_long_off, lev_long_h;
+    dm::PinnedBuf pin_long;
     cudaStream_t copy_stream = nullptr;  // host->device staging of streamed batches
     static constexpr int kStreamSlots = 4;  // chunks of a streamed batch in flight
     dm::DevBuf stage[kStreamSlots], stream_pairs, stream_out, stream_offs, stream_flags;
@@ -199,13 +203,19 @@ struct dm_msa_out {
 
 namespace dm {
 
+// Resident blocks per SM of `kern` at (threads, dynamic smem) on the current
+// device, cached per (kernel, device, threads, smem) and thread-safe; opts the
+// kernel into more than 48 KB of dynamic shared memory on that device when
+// smem needs it (capi.cpp).
+int occupancy(const void* kern, int threads, size_t smem);
+
 struct NwScheme;
 
 // One Levenshtein job: distance(seq pat, seq txt) -> out[slot].
 struct LevItem {
     uint32_t pat;
     uint32_t txt;
-    uint32_t slot;
+    uint64_t slot;  // 64-bit: per-level candidate matrices can exceed 2^32 cells
 };
 
 struct LevTotals {

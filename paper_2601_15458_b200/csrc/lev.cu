@@ -33,6 +33,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -73,6 +74,14 @@ struct LevArgs {
     uint32_t* counter;
     uint32_t one;        // == 1; opaque to ptxas so the carry chains stay on the FMA pipe
     uint32_t max_pulls;  // task pulls per warp before its block retires (see launch_one)
+    // multi-pass mode (LONG kernels, patterns longer than one warp's rows):
+    // pass `pass` covers pattern rows [pass * 1024 W, (pass + 1) * 1024 W);
+    // hbuf + hoff[item] holds, per text column, the horizontal delta leaving
+    // the previous pass's bottom row (2 bits: h_minus << 1 | h_plus), and is
+    // overwritten in place with the one leaving this pass.
+    uint8_t* hbuf;
+    const uint64_t* hoff;
+    uint32_t pass;
 };
 
 // One lane = W consecutive 32-bit words of the pattern, handled as ONE
@@ -116,7 +125,11 @@ __device__ __forceinline__ uint32_t shl1(uint32_t (&v)[W], uint32_t cin, uint32_
     return __umulhi(t[W - 1], two);
 }
 
-template <int NP, int W>
+// LONG: the multi-pass form for patterns longer than 32 lanes x W words
+// (Myers' block formulation across passes: the same recurrence, with the
+// horizontal delta between row blocks carried through global memory instead
+// of a shuffle). One warp (G = 32) per job, checked columns only.
+template <int NP, int W, bool LONG = false>
 __global__ void __launch_bounds__(256, NP == 2 ? (W <= 16 ? 3 : 2) : 1) lev_kernel(const LevArgs a) {
     constexpr bool TAB = NP == 2;
     extern __shared__ uint32_t s_tab[];  // TAB: 4 codes x W words x 256 threads
@@ -138,8 +151,16 @@ __global__ void __launch_bounds__(256, NP == 2 ? (W <= 16 ? 3 : 2) : 1) lev_kern
         const bool valid = it < a.nitems;
         LevItem item{0, 0, 0};
         if (valid) item = a.items[it];
-        const uint32_t m = valid ? a.len[item.pat] : 0;
+        constexpr uint32_t kPassRows = 32u * W * 32u;
+        uint32_t m = valid ? a.len[item.pat] : 0;
         const uint32_t n = valid ? a.len[item.txt] : 0;
+        uint64_t blk0 = a.blk[item.pat];
+        if constexpr (LONG) {
+            const uint32_t done = a.pass * kPassRows;  // rows handled by earlier passes
+            if (m <= done) continue;                   // whole warp: one job per warp
+            m = min(m - done, kPassRows);
+            blk0 += done / 64u;
+        }
         const uint32_t nwords = (m + 31) >> 5;
 
         // NP == 2 (<= 4 residue codes, DNA): the lane's match masks for all
@@ -150,7 +171,7 @@ __global__ void __launch_bounds__(256, NP == 2 ? (W <= 16 ? 3 : 2) : 1) lev_kern
         constexpr int NPR = TAB ? 1 : NP;
         uint32_t P[NPR][W];
         uint32_t Pv[W], Mv[W];
-        const uint32_t* pp = reinterpret_cast<const uint32_t*>(a.planes + a.blk[item.pat] * NP);
+        const uint32_t* pp = reinterpret_cast<const uint32_t*>(a.planes + blk0 * NP);
 #pragma unroll
         for (int w = 0; w < W; ++w) {
             const uint32_t gw = (uint32_t)g * W + w;  // global word index in the pattern
@@ -177,6 +198,8 @@ __global__ void __launch_bounds__(256, NP == 2 ? (W <= 16 ? 3 : 2) : 1) lev_kern
         steps = __reduce_max_sync(FULL, steps);
         const uint8_t* tp = a.codes + a.off[item.txt];
         const bool lead = g == 0 && valid;  // lane reading the text
+        [[maybe_unused]] uint8_t* hb = nullptr;
+        if constexpr (LONG) hb = a.hbuf + a.hoff[it];
         const uint32_t leadmask = g == 0 ? 0xffffffffu : 0u;
         uint32_t word = 0;
         // One text column through the lane pipeline. CHK: some lane of the
@@ -255,6 +278,9 @@ __global__ void __launch_bounds__(256, NP == 2 ? (W <= 16 ? 3 : 2) : 1) lev_kern
                 }
             }
             word = imad(c, four, imad(hm, two, hp));
+            if constexpr (LONG) {  // bottom lane: the delta leaving this pass, in place
+                if (g == G - 1 && j < n) hb[j] = (uint8_t)(word & 3u);
+            }
         };
         // steady state [s0, s1): every valid lane has 0 <= j < n - 1
         uint32_t nmin = __reduce_min_sync(FULL, valid ? n : 0xffffffffu);
@@ -271,60 +297,67 @@ __global__ void __launch_bounds__(256, NP == 2 ? (W <= 16 ? 3 : 2) : 1) lev_kern
             return imad(c, four, a.one);
         };
         uint32_t s = 0;
-        for (; s < s0; ++s) column(s, std::true_type{}, code_at(s));
-        if constexpr (TAB) {
-            // steady state, 16 columns per text word (2-bit codes), taken 4 at a
-            // time from a register (the 4-column body is not unrolled further:
-            // instruction cache)
-            for (; s < s1 && (s & 15u); ++s) column(s, std::false_type{}, code_at(s));
-            for (; s + 16 <= s1; s += 16) {
-                uint32_t w16 = lead ? __ldg(tw + (s >> 4)) : 0u;
-#pragma unroll 1
-                for (uint32_t q = 0; q < 16; q += 4) {
-                    // word k = (code_k << 2) | 1, one or two ops each
-                    column(s + q, std::false_type{}, lop3<0xEA>(w16 << 2, 0xcu, 1u));
-                    column(s + q + 1, std::false_type{}, lop3<0xEA>(w16, 0xcu, 1u));
-                    column(s + q + 2, std::false_type{}, lop3<0xEA>(w16 >> 2, 0xcu, 1u));
-                    column(s + q + 3, std::false_type{}, lop3<0xEA>(w16 >> 4, 0xcu, 1u));
-                    w16 >>= 8;
+        if constexpr (LONG) {
+            // lane 0's word: text code, h_in from the previous pass (+1 on the first)
+            for (; s < steps; ++s) {
+                uint32_t w0 = code_at(s);
+                if (a.pass > 0 && lead && s < n) w0 = (w0 & ~3u) | hb[s];
+                column(s, std::true_type{}, w0);
+            }
+        } else {
+            for (; s < s0; ++s) column(s, std::true_type{}, code_at(s));
+            if constexpr (TAB) {
+                // steady state, 16 columns per text word (2-bit codes), taken 4 at a
+                // time from a register (the 4-column body is not unrolled further:
+                // instruction cache)
+                for (; s < s1 && (s & 15u); ++s) column(s, std::false_type{}, code_at(s));
+                for (; s + 16 <= s1; s += 16) {
+                    uint32_t w16 = lead ? __ldg(tw + (s >> 4)) : 0u;
+    #pragma unroll 1
+                    for (uint32_t q = 0; q < 16; q += 4) {
+                        // word k = (code_k << 2) | 1, one or two ops each
+                        column(s + q, std::false_type{}, lop3<0xEA>(w16 << 2, 0xcu, 1u));
+                        column(s + q + 1, std::false_type{}, lop3<0xEA>(w16, 0xcu, 1u));
+                        column(s + q + 2, std::false_type{}, lop3<0xEA>(w16 >> 2, 0xcu, 1u));
+                        column(s + q + 3, std::false_type{}, lop3<0xEA>(w16 >> 4, 0xcu, 1u));
+                        w16 >>= 8;
+                    }
                 }
             }
-        }
-        // steady state, four columns per text load (4-aligned code runs)
-        for (; s < s1 && (s & 3u); ++s) column(s, std::false_type{}, code_at(s));
-        for (; s + 4 <= s1; s += 4) {
-            if constexpr (TAB) {
-                // 4 codes in bits 0..7 of t4; word k = (code_k << 2) | 1, one or two ops each
-                const uint32_t t4 = lead ? __ldg(tw + (s >> 4)) >> ((s & 12u) * 2u) : 0u;
-                column(s, std::false_type{}, lop3<0xEA>(t4 << 2, 0xcu, 1u));
-                column(s + 1, std::false_type{}, lop3<0xEA>(t4, 0xcu, 1u));
-                column(s + 2, std::false_type{}, lop3<0xEA>(t4 >> 2, 0xcu, 1u));
-                column(s + 3, std::false_type{}, lop3<0xEA>(t4 >> 4, 0xcu, 1u));
-            } else {
-                const uint32_t t4 = lead ? __ldg(reinterpret_cast<const uint32_t*>(tp + s)) : 0u;
-                column(s, std::false_type{}, imad(t4 & 0xffu, four, a.one));
-                column(s + 1, std::false_type{}, imad(__byte_perm(t4, 0u, 0x4441u), four, a.one));
-                column(s + 2, std::false_type{}, imad(__byte_perm(t4, 0u, 0x4442u), four, a.one));
-                column(s + 3, std::false_type{}, imad(t4 >> 24, four, a.one));
+            // steady state, four columns per text load (4-aligned code runs)
+            for (; s < s1 && (s & 3u); ++s) column(s, std::false_type{}, code_at(s));
+            for (; s + 4 <= s1; s += 4) {
+                if constexpr (TAB) {
+                    // 4 codes in bits 0..7 of t4; word k = (code_k << 2) | 1, one or two ops each
+                    const uint32_t t4 = lead ? __ldg(tw + (s >> 4)) >> ((s & 12u) * 2u) : 0u;
+                    column(s, std::false_type{}, lop3<0xEA>(t4 << 2, 0xcu, 1u));
+                    column(s + 1, std::false_type{}, lop3<0xEA>(t4, 0xcu, 1u));
+                    column(s + 2, std::false_type{}, lop3<0xEA>(t4 >> 2, 0xcu, 1u));
+                    column(s + 3, std::false_type{}, lop3<0xEA>(t4 >> 4, 0xcu, 1u));
+                } else {
+                    const uint32_t t4 = lead ? __ldg(reinterpret_cast<const uint32_t*>(tp + s)) : 0u;
+                    column(s, std::false_type{}, imad(t4 & 0xffu, four, a.one));
+                    column(s + 1, std::false_type{}, imad(__byte_perm(t4, 0u, 0x4441u), four, a.one));
+                    column(s + 2, std::false_type{}, imad(__byte_perm(t4, 0u, 0x4442u), four, a.one));
+                    column(s + 3, std::false_type{}, imad(t4 >> 24, four, a.one));
+                }
             }
+            for (; s < s1; ++s) column(s, std::false_type{}, code_at(s));
+            for (; s < steps; ++s) column(s, std::true_type{}, code_at(s));
         }
-        for (; s < s1; ++s) column(s, std::false_type{}, code_at(s));
-        for (; s < steps; ++s) column(s, std::true_type{}, code_at(s));
         for (int o = G >> 1; o > 0; o >>= 1) partial += __shfl_down_sync(FULL, partial, o, G);
-        if (valid && g == 0) a.out[item.slot] = n + (uint32_t)partial;
+        // D[m][n] = n + sum of the vertical deltas of every row block at column n
+        if (valid && g == 0) {
+            if (LONG && a.pass > 0) a.out[item.slot] += (uint32_t)partial;
+            else a.out[item.slot] = n + (uint32_t)partial;
+        }
     }
 }
 
-template <int NP, int W>
+template <int NP, int W, bool LONG = false>
 void launch_one(const LevArgs& a, int sm_count, cudaStream_t st) {
-    static int occ = -1;
     const size_t smem = NP == 2 ? (size_t)4 * W * 256 * sizeof(uint32_t) : 0;
-    if (occ < 0) {
-        if (smem > 48 * 1024)
-            DM_CUDA(cudaFuncSetAttribute(lev_kernel<NP, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        DM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lev_kernel<NP, W>, 256, smem));
-        occ = std::max(occ, 1);
-    }
+    const int occ = occupancy((const void*)lev_kernel<NP, W, LONG>, 256, smem);
     // Warps pull tasks (32/G jobs) from the counter; each retires after
     // max_pulls tasks, and the grid is sized for ~kWaves waves of resident
     // blocks, so blocks turn over during a launch: kernels on other streams
@@ -340,7 +373,7 @@ void launch_one(const LevArgs& a, int sm_count, cudaStream_t st) {
     const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(want, resident * kWaves));
     LevArgs b = a;
     b.max_pulls = (uint32_t)((tasks + grid * 8 - 1) / (grid * 8));
-    lev_kernel<NP, W><<<(unsigned)grid, 256, smem, st>>>(b);
+    lev_kernel<NP, W, LONG><<<(unsigned)grid, 256, smem, st>>>(b);
 }
 
 template <int NP, int W>
@@ -363,6 +396,65 @@ void warm_np() {
         DM_CUDA(cudaFuncGetAttributes(&fa, lev_kernel<NP, W>));
         warm_np<NP, W + 1>();
     }
+}
+
+// prefix offsets of the per-column delta buffers of the long jobs, and the
+// longest pattern (passes needed): cnt slots + total + max pattern
+__global__ void long_prep_kernel(const LevItem* __restrict__ items, uint32_t cnt, const uint32_t* __restrict__ len,
+                                 unsigned long long* __restrict__ hoff) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cnt) return;
+    const unsigned long long n = len[items[i].txt];
+    hoff[i] = atomicAdd(&hoff[cnt], (n + 15ull) & ~15ull);
+    atomicMax(&hoff[cnt + 1], (unsigned long long)len[items[i].pat]);
+}
+
+template <int NP>
+void run_long_np(dm_ctx* ctx, const LevItem* items, uint32_t cnt, const dm_seqset* s, uint32_t* d_out,
+                 cudaStream_t st) {
+    constexpr int W = WMax<NP>::value;
+    constexpr uint64_t kPassRows = 32ull * W * 32ull;
+    uint64_t* hoff = ctx->lev_long_off.as<uint64_t>((uint64_t)cnt + 2 + 64);
+    DM_CUDA(cudaMemsetAsync(hoff + cnt, 0, 2 * sizeof(uint64_t), st));
+    long_prep_kernel<<<(cnt + 255) / 256, 256, 0, st>>>(items, cnt, s->d_len, (unsigned long long*)hoff);
+    DM_CUDA(cudaGetLastError());
+    uint64_t* h = ctx->pin_long.as<uint64_t>(2);
+    DM_CUDA(cudaMemcpyAsync(h, hoff + cnt, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    DM_CUDA(cudaStreamSynchronize(st));  // rare path: size the delta buffers
+    const uint64_t total = h[0], maxm = h[1];
+    const uint32_t passes = (uint32_t)((maxm + kPassRows - 1) / kPassRows);
+    uint8_t* hbuf = ctx->lev_long_h.as<uint8_t>(total + 16);
+    uint32_t* counters = reinterpret_cast<uint32_t*>(hoff + cnt + 2);
+    if (passes > 128) throw invalid_argument("sequence too long for the distance engine");
+    DM_CUDA(cudaMemsetAsync(counters, 0, passes * sizeof(uint32_t), st));
+    LevArgs a{};
+    a.items = items;
+    a.nitems = cnt;
+    a.lgG = 5;
+    a.codes = s->d_codes;
+    a.off = s->d_off;
+    a.len = s->d_len;
+    a.blk = s->d_blk;
+    a.planes = s->d_planes;
+    a.out = d_out;
+    a.one = 1u;
+    a.hbuf = hbuf;
+    a.hoff = hoff;
+    for (uint32_t p = 0; p < passes; ++p) {  // stream-ordered: pass p reads what pass p - 1 wrote
+        a.pass = p;
+        a.counter = counters + p;
+        launch_one<NP, W, true>(a, ctx->sm_count, st);
+        DM_CUDA(cudaGetLastError());
+    }
+    ctx->launches += passes + 1;
+}
+
+// Patterns longer than 32 lanes x WMax words: multi-pass (LONG kernels).
+void run_long(dm_ctx* ctx, const LevItem* items, uint32_t cnt, const dm_seqset* s, uint32_t* d_out,
+              cudaStream_t st) {
+    if (s->planes == 2) run_long_np<2>(ctx, items, cnt, s, d_out, st);
+    else if (s->planes == 5) run_long_np<5>(ctx, items, cnt, s, d_out, st);
+    else run_long_np<8>(ctx, items, cnt, s, d_out, st);
 }
 
 void launch_bucket(int np, int w, const LevArgs& a, int sm, cudaStream_t st) {
@@ -390,7 +482,8 @@ __global__ void plan_kernel(const uint32_t* __restrict__ ia, const uint32_t* __r
     unsigned long long c0 = 0, c1 = 0;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        uint32_t x, y, slot;
+        uint32_t x, y;
+        uint64_t slot;
         if (in_items) {
             x = in_items[i].pat;
             y = in_items[i].txt;
@@ -398,7 +491,7 @@ __global__ void plan_kernel(const uint32_t* __restrict__ ia, const uint32_t* __r
         } else {
             x = ia[i];
             y = ib[i];
-            slot = (uint32_t)i;
+            slot = i;
         }
         uint32_t lx = len[x], ly = len[y];
         if (lx > ly) {  // pattern = shorter
@@ -411,13 +504,18 @@ __global__ void plan_kernel(const uint32_t* __restrict__ ia, const uint32_t* __r
         uint32_t R = (B + (1u << lg) - 1) >> lg;  // words per lane
         if (R < 1) R = 1;
         uint32_t bucket = (uint32_t)lg * 32 + R;
-        if (R > (uint32_t)wmax) bucket = kBuckets - 1;  // too long: flagged below
+        unsigned long long rows = (unsigned long long)(R << lg) * 32ull;
+        if (R > (uint32_t)wmax) {  // longer than one warp's rows: the multi-pass bucket
+            bucket = kBuckets - 1;
+            const unsigned long long pr = 1024ull * (unsigned)wmax;
+            rows = (lx + pr - 1) / pr * pr;
+        }
         items[i] = LevItem{x, y, slot};
         keys[i] = ((uint64_t)bucket << 32) | (uint64_t)(0xffffffffu - ly);
         idx[i] = (uint32_t)i;
         atomicAdd(&sh[bucket], 1u);
         c0 += (unsigned long long)lx * ly;
-        c1 += (unsigned long long)(R << lg) * 32ull * ly;
+        c1 += rows * ly;
     }
     atomicAdd(&scells[0], c0);
     atomicAdd(&scells[1], c1);
@@ -464,10 +562,12 @@ void plan_hist_host(const uint64_t* offs, uint64_t n, int lg_gpar, int wsel, int
         const uint32_t B = (lx + 31) >> 5;
         const int lg = lgof[std::min(B, bmax + 1)];
         const uint32_t R = std::max((B + (1u << lg) - 1) >> lg, 1u);
-        const uint32_t bucket = R > (uint32_t)wmax ? kBuckets - 1 : (uint32_t)lg * 32 + R;
+        const bool lng = R > (uint32_t)wmax;
+        const uint32_t bucket = lng ? kBuckets - 1 : (uint32_t)lg * 32 + R;
         ++h[(i & 3) * kBuckets + bucket];
         c0 += (unsigned long long)lx * ly;
-        c1 += (unsigned long long)(R << lg) * 32ull * ly;
+        const unsigned long long pr = 1024ull * (unsigned)wmax;
+        c1 += (lng ? (lx + pr - 1) / pr * pr : (unsigned long long)(R << lg) * 32ull) * ly;
     }
     for (int k = 0; k < kBuckets; ++k) P.h[k] = h[k] + h[kBuckets + k] + h[2 * kBuckets + k] + h[3 * kBuckets + k];
     P.hc[0] = c0;
@@ -494,6 +594,10 @@ void plan_batch(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const uin
     const uint64_t target = (uint64_t)ctx->sm_count * 512;  // lanes wanted in flight
     int lg_gpar = 0;
     while (lg_gpar < 5 && (n << lg_gpar) < target) ++lg_gpar;
+    if (const char* e = std::getenv("DM_LEV_GPAR")) {  // test knob: force the minimum lanes per pair (log2)
+        const int v = std::atoi(e);
+        if (v >= 0 && v <= 5) lg_gpar = v;
+    }
 
     // scratch: items(2x), keys(2x), idx(2x), hist, cells, counters, cub temp
     const size_t item_b = n * sizeof(LevItem), key_b = n * 8, idx_b = n * 4;
@@ -531,9 +635,6 @@ void plan_batch(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const uin
         DM_CUDA(cudaMemcpyAsync(P.hc, cells, sizeof(P.hc), cudaMemcpyDeviceToHost, st));
         DM_CUDA(cudaStreamSynchronize(st));
     }
-    if (P.h[kBuckets - 1])
-        throw invalid_argument("sequence too long for the distance engine (max " +
-                               std::to_string(32 * wmax * 32) + " residues for this alphabet)");
     P.items = it1;
     P.counters = counters;
     ctx->launches += 2;
@@ -555,6 +656,9 @@ int launch_plan(dm_ctx* ctx, const LevPlan& P, const dm_seqset* s, uint32_t* d_o
         start += P.h[b];
         if (P.h[b]) order[nb++] = b;
     }
+    // the multi-pass bucket (largest work per job) is first in `order`:
+    // it goes to the first side stream and syncs that stream once to size
+    // its buffers (run_long)
     // largest per-task work first: lanes per pair x words per lane
     std::stable_sort(order, order + nb, [](int x, int y) { return ((x % 32) << (x / 32)) > ((y % 32) << (y / 32)); });
     const bool fork = nb > 1 || after != nullptr;
@@ -582,7 +686,11 @@ int launch_plan(dm_ctx* ctx, const LevPlan& P, const dm_seqset* s, uint32_t* d_o
     }
     for (int i = 0; i < nb; ++i) {
         const int b = order[i];
-        LevArgs a;
+        if (b == kBuckets - 1) {
+            run_long(ctx, P.items + starts[b], P.h[b], s, d_out, fork ? ctx->lev_side[used[i % nused]] : st);
+            continue;
+        }
+        LevArgs a{};
         a.items = P.items + starts[b];
         a.nitems = P.h[b];
         a.lgG = b / 32;
@@ -683,7 +791,7 @@ void lev_run_host_items(dm_ctx* ctx, const dm_seqset* s, std::vector<LevItem>& i
         shard_range(n, r, w, &lo, &hi);
         if (hi == lo) continue;
         sub.assign(items.begin() + lo, items.begin() + hi);
-        for (uint64_t k = 0; k < sub.size(); ++k) sub[k].slot = (uint32_t)k;
+        for (uint64_t k = 0; k < sub.size(); ++k) sub[k].slot = k;
         LevItem* d_items = ctx->aux3.as<LevItem>(sub.size());
         DM_CUDA(cudaMemcpyAsync(d_items, sub.data(), sub.size() * sizeof(LevItem), cudaMemcpyHostToDevice,
                                 ctx->stream));

@@ -131,13 +131,7 @@ __global__ void __launch_bounds__(128) nw_traceback_kernel(const TbArgs a) {
 // such launches get a per-CTA global row for the round-to-round hand-off.
 template <class V, int NWW>
 void launch_fwd(dm_ctx* ctx, const nwk::FwdArgs& fa, size_t smem, uint32_t wrap_m) {
-    static int occ = -1;
-    if (occ < 0) {
-        DM_CUDA(cudaFuncSetAttribute(nwk::nw_fwd_kernel<V, NWW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     48 * 1024));
-        DM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nwk::nw_fwd_kernel<V, NWW>, NWW * 32, smem));
-        occ = std::max(occ, 1);
-    }
+    const int occ = occupancy((const void*)nwk::nw_fwd_kernel<V, NWW>, NWW * 32, smem);
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(fa.njobs, (uint64_t)occ * ctx->sm_count));
     nwk::FwdArgs f = fa;
     if (NWW > 1 && wrap_m) {

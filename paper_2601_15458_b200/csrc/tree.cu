@@ -422,7 +422,7 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
             const uint32_t* c = cand.data() + cand_off[v];
             for (uint32_t i = 0; i < k; ++i)
                 for (uint32_t j = i + 1; j < k; ++j)
-                    items.push_back(LevItem{c[i], c[j], (uint32_t)(mtot + (uint64_t)i * k + j)});
+                    items.push_back(LevItem{c[i], c[j], mtot + (uint64_t)i * k + j});
             mtot += (uint64_t)k * k;
         }
         uint32_t* d_mat = sc.mat.as<uint32_t>(mtot);
@@ -523,7 +523,7 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
             const uint32_t* mem = order.data() + nd.begin;
             for (uint32_t i = 0; i < k; ++i)
                 for (uint32_t j = i + 1; j < k; ++j)
-                    items.push_back(LevItem{mem[i], mem[j], (uint32_t)(mtot + (uint64_t)i * k + j)});
+                    items.push_back(LevItem{mem[i], mem[j], mtot + (uint64_t)i * k + j});
             mtot += (uint64_t)k * k;
             rtot += 2ull * k - 1;
         }
@@ -637,7 +637,7 @@ uint32_t geometric_median(dm_ctx* ctx, const dm_seqset* s, const uint32_t* membe
     const uint32_t k = (uint32_t)cand.size();
     std::vector<LevItem> items;
     for (uint32_t i = 0; i < k; ++i)
-        for (uint32_t j = i + 1; j < k; ++j) items.push_back(LevItem{cand[i], cand[j], i * k + j});
+        for (uint32_t j = i + 1; j < k; ++j) items.push_back(LevItem{cand[i], cand[j], (uint64_t)i * k + j});
     uint32_t* d = ctx->out.as<uint32_t>((size_t)k * k);
     lev_run_host_items(ctx, s, items, d, nullptr, false);
     std::vector<uint32_t> mat((size_t)k * k);

@@ -88,7 +88,11 @@ def main():
     args = ap.parse_args()
     ref = oracle.reference()
     if args.only:
-        return big_configs(ref, [k for k in args.only.split(",") if k])
+        keys = [k for k in args.only.split(",") if k]
+        if "cfg1@1.0" in keys:
+            keys.remove("cfg1@1.0")
+            cfg1_distances(ref)
+        return big_configs(ref, keys) if keys else None
 
     lev = [[a, b, ref.levenshtein(a, b)] for a, b in lev_cases()]
     with open(os.path.join(HERE, "lev.json"), "w") as f:
@@ -121,6 +125,33 @@ def main():
 
     if args.big:
         big_configs(ref, ["cfg0@1.0", "cfg3@1.0", "cfg2@0.1", "cfg2@1.0"])
+
+
+def cfg1_distances(ref):
+    """BASELINE configs[1] pinned in full: the reference's levenshtein
+    (distance.cpp:9-48) over all 10^6 synth(1) pairs (2i, 2i+1), stored as the
+    SHA-256 of the little-endian uint32 vector, one SHA per 65,536-pair block
+    (to localise a mismatch), the sum and a histogram."""
+    import paper_2601_15458_b200 as dm
+    data, offs = dm.synth(1)
+    seqs = dm.split(data, offs)
+    n = len(seqs) // 2
+    ia = np.arange(n, dtype=np.uint32) * 2
+    t0 = time.time()
+    d = ref.lev_pairs(seqs, ia, ia + 1, threads=os.cpu_count())
+    wall = time.time() - t0
+    d = np.ascontiguousarray(d, dtype="<u4")
+    blk = 65536
+    hist, edges = np.histogram(d, bins=64, range=(0, 1600))
+    out = dict(cfg=1, pairs=int(n), sha256=hashlib.sha256(d.tobytes()).hexdigest(),
+               block=blk, block_sha256=[hashlib.sha256(d[i:i + blk].tobytes()).hexdigest() for i in range(0, n, blk)],
+               sum=int(d.astype(np.uint64).sum()), min=int(d.min()), max=int(d.max()),
+               hist_range=[0, 1600], hist=hist.tolist(), first16=d[:16].tolist(),
+               threads=os.cpu_count(), wall_s=wall,
+               cells=int(sum((int(offs[2 * i + 1] - offs[2 * i]) * int(offs[2 * i + 2] - offs[2 * i + 1])) for i in range(n))))
+    with open(os.path.join(HERE, "lev_cfg1.json"), "w") as f:
+        json.dump(out, f, indent=1)
+    print("cfg1", {k: v for k, v in out.items() if k not in ("block_sha256", "hist")}, flush=True)
 
 
 def big_configs(ref, keys):

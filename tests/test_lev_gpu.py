@@ -113,24 +113,91 @@ def test_batch_sizes_and_grouping(dm, ctx, orc):
         assert list(got) == [want[p] for p in pairs]
 
 
-def test_cfg1_full_properties(dm, ctx, orc):
-    """Full cfg1 batch (10^6 pairs): size-independent checks plus a sampled oracle."""
+def _cfg1_golden():
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "lev_cfg1.json")) as f:
+        return json.load(f)
+
+
+def _sha(d):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(d, dtype="<u4").tobytes()).hexdigest()
+
+
+def _first_bad_block(d, g):
+    import hashlib
+    blk = g["block"]
+    for k, h in enumerate(g["block_sha256"]):
+        if hashlib.sha256(np.ascontiguousarray(d[k * blk:(k + 1) * blk], dtype="<u4").tobytes()).hexdigest() != h:
+            return k
+    return None
+
+
+@pytest.fixture(scope="module")
+def cfg1(dm):
     data, offs = dm.synth(1, scale=1.0)
+    return data, offs
+
+
+def test_cfg1_full_pinned_to_reference(dm, ctx, cfg1):
+    """All 10^6 cfg1 pairs == the compiled reference's levenshtein
+    (distance.cpp:9-48), by SHA-256 of the uint32 vector (tests/golden/
+    lev_cfg1.json, made by make_golden.py --only cfg1@1.0 from oracle/_ref),
+    device-resident, in both orientations."""
+    g = _cfg1_golden()
+    data, offs = cfg1
     ss = dm.SeqSet(data=data, offsets=offs, ctx=ctx)
     n = (len(offs) - 1) // 2
+    assert n == g["pairs"]
     ia = np.arange(n, dtype=np.uint32) * 2
     ib = ia + 1
     d = dm.lev_pairs(ss, ia, ib)
-    d2 = dm.lev_pairs(ss, ib, ia)
-    assert np.array_equal(d, d2)  # symmetry through a different orientation path
-    lens = np.diff(offs).astype(np.int64)
-    la, lb = lens[ia], lens[ib]
-    assert (d >= np.abs(la - lb)).all() and (d <= np.maximum(la, lb)).all()
-    rng = np.random.default_rng(3)
-    for i in rng.choice(n, 200, replace=False):
-        a = data[offs[2 * i]:offs[2 * i + 1]]
-        b = data[offs[2 * i + 1]:offs[2 * i + 2]]
-        assert d[i] == orc.levenshtein(a, b)
+    assert d[:16].tolist() == g["first16"]
+    assert _sha(d) == g["sha256"], f"first differing 65,536-pair block: {_first_bad_block(d, g)}"
+    assert int(d.astype(np.uint64).sum()) == g["sum"]
+    assert _sha(dm.lev_pairs(ss, ib, ia)) == g["sha256"]
+
+
+@pytest.mark.parametrize("mode", ["pageable", "pinned-frac0", "pinned-frac0.3", "pinned-frac1", "nopack"])
+def test_cfg1_full_streamed_pinned_to_reference(dm, ctx, cfg1, monkeypatch, mode):
+    """The same 10^6 pairs from host memory through dm_lev_pairs_packed:
+    pageable and pinned buffers, every speculative raw share, packing off."""
+    g = _cfg1_golden()
+    data, offs = cfg1
+    if mode.startswith("pinned"):
+        import torch
+        buf = torch.frombuffer(bytearray(data), dtype=torch.uint8).pin_memory()
+        monkeypatch.setenv("DM_STREAM_RAW_FRAC", mode.split("frac")[1])
+    else:
+        buf = data
+        if mode == "nopack":
+            monkeypatch.setenv("DM_STREAM_PACK", "0")
+    d = dm.lev_pairs_packed(buf, offs, ctx)
+    assert _sha(d) == g["sha256"], f"first differing 65,536-pair block: {_first_bad_block(d, g)}"
+
+
+@pytest.mark.parametrize("alphabet", ["ACGT", "ARNDCQEGHILKMFPSTWYV", "".join(chr(c) for c in range(33, 127))])
+@pytest.mark.parametrize("gpar", ["0", "1", "3"])
+def test_every_bucket_forced_lanes(dm, ctx, ref, monkeypatch, alphabet, gpar):
+    """Small batches normally widen groups to 32 lanes; DM_LEV_GPAR forces
+    the minimum lanes per pair so every (G, W) kernel runs: patterns of
+    1..48 words (W = 17..24 kernels for <= 4 symbols, 6..10 for 5 planes)."""
+    monkeypatch.setenv("DM_LEV_GPAR", gpar)
+    rng = random.Random(len(alphabet) * 7 + int(gpar))
+    seqs, ia, ib = [], [], []
+    for B in list(range(1, 25)) + list(range(33, 49)) + [64, 96, 128, 192, 256, 384, 768]:
+        for delta in (-17, 0):
+            la = max(1, 32 * B + delta)
+            a = rand_str(rng, la, alphabet)
+            b = list(a)
+            for _ in range(max(1, la // 15)):
+                b[rng.randrange(len(b))] = rng.choice(alphabet)
+            b = "".join(b[:max(1, la - rng.randint(0, 40))]) + rand_str(rng, rng.randint(0, 40), alphabet)
+            ia.append(len(seqs)); seqs.append(a)
+            ib.append(len(seqs)); seqs.append(b)
+    ss = dm.SeqSet(seqs, ctx)
+    assert np.array_equal(dm.lev_pairs(ss, ia, ib), ref.lev_pairs(seqs, ia, ib))
 
 
 def test_packed_streaming_matches(dm, ctx, orc, monkeypatch):
