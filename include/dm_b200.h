@@ -195,6 +195,20 @@ int dm_insert_gap_columns(dm_ctx* ctx, const char* rows, uint64_t nrows, uint64_
 int dm_align_all(dm_ctx* ctx, const dm_seqset* s, const dm_node* nodes, uint64_t nnodes,
                  const uint32_t* order, const int16_t* table, const uint8_t* has_symbol,
                  int open_surcharge, int gap_extend, dm_msa_out** out, dm_stats* st);
+/* Progress callback of align_all (ProgressFn, msa_merge.hpp:43-49): called
+ * once per tree node as it completes, done = 1..nnodes, on the calling
+ * thread (leaves first, then each merge level's nodes once that level's
+ * alignments are known). */
+typedef void (*dm_progress_fn)(uint64_t done, uint64_t total, void* user);
+int dm_align_all_progress(dm_ctx* ctx, const dm_seqset* s, const dm_node* nodes, uint64_t nnodes,
+                          const uint32_t* order, const int16_t* table, const uint8_t* has_symbol,
+                          int open_surcharge, int gap_extend, dm_progress_fn progress, void* user,
+                          dm_msa_out** out, dm_stats* st);
+/* dump_tree (cluster_tree.hpp:70-72) into memory: the NDJSON text of the
+ * tree (one record per node, nlohmann key order), *text malloc'd (dm_free).
+ * ids: node centers' names, ids + id_off[k] .. id_off[k+1]. */
+int dm_format_tree(const dm_node* nodes, uint64_t nnodes, const char* ids, const uint64_t* id_off, uint64_t nids,
+                   char** text, uint64_t* len);
 /* build_tree + align_all, device-resident between the two. */
 int dm_msa(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_cap,
            const int16_t* table, const uint8_t* has_symbol, int open_surcharge,

@@ -220,9 +220,9 @@ int dm_insert_gap_columns(dm_ctx* ctx, const char* rows, uint64_t nrows, uint64_
     });
 }
 
-int dm_align_all(dm_ctx* ctx, const dm_seqset* s, const dm_node* nodes, uint64_t nnodes, const uint32_t* order,
-                 const int16_t* table, const uint8_t* has_symbol, int open_surcharge, int gap_extend,
-                 dm_msa_out** out, dm_stats* st) {
+int dm_align_all_progress(dm_ctx* ctx, const dm_seqset* s, const dm_node* nodes, uint64_t nnodes,
+                          const uint32_t* order, const int16_t* table, const uint8_t* has_symbol, int open_surcharge,
+                          int gap_extend, dm_progress_fn progress, void* user, dm_msa_out** out, dm_stats* st) {
     return guard(ctx, [&] {
         if (!ctx || !s || !nodes || !order || !table || !has_symbol || !out) throw dm::invalid_argument("null argument");
         const dm::NwScheme sc = dm::make_scheme(table, has_symbol, open_surcharge, gap_extend);
@@ -234,7 +234,7 @@ int dm_align_all(dm_ctx* ctx, const dm_seqset* s, const dm_node* nodes, uint64_t
         DM_CUDA(cudaEventCreate(&t0));
         DM_CUDA(cudaEventCreate(&t1));
         DM_CUDA(cudaEventRecord(t0, ctx->stream));
-        dm_msa_out* m = dm::align_all(ctx, s, nv, ov, sc, st);
+        dm_msa_out* m = dm::align_all(ctx, s, nv, ov, sc, st, progress, user);
         DM_CUDA(cudaEventRecord(t1, ctx->stream));
         DM_CUDA(cudaEventSynchronize(t1));
         float ms = 0;
@@ -247,6 +247,13 @@ int dm_align_all(dm_ctx* ctx, const dm_seqset* s, const dm_node* nodes, uint64_t
         }
         *out = m;
     });
+}
+
+int dm_align_all(dm_ctx* ctx, const dm_seqset* s, const dm_node* nodes, uint64_t nnodes, const uint32_t* order,
+                 const int16_t* table, const uint8_t* has_symbol, int open_surcharge, int gap_extend,
+                 dm_msa_out** out, dm_stats* st) {
+    return dm_align_all_progress(ctx, s, nodes, nnodes, order, table, has_symbol, open_surcharge, gap_extend,
+                                 nullptr, nullptr, out, st);
 }
 
 int dm_msa(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_cap, const int16_t* table,

@@ -272,8 +272,12 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
 double int32_peak(dm_ctx* ctx, int mode);
 void lev_warm();
 void nw_warm();
+// progress (optional): called once per node as it completes (leaves when the
+// rows are initialised, each merge when its level's results are known), as
+// align_all's ProgressFn (msa_merge.cpp:121-129): done = 1..nodes.size().
 dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node>& nodes,
-                      const std::vector<uint32_t>& order, const NwScheme& sc, dm_stats* st);
+                      const std::vector<uint32_t>& order, const NwScheme& sc, dm_stats* st,
+                      dm_progress_fn progress = nullptr, void* progress_user = nullptr);
 void insert_gap_columns(dm_ctx* ctx, const char* rows, uint64_t nrows, uint64_t width, const uint32_t* pos,
                         uint64_t npos, char* out);
 uint32_t geometric_median(dm_ctx* ctx, const dm_seqset* s, const uint32_t* members, uint64_t n,

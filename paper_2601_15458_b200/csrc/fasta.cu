@@ -311,6 +311,24 @@ int dm_run_align(dm_ctx* ctx, const char* input_path, const char* output_path, i
     });
 }
 
+int dm_format_tree(const dm_node* nodes, uint64_t nnodes, const char* ids, const uint64_t* id_off, uint64_t nids,
+                   char** text, uint64_t* len) {
+    return dm::guard([&] {
+        dm::require(nodes && id_off && text && len, "null argument");
+        std::vector<std::string> v(nids);
+        for (uint64_t k = 0; k < nids; ++k) v[k] = std::string(ids + id_off[k], id_off[k + 1] - id_off[k]);
+        for (uint64_t i = 0; i < nnodes; ++i)
+            if (nodes[i].center >= nids) throw dm::invalid_argument("node center outside the id list");
+        const std::string t = dm::tree_ndjson(nodes, nnodes, v);
+        char* p = static_cast<char*>(std::malloc(t.size() + 1));
+        if (!p) throw std::bad_alloc();
+        std::memcpy(p, t.data(), t.size());
+        p[t.size()] = 0;
+        *text = p;
+        *len = t.size();
+    });
+}
+
 int dm_dump_tree(const dm_node* nodes, uint64_t nnodes, const char* ids, const uint64_t* id_off, uint64_t nids,
                  const char* path) {
     return dm::guard([&] {

@@ -144,7 +144,8 @@ void apply_sides(dm_ctx* ctx, std::vector<SideDesc>& sides, const uint32_t* d_ga
 }  // namespace
 
 dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node>& nodes,
-                      const std::vector<uint32_t>& order, const NwScheme& sc, dm_stats* st) {
+                      const std::vector<uint32_t>& order, const NwScheme& sc, dm_stats* st,
+                      dm_progress_fn progress, void* progress_user) {
     const uint32_t n = s->n;
     if (order.size() != n) throw invalid_argument("tree order does not match the sequence set");
     if (nodes.empty()) throw invalid_argument("empty tree");
@@ -186,6 +187,11 @@ dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node
             ctx->launches += 1;
         }
         const bool trace = std::getenv("DM_TRACE") != nullptr;
+        uint64_t done = 0;
+        const uint64_t total = nodes.size();
+        if (progress)
+            for (const dm_node& nd : nodes)
+                if (nd.left < 0) progress(++done, total, progress_user);
         float fwd_ms = 0, tb_ms = 0;
         uint64_t cells = 0, nw_calls = 0, launches = 0;
         for (int d = (int)by_depth.size() - 1; d >= 0; --d) {
@@ -233,6 +239,8 @@ dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node
                     sides.push_back(SideDesc{rc.begin, rc.end, (uint32_t)W[nd.right], (uint32_t)w, 0,
                                              jobs[k].gb_off, res[k].ngb, 0});
             }
+            if (progress)
+                for (size_t k = 0; k < lvl.size(); ++k) progress(++done, total, progress_user);
             if (trace) DM_CUDA(cudaEventRecord(ctx->ev0, stream));
             grow_rows(ctx, rowsbuf, pitch, n, wmax);
             apply_sides(ctx, sides, no.d_gaps, (uint8_t*)rowsbuf.p, pitch, wold);
