@@ -22,12 +22,29 @@ A step = one pass of the distance engine over the whole pair batch.
          traceback), bit-checked against the C restatement on a sample;
          roofline c_nw = 13 INT32 ops/cell.
 
+  msa    the second half of BASELINE's metric: end-to-end MSA wall time of
+         cfg2 (10^4 x ~1,500 nt) and cfg4 (10^5 x ~1,500 nt, 50 clades)
+         through dm_align_sequences (the reference's align_sequences,
+         pipeline.cpp:78-159: host residues in, de-dup, guide tree, merges,
+         host rows out), tree / align split, cells, and the rows' SHA-256
+         asserted against the reference's output (tests/golden/
+         msa_configs.json); the reference CPU times quoted there come from
+         that golden file (oracle/_ref run in the build container).
+
+The timed cfg1 distances are asserted bit-exact against the reference's full
+10^6-pair output (SHA-256, tests/golden/lev_cfg1.json).
+
 --impl reference times the compiled reference (oracle/_ref, the unmodified
 divmsa C++ sources) on the box's host cores: divmsa::parallel_for +
-divmsa::levenshtein over a bounded sample of the same pairs per step.
+divmsa::levenshtein over a bounded sample of the same pairs per step. It
+loads only oracle/ libraries (inputs from oracle/_build/libsynth.so, the same
+generator compiled apart from the product).
 
-Multi-GPU (torchrun): pairs are independent, so each rank owns its own batch
-(weak scaling, no data-path collective); barrier + max-over-ranks timing.
+Multi-GPU (torchrun): every rank runs the same cfg1 batch independently
+(weak scaling, no data-path collective; barrier + max-over-ranks timing).
+The msa key is then strong-scaled: cfg4 (and cfg2) sharded across the ranks
+inside libdmb200 (NCCL all-gather of distance shards and merge results),
+every rank's rows checked against the reference's SHA.
 """
 from __future__ import annotations
 
@@ -127,6 +144,79 @@ def load_peaks():
         with open(p) as f:
             return json.load(f)
     return {}
+
+
+def golden(name):
+    p = os.path.join(ROOT, "tests", "golden", name)
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+def sha_u32(d):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(d, dtype="<u4").tobytes()).hexdigest()
+
+
+def msa_bench(dm, ctx, cfgs, reps, world, rank):
+    """End-to-end MSA through the reference-facing pipeline call
+    (dm_align_sequences = align_sequences, pipeline.cpp:78-159): host residue
+    buffer in, host row buffer out; best of `reps` wall times (the first call
+    also warms the context's buffers), max over ranks."""
+    import ctypes as C
+    import hashlib
+    from paper_2601_15458_b200._lib import check, dm_align_summary, lib
+    gold = golden("msa_configs.json")
+    res = {}
+    for cfg, scale in cfgs:
+        data, offs = dm.synth(cfg, scale)
+        n = len(offs) - 1
+        offs_c = np.ascontiguousarray(offs, dtype=np.uint64)
+        best = None
+        for _ in range(reps):
+            rows = C.c_void_p()
+            width = C.c_uint64()
+            summ = dm_align_summary()
+            st = dm.dm_stats()
+            if world > 1:
+                import torch.distributed as tdist
+                tdist.barrier()
+            t0 = time.perf_counter()
+            check(lib().dm_align_sequences(ctx.handle, data, offs_c.ctypes.data_as(C.POINTER(C.c_uint64)), n,
+                                           1 if cfg != 3 else 2, -10, -1, 0, None, None, 42, 0, C.byref(rows),
+                                           C.byref(width), C.byref(summ), C.byref(st)))
+            wall = time.perf_counter() - t0
+            if world > 1:
+                import torch
+                t = torch.tensor([wall], dtype=torch.float64, device="cuda")
+                torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+                wall = float(t[0])
+            W = width.value
+            buf = np.ctypeslib.as_array(C.cast(rows, C.POINTER(C.c_uint8)), shape=(max(1, n * W),))[:n * W]
+            flat = np.concatenate([buf.reshape(n, W), np.full((n, 1), 10, np.uint8)], axis=1)
+            digest = hashlib.sha256(flat.tobytes()).hexdigest()
+            lib().dm_free(rows)
+            if best is None or wall < best["wall_s"]:
+                best = {"wall_s": wall, "tree_ms": st.tree_ms, "align_ms": st.align_ms, "cells": int(st.cells),
+                        "width": W, "sha": digest, "launches": int(st.launches)}
+        key = f"cfg{cfg}@{scale}"
+        g = gold.get(key)
+        match = None if g is None else best["sha"] == g["rows_sha256"]
+        if match is False:
+            raise SystemExit(f"bench: {key} MSA rows differ from the reference's (rank {rank})")
+        entry = {"n": n, "width": best["width"], "wall_s": best["wall_s"], "tree_ms": best["tree_ms"],
+                 "align_ms": best["align_ms"], "cells": best["cells"],
+                 "gcups_e2e": best["cells"] / best["wall_s"] / 1e9, "gpu_launches": best["launches"],
+                 "n_gpus": world, "rows_sha256_matches_reference": match}
+        if g is not None:
+            entry["reference_cpu"] = {"wall_s": g["tree_s"] + g["align_s"], "tree_s": g["tree_s"],
+                                      "align_s": g["align_s"], "threads": g["threads"],
+                                      "source": "tests/golden/msa_configs.json (oracle/_ref align_all, build "
+                                                "container, not this box)"}
+            entry["speedup_vs_reference_cpu"] = entry["reference_cpu"]["wall_s"] / best["wall_s"]
+        res[key] = entry
+    return res
 
 
 def cpu_baseline(data, offs, n_pairs, budget_s=12.0, threads=None):
@@ -234,13 +324,16 @@ def nw_micro(dm, ctx, data, offs, p_int32, npairs=65536, reps=3, cpu=True):
     return res
 
 
+WORKLOAD = ("cfg1: 1e6 DNA pairs/GPU, L~U[500,1500], 5% sub + 1% indel "
+            "(batched Levenshtein, BASELINE.json configs[1])")
+
+
 def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
         return 0
-    import paper_2601_15458_b200 as dm  # only for the synthetic generator (host code)
-    data, offs = dm.synth(1, scale=args.scale)
-    import oracle
+    import oracle  # test infrastructure only: the compiled reference + the input generator
+    data, offs = oracle.synth(1, scale=args.scale)
     ref = oracle.reference()
     threads = os.cpu_count() or 1
     seqs = [data[int(offs[i]):int(offs[i + 1])] for i in range(len(offs) - 1)]
@@ -255,17 +348,22 @@ def run_reference(args):
         ref.lev_pairs(seqs, ia[:max(1, k // 8)], ib[:max(1, k // 8)], threads=threads)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        ref.lev_pairs(seqs, ia, ib, threads=threads)
+        d = ref.lev_pairs(seqs, ia, ib, threads=threads)
     dt = time.perf_counter() - t0
     v = cells * args.steps / dt / 1e9
+    sample = (f"bounded CPU sample: the first {k} of the {n_pairs} cfg1 pairs per step ({cells:.3e} cells), "
+              f"divmsa::parallel_for(grain 64) + divmsa::levenshtein on {threads} host threads")
     line = {"metric": "levenshtein_gcups", "value": v, "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": "cfg1: 1e6 DNA pairs, L~U[500,1500], 5% sub + 1% indel (batched Levenshtein)",
-                       "pairs_per_step": k, "scale": args.scale},
-            "cpu_baseline": {"value": v, "unit": "GCUPS", "cores": threads, "kind": "reference",
-                             "sample": f"first {k} cfg1 pairs per step ({cells:.3e} cells)"},
+            "config": {"workload": WORKLOAD, "pairs_per_gpu": n_pairs,
+                       "cells_per_step_per_gpu": int(np.sum(lens[0::2] * lens[1::2])),
+                       "l2": "inputs (%.1f GB/GPU) larger than L2" % (len(data) / 1e9),
+                       "parallelism": "host threads (reference CPU build)"},
+            "sample": sample, "pairs_timed_per_step": k,
+            "sample_first16": [int(x) for x in d[:16]],
+            "cpu_baseline": {"value": v, "unit": "GCUPS", "cores": threads, "kind": "reference", "sample": sample},
             "e2e": {"value": v, "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -283,6 +381,8 @@ def main():
     ap.add_argument("--ref-step-s", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nw", action="store_true", help="skip the NW micro-benchmark")
+    ap.add_argument("--msa", default="2,4", help="MSA configs for the msa key (comma list; '' to skip)")
+    ap.add_argument("--msa-reps", type=int, default=2)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -308,7 +408,8 @@ def main():
     stream = torch.cuda.current_stream()
     check(lib().dm_ctx_set_stream(ctx.handle, C.c_void_p(stream.cuda_stream)))
 
-    data, offs = dm.synth(1, scale=args.scale, seed=2601154581 + 1000003 * rank)
+    # every rank runs the same batch (the one pinned by tests/golden/lev_cfg1.json)
+    data, offs = dm.synth(1, scale=args.scale)
     n_pairs = (len(offs) - 1) // 2
     lens = np.diff(offs).astype(np.int64)
     cells_step = int(np.sum(lens[0::2] * lens[1::2]))
@@ -354,16 +455,24 @@ def main():
     value = cells_step * world / (ms_per_step * 1e-3) / 1e9
     kernel_gcups = cells_step / (kern_ms / args.steps * 1e-3) / 1e9
 
-    # parity spot-check of the timed output against the C restatement
-    import oracle
-    orc = oracle.restatement()
+    # parity of the timed output: the reference's full cfg1 output (SHA-256)
     got = out.cpu().numpy().astype(np.uint32)
-    rs = np.random.default_rng(rank)
-    for i in rs.choice(n_pairs, 16, replace=False):
-        a = data[int(offs[2 * i]):int(offs[2 * i + 1])]
-        b = data[int(offs[2 * i + 1]):int(offs[2 * i + 2])]
-        if got[i] != orc.levenshtein(a, b):
-            raise SystemExit(f"bench: distance mismatch at pair {i}")
+    g1 = golden("lev_cfg1.json")
+    parity = {"checked": "none"}
+    if g1 and args.scale == 1.0 and n_pairs == g1["pairs"]:
+        if sha_u32(got) != g1["sha256"]:
+            raise SystemExit("bench: timed cfg1 distances differ from the reference's (SHA-256)")
+        parity = {"checked": "sha256 of all %d timed distances == reference (tests/golden/lev_cfg1.json)" % n_pairs}
+    else:
+        import oracle
+        orc = oracle.restatement()
+        rs = np.random.default_rng(rank)
+        for i in rs.choice(n_pairs, 64, replace=False):
+            a = data[int(offs[2 * i]):int(offs[2 * i + 1])]
+            b = data[int(offs[2 * i + 1]):int(offs[2 * i + 2])]
+            if got[i] != orc.levenshtein(a, b):
+                raise SystemExit(f"bench: distance mismatch at pair {i}")
+        parity = {"checked": "64 sampled pairs == C restatement (scaled run: no full golden)"}
     del ss
 
     # ---- end-to-end through the C ABI with host buffers (e2e) ----------
@@ -400,11 +509,37 @@ def main():
         e2e_s = float(t[0])
     if not np.array_equal(out_h, got):
         raise SystemExit("bench: e2e distances differ from the device-resident run")
+    # the same call from a pageable caller buffer (INTEGRATION.md's example)
+    pest = dm.dm_stats()
+    out_p = np.empty(n_pairs, dtype=np.uint32)
+
+    def e2e_pageable():
+        check(lib().dm_lev_pairs_packed(ctx.handle, data, offs_c.ctypes.data_as(C.POINTER(C.c_uint64)), n_pairs,
+                                        out_p.ctypes.data_as(u32p), C.byref(pest)))
+
+    e2e_pageable()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        e2e_pageable()
+    torch.cuda.synchronize()
+    pg_s = (time.perf_counter() - t0) / args.e2e_steps
+    if world > 1:
+        t = torch.tensor([pg_s], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        pg_s = float(t[0])
+    if not np.array_equal(out_p, got):
+        raise SystemExit("bench: pageable e2e distances differ from the device-resident run")
     e2e = {"value": cells_step * world / e2e_s / 1e9, "unit": "GCUPS",
            "h2d_bytes_per_step": int(est.h2d_bytes), "d2h_bytes_per_step": int(est.d2h_bytes),
            "host_input_bytes_per_step": int(len(data) + offs_c.nbytes),
            "upload": ("~70% of the residue bytes packed to 2 bits/residue by host threads (the upload is the "
-                      "device code buffer), ~30% sent raw by the copy engine and checked on the device")}
+                      "device code buffer), ~30% sent raw by the copy engine and checked on the device"),
+           "caller_buffer": "pinned",
+           "pageable": {"value": cells_step * world / pg_s / 1e9, "unit": "GCUPS",
+                        "h2d_bytes_per_step": int(pest.h2d_bytes), "d2h_bytes_per_step": int(pest.d2h_bytes),
+                        "caller_buffer": "pageable (Python bytes)"}}
 
     # ---- roofline: INT32 lane-op peak measured on this box --------------
     peaks = []
@@ -432,16 +567,22 @@ def main():
     line = {"metric": "levenshtein_gcups", "value": value, "unit": "GCUPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": "cfg1: 1e6 DNA pairs/GPU, L~U[500,1500], 5% sub + 1% indel "
-                                   "(batched Levenshtein, BASELINE.json configs[1])",
-                       "pairs_per_gpu": n_pairs, "cells_per_step_per_gpu": cells_step,
+            "config": {"workload": WORKLOAD, "pairs_per_gpu": n_pairs, "cells_per_step_per_gpu": cells_step,
                        "l2": "inputs (%.1f GB/GPU) larger than L2" % (len(data) / 1e9),
                        "parallelism": f"dp{world} (independent pair batches)"},
-            "gpu_launches": int(launches), "clocks": clk, "e2e": e2e, "roofline": roofline}
+            "gpu_launches": int(launches), "clocks": clk, "e2e": e2e, "roofline": roofline, "parity": parity}
     if nw is not None:
         line["nw"] = nw
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(data, offs, n_pairs, args.cpu_budget_s)
+    if args.msa:
+        del data, offs, pinned
+        if world > 1:  # the MSA job is sharded across the ranks inside libdmb200 (strong scaling)
+            from paper_2601_15458_b200 import dist as dmdist
+            dmdist.attach_from_torch(ctx)
+        cfgs = [(int(c), 1.0) for c in args.msa.split(",") if c]
+        line["msa"] = msa_bench(dm, ctx, cfgs, args.msa_reps, world, rank)
+        line["msa_scaling"] = "strong (one MSA job sharded across the ranks)" if world > 1 else "1 GPU"
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

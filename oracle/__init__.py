@@ -444,6 +444,37 @@ class Reference:
 _cache = {}
 
 
+SYNTH_SO = os.path.join(HERE, "_build", "libsynth.so")
+_synth_lib = None
+
+
+def synth(cfg: int, scale: float = 1.0, seed: int = 0):
+    """The seeded synthetic inputs of BASELINE config `cfg` from
+    oracle/_build/libsynth.so (the generator source compiled on its own), so
+    a CPU-only process gets the same inputs as the product's dm.synth without
+    loading the product library. Returns (data: bytes, offsets: uint64[n+1])."""
+    global _synth_lib
+    if _synth_lib is None:
+        L = C.CDLL(SYNTH_SO)
+        L.dm_synth.restype = C.c_int
+        L.dm_synth.argtypes = [C.c_int, C.c_double, C.c_uint64, C.POINTER(C.c_char_p), C.POINTER(_u64p),
+                               C.POINTER(C.c_uint64)]
+        _synth_lib = L
+    libc = C.CDLL(None)
+    data = C.c_char_p()
+    offs = _u64p()
+    n = C.c_uint64()
+    if _synth_lib.dm_synth(cfg, float(scale), int(seed), C.byref(data), C.byref(offs), C.byref(n)) != 0:
+        raise ValueError("dm_synth failed")
+    try:
+        o = np.ctypeslib.as_array(offs, shape=(n.value + 1,)).copy()
+        buf = C.string_at(data, int(o[-1]))
+    finally:
+        libc.free(C.cast(data, C.c_void_p))
+        libc.free(C.cast(offs, C.c_void_p))
+    return buf, o
+
+
 def restatement() -> Restatement:
     if "r" not in _cache:
         _cache["r"] = Restatement()

@@ -401,15 +401,31 @@ def _msa_from(h) -> Msa:
                nodes_to_array(nodes, nn), order[:R].copy())
 
 
-def align_all(seqset: SeqSet, nodes: np.ndarray, order, scheme: ScoringScheme, stats: bool = False) -> Msa:
-    """divmsa::align_all (msa_merge.hpp:47-49) on the GPU: per-level merge scheduler."""
+def align_all(seqset: SeqSet, nodes: np.ndarray, order, scheme: ScoringScheme, stats: bool = False,
+              progress=None) -> Msa:
+    """divmsa::align_all (msa_merge.hpp:47-49) on the GPU: per-level merge scheduler.
+    progress(done, total) is called once per node as it completes (ProgressFn)."""
+    from ._lib import PROGRESS_FN
     order = _u32(order)
     nd = array_to_nodes(nodes)
     h = C.c_void_p()
     s = dm_stats()
-    check(lib().dm_align_all(seqset.ctx.handle, seqset.handle, nd, len(nodes), _ptr(order),
-                             _ptr(scheme.table, C.c_int16), _ptr(scheme.has_symbol, C.c_uint8),
-                             scheme.open_surcharge(), scheme.gap_extend(), C.byref(h), C.byref(s)))
+    errors = []
+
+    def _cb(done, total, _user):
+        try:
+            progress(int(done), int(total))
+        except BaseException as e:  # noqa: BLE001 -- re-raised after the call
+            errors.append(e)
+
+    cb = PROGRESS_FN(_cb) if progress else None
+    check(lib().dm_align_all_progress(seqset.ctx.handle, seqset.handle, nd, len(nodes), _ptr(order),
+                                      _ptr(scheme.table, C.c_int16), _ptr(scheme.has_symbol, C.c_uint8),
+                                      scheme.open_surcharge(), scheme.gap_extend(),
+                                      C.cast(cb, C.c_void_p) if cb else None, None, C.byref(h), C.byref(s)))
+    if errors:
+        lib().dm_msa_free(h)
+        raise errors[0]
     try:
         m = _msa_from(h)
     finally:

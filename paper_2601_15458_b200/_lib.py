@@ -19,6 +19,10 @@ class DmError(RuntimeError):
     """A CUDA / runtime failure inside libdmb200 (DM_ECUDA / DM_ENOMEM)."""
 
 
+# dm_progress_fn (include/dm_b200.h): void (*)(uint64_t done, uint64_t total, void* user)
+PROGRESS_FN = C.CFUNCTYPE(None, C.c_uint64, C.c_uint64, C.c_void_p)
+
+
 class dm_node(C.Structure):
     _fields_ = [(f, C.c_uint32) for f in ("begin", "end", "center", "radius", "pole_l", "pole_r")] + [
         (f, C.c_int32) for f in ("left", "right", "parent")] + [("depth", C.c_uint32)]
@@ -98,6 +102,10 @@ SIGNATURES = {
                                         C.c_char_p]),
     "dm_align_all": (C.c_int, [_P, _P, C.POINTER(dm_node), C.c_uint64, _u32p, _i16p, _u8p, C.c_int, C.c_int,
                                C.POINTER(_P), C.POINTER(dm_stats)]),
+    "dm_align_all_progress": (C.c_int, [_P, _P, C.POINTER(dm_node), C.c_uint64, _u32p, _i16p, _u8p, C.c_int, C.c_int,
+                                        C.c_void_p, C.c_void_p, C.POINTER(_P), C.POINTER(dm_stats)]),
+    "dm_format_tree": (C.c_int, [C.POINTER(dm_node), C.c_uint64, C.c_char_p, _u64p, C.c_uint64,
+                                 C.POINTER(C.c_void_p), _u64p]),
     "dm_msa": (C.c_int, [_P, _P, C.c_uint64, C.c_uint64, _i16p, _u8p, C.c_int, C.c_int, C.POINTER(_P),
                          C.POINTER(dm_stats)]),
     "dm_msa_width": (C.c_uint64, [_P]),

@@ -124,8 +124,11 @@ AlignCore align_core(dm_ctx* ctx, const char* data, const uint64_t* offsets, uin
         std::vector<dm_node> nodes;
         std::vector<uint32_t> order;
         dm_stats ts{}, as{};
+        const auto p0 = std::chrono::steady_clock::now();
         build_tree(ctx, s, seed, 100, nodes, order, st ? &ts : nullptr);
+        const auto p1 = std::chrono::steady_clock::now();
         res.msa.reset(align_all(ctx, s, nodes, order, sc, st ? &as : nullptr));
+        const auto p2 = std::chrono::steady_clock::now();
         // re-expand duplicates (pipeline.cpp:130-146): output slot -> (input record, MSA row)
         res.slot_input.assign(n, 0);
         res.slot_row.assign(n, 0);
@@ -156,6 +159,11 @@ AlignCore align_core(dm_ctx* ctx, const char* data, const uint64_t* offsets, uin
             st->kernel_ms = ts.kernel_ms + as.kernel_ms;
             st->launches = ts.launches + as.launches;
             st->nw_calls = as.nw_calls;
+            // host wall time of the two phases (both end synchronised: the
+            // tree's nodes and the MSA rows are in host memory)
+            st->tree_ms = std::chrono::duration<double, std::milli>(p1 - p0).count();
+            st->align_ms = std::chrono::duration<double, std::milli>(p2 - p1).count();
+            st->total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         }
     } catch (...) {
         delete s;

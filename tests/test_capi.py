@@ -137,3 +137,15 @@ def _check_pack_seqs(lens):
         assert lib().dm_pack_nt_seqs(bytes(bad), offs.ctypes.data_as(u64p), len(seqs), dst.ctypes.data,
                                      C.byref(nb)) != 0
     assert lib().dm_pack_nt_seqs(data, offs.ctypes.data_as(u64p), len(seqs), dst[1:].ctypes.data, C.byref(nb)) != 0
+
+
+def test_oracle_synth_is_the_product_generator():
+    """bench.py --impl reference takes its inputs from oracle/_build/libsynth.so
+    (so it never loads libdmb200.so); they must be the product's dm.synth inputs."""
+    import numpy as np
+
+    import oracle
+    import paper_2601_15458_b200 as dm
+    for cfg, scale in ((0, 1.0), (1, 0.001), (3, 0.01), (4, 0.01)):
+        a, b = oracle.synth(cfg, scale), dm.synth(cfg, scale)
+        assert a[0] == b[0] and np.array_equal(a[1], b[1])

@@ -185,3 +185,24 @@ def test_align_all_rejects_malformed_trees(dm, ctx):
         dm.align_all(ss, nodes, [0, 0, 1, 2], sc)
     with pytest.raises(ValueError, match="2n-1"):
         dm.align_all(ss, nodes[:5], order, sc)
+
+
+def test_align_all_progress_per_node(dm, ctx):
+    """ProgressFn (msa_merge.cpp:121-129): one call per node, done = 1..N,
+    total = N, leaves first; a throwing callback surfaces after the call."""
+    import random
+    rng = random.Random(5)
+    seqs = list(dict.fromkeys("".join(rng.choice("ACGT") for _ in range(rng.randint(20, 60))) for _ in range(80)))
+    ss = dm.SeqSet(seqs, ctx)
+    nodes, order = dm.build_tree(ss, seed=3)
+    seen = []
+    m = dm.align_all(ss, nodes, order, dm.ScoringScheme.nucleotide(), progress=lambda d, t: seen.append((d, t)))
+    assert [d for d, _ in seen] == list(range(1, len(nodes) + 1))
+    assert {t for _, t in seen} == {len(nodes)}
+    assert len(m.rows) == len(seqs)
+
+    def boom(d, t):
+        raise KeyError("stop")
+    import pytest as _pt
+    with _pt.raises(KeyError):
+        dm.align_all(ss, nodes, order, dm.ScoringScheme.nucleotide(), progress=boom)
