@@ -29,7 +29,7 @@ int occupancy(const void* kern, int threads, size_t smem) {
     const auto key = std::make_tuple(kern, dev, threads, smem);
     auto it = occ.find(key);
     if (it != occ.end()) return it->second;
-    if (smem > 48 * 1024) {
+    if (smem > 32 * 1024) {  // dynamic + static above 48 KB needs the opt-in
         size_t& lim = optin[{kern, dev}];
         if (smem > lim) {
             DM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

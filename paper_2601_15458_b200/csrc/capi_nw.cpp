@@ -101,7 +101,8 @@ void run_batch(dm_ctx* ctx, const char* A, const uint64_t* a_off, const char* B,
     // symbols (pairwise.cpp:288-297), checked on the uploaded bytes: the first
     // pair in batch order with a bad symbol reports it, a before b
     const uint64_t bad_a = dm::nw_first_bad_symbol(ctx, d_in, abytes, sc.has);
-    const uint64_t bad_b = dm::nw_first_bad_symbol(ctx, d_in + abytes, bbytes, sc.has);
+    bool present[128] = {};
+    const uint64_t bad_b = dm::nw_first_bad_symbol(ctx, d_in + abytes, bbytes, sc.has, present);
     if (bad_a != UINT64_MAX || bad_b != UINT64_MAX) {
         auto job_of = [](const uint64_t* off, uint32_t nj, uint64_t pos) {  // pair holding byte off[0] + pos
             return (uint32_t)(std::upper_bound(off, off + nj + 1, off[0] + pos) - off - 1);
@@ -120,8 +121,10 @@ void run_batch(dm_ctx* ctx, const char* A, const uint64_t* a_off, const char* B,
         jobs[k].b_off = abytes + (b_off[k] - b_off[0]);
         jobs[k].m = (uint32_t)(b_off[k + 1] - b_off[k]);
     }
+    dm::NwScheme scb = sc;  // the column symbols b actually holds (query profiles)
+    dm::set_columns(scb, present);
     dm::NwOut no;
-    dm::nw_run(ctx, d_in, jobs, sc, no, st != nullptr);
+    dm::nw_run(ctx, d_in, jobs, scb, no, st != nullptr);
     mark("aligned");
     std::vector<dm::NwRes> res(njobs);
     if (njobs)

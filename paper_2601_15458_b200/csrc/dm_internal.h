@@ -126,7 +126,8 @@ struct dm_ctx {
     dm::PinnedBuf pin_stage;                 // host_copy.cpp: double buffer for pageable uploads
     cudaEvent_t stage_ev[2] = {};
     // scratch for the aligner / merge scheduler
-    dm::DevBuf nw_in, nw_table, nw_jobs, nw_trace, nw_res, nw_gaps, nw_wrap, rows_a, rows_b, colmap, tree_buf;
+    dm::DevBuf nw_in, nw_table, nw_jobs, nw_trace, nw_res, nw_gaps, nw_wrap, rows_a, rows_b, colmap, tree_buf,
+        nw_seqtab;
     uint64_t launches = 0;
     // Every C ABI call on a context holds this lock (capi_guard.h), so one
     // context may be shared by host threads (the reference's functions are
@@ -140,7 +141,7 @@ private:
         for (dm::DevBuf* b : {&items, &out, &counter, &aux, &aux2, &aux3, &lev_all, &lev_items,
                               &stream_pairs, &stream_out, &stream_offs, &stream_flags, &nw_in, &nw_table,
                               &nw_jobs, &nw_trace, &nw_wrap,
-                              &nw_res, &nw_gaps, &rows_a, &rows_b, &colmap, &tree_buf, &ss_meta, &ss_codes,
+                              &nw_res, &nw_gaps, &rows_a, &rows_b, &colmap, &tree_buf, &nw_seqtab, &ss_meta, &ss_codes,
                               &ss_planes})
             b->sp = s;
         for (dm::DevBuf& b : stage) b.sp = s;

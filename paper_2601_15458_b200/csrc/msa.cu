@@ -186,6 +186,14 @@ dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node
             DM_CUDA(cudaGetLastError());
             ctx->launches += 1;
         }
+        // columns of a merge are a center row: the set's residues and '-'
+        NwScheme scc = sc;
+        {
+            bool present[128] = {};
+            for (int c = 0; c < 128; ++c) present[c] = s->present[c];
+            present[(unsigned char)'-'] = true;
+            set_columns(scc, present);
+        }
         const bool trace = std::getenv("DM_TRACE") != nullptr;
         uint64_t done = 0;
         const uint64_t total = nodes.size();
@@ -210,7 +218,7 @@ dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node
             }
             NwOut no;
             const auto h0 = std::chrono::steady_clock::now();
-            nw_run_sharded(ctx, (const uint8_t*)rowsbuf.p, jobs, sc, no, st != nullptr || trace);
+            nw_run_sharded(ctx, (const uint8_t*)rowsbuf.p, jobs, scc, no, st != nullptr || trace);
             fwd_ms += no.fwd_ms;
             tb_ms += no.tb_ms;
             cells += no.cells;

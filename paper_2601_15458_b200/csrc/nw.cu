@@ -34,6 +34,7 @@
 #include "dm_internal.h"
 #include "nw.h"
 #include "nw_fwd.cuh"
+#include "nw_seq.cuh"
 #include "comm.h"
 
 namespace dm {
@@ -48,7 +49,41 @@ struct TbArgs {
     NwRes* res;
     uint32_t* gaps;
     uint32_t* counter;
+    int diag;  // trace in the throughput kernel's step-major layout (nw_seq.cuh)
 };
+
+// 16 trace bytes: rows R .. R+15 (R 16-aligned, 0-based) of column j (1-based).
+// Column-major (ring kernel): column j-1 of pa bytes. Step-major (throughput
+// kernel, nw_seq.cuh): band b = R / 512 holds (m + 31) steps x 32 lanes x RR
+// bytes, lane g owning rows [g RR, g RR + RR) of the band and writing column j
+// at step j + g - 1; the last band has RR = 16, 8 or 4.
+__device__ __forceinline__ uint4 trace_chunk16(const uint8_t* T, uint32_t n, uint32_t m, uint32_t pa, int diag,
+                                               uint32_t R, uint32_t j) {
+    if (!diag) return *reinterpret_cast<const uint4*>(T + (uint64_t)(j - 1) * pa + R);
+    const uint32_t b = R / nwk::BAND, nb = (n + nwk::BAND - 1) / nwk::BAND;
+    const uint32_t rr = b + 1 < nb ? 16u : nwk::seq_tail_rr(n - b * nwk::BAND);
+    const uint8_t* base = T + (uint64_t)b * (m + 31) * nwk::BAND;
+    const uint32_t l = R - b * nwk::BAND;
+    if (rr == 16) {
+        const uint32_t g = l / 16;
+        return *reinterpret_cast<const uint4*>(base + (uint64_t)(j + g - 1) * 512 + g * 16);
+    }
+    uint32_t w[4];
+    if (rr == 8) {
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t g = l / 8 + h;
+            const uint2 v = *reinterpret_cast<const uint2*>(base + (uint64_t)(j + g - 1) * 256 + g * 8);
+            w[2 * h] = v.x;
+            w[2 * h + 1] = v.y;
+        }
+    } else {
+        for (int h = 0; h < 4; ++h) {
+            const uint32_t g = l / 4 + h;
+            w[h] = *reinterpret_cast<const uint32_t*>(base + (uint64_t)(j + g - 1) * 128 + g * 4);
+        }
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
 
 constexpr int TC = 32;  // tile columns (one per lane)
 constexpr int TR = 64;  // tile rows (bytes per column)
@@ -76,11 +111,11 @@ __global__ void __launch_bounds__(128) nw_traceback_kernel(const TbArgs a) {
             const int r0 = max(0, (int)((i - 1) & ~15u) - (TR - 16));
             const int jc = (int)jtop - g;
             if (jc >= 1) {
-                const uint4* src = reinterpret_cast<const uint4*>(T + (uint64_t)(jc - 1) * pa + r0);
                 uint4* dst = reinterpret_cast<uint4*>(&tile[w][g][0]);
 #pragma unroll
                 for (int q = 0; q < TR / 16; ++q)
-                    if ((uint32_t)(r0 + q * 16) < pa) dst[q] = src[q];
+                    if ((uint32_t)(r0 + q * 16) < pa)
+                        dst[q] = trace_chunk16(T, n, job.m, pa, a.diag, (uint32_t)(r0 + q * 16), (uint32_t)jc);
             }
             __syncwarp();
             if (g == 0) {
@@ -158,6 +193,46 @@ int group_of(uint32_t n) {
     return nb <= 4 ? (int)std::max<uint32_t>(nb, 1) : 8;
 }
 
+// Throughput form (nw_seq.cuh): one warp per alignment, bands in sequence.
+// Used when a batch holds at least as many alignments as the GPU has
+// resident warps: every warp then has its own work and the multi-warp
+// form's ring hand-off (there to cut one alignment's latency) only costs.
+bool use_seq(const dm_ctx* ctx, size_t cnt) {
+    const char* e = std::getenv("DM_NW_SEQ");  // tests / tuning: 1 always, 0 never
+    const int force = e ? std::atoi(e) : -1;
+    if (force >= 0) return force > 0;
+    return cnt >= (size_t)ctx->sm_count * 16;
+}
+
+struct SeqDev {
+    const int32_t* table = nullptr;
+    const int32_t* ptab = nullptr;
+    const uint8_t* plut = nullptr;
+};
+
+template <class V, bool PROF>
+void launch_seq(dm_ctx* ctx, const nwk::SeqArgs& base, uint32_t mmax) {
+    const size_t smem = PROF ? (size_t)nwk::SEQ_WARPS * base.KE * 2048 : (size_t)base.K * base.Kp * 4;
+    const int occ = occupancy((const void*)nwk::nw_seq_kernel<V, PROF>, nwk::SEQ_WARPS * 32, smem);
+    const uint64_t want = (base.njobs + nwk::SEQ_WARPS - 1) / nwk::SEQ_WARPS;
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)occ * ctx->sm_count));
+    nwk::SeqArgs a = base;
+    a.hstride = ((uint64_t)mmax + 2) * nwk::Cell4<V>::words;
+    a.hrow = (int4*)ctx->nw_wrap.get((uint64_t)grid * nwk::SEQ_WARPS * a.hstride * sizeof(int4));
+    nwk::nw_seq_kernel<V, PROF><<<grid, nwk::SEQ_WARPS * 32, smem, ctx->stream>>>(a);
+}
+
+// rows the throughput kernel computes for n rows: whole 512-row bands, the
+// last one at 16 / 8 / 4 rows per lane
+uint64_t seq_rows(uint32_t n) {
+    const uint32_t nb = (n + nwk::BAND - 1) / nwk::BAND;
+    return (uint64_t)(nb - 1) * nwk::BAND + 32ull * nwk::seq_tail_rr(n - (nb - 1) * nwk::BAND);
+}
+// trace bytes of one alignment: column-major (ring kernel) or step-major
+uint64_t trace_bytes(const NwJob& jb, bool seq) {
+    return seq ? seq_rows(jb.n) * (jb.m + 31ull) : (uint64_t)jb.m * ((jb.n + 15) & ~15u);
+}
+
 }  // namespace
 
 void nw_warm() {
@@ -173,6 +248,10 @@ void nw_warm() {
     DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int64_t, 4>));
     DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int64_t, 8>));
     DM_CUDA(cudaFuncGetAttributes(&fa, nw_traceback_kernel));
+    DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_seq_kernel<int32_t, true>));
+    DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_seq_kernel<int32_t, false>));
+    DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_seq_kernel<int64_t, true>));
+    DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_seq_kernel<int64_t, false>));
 }
 
 NwScheme make_scheme(const int16_t* table, const uint8_t* has_symbol, int open_surcharge, int gap_extend) {
@@ -184,18 +263,31 @@ NwScheme make_scheme(const int16_t* table, const uint8_t* has_symbol, int open_s
     if (s.K == 0) throw invalid_argument("scoring scheme has no symbols");
     s.Kp = s.K | 1;
     s.table4.assign((size_t)s.K * s.Kp, 0);
+    s.score.assign((size_t)s.K * s.K, 0);
     for (int x = 0; x < 128; ++x) {
         if (!s.has[x]) continue;
         for (int y = 0; y < 128; ++y) {
             if (!s.has[y]) continue;
             const int v = table[x * 128 + y];
             s.table4[(size_t)s.lut[x] * s.Kp + s.lut[y]] = 4 * v;
+            s.score[(size_t)s.lut[x] * s.K + s.lut[y]] = (int16_t)v;
             s.maxabs = std::max(s.maxabs, std::abs(v));
         }
     }
     s.open = open_surcharge;
     s.extend = gap_extend;
     return s;
+}
+
+void set_columns(NwScheme& sc, const bool* present) {
+    sc.KE = 0;
+    std::memset(sc.plut, 0, sizeof(sc.plut));
+    for (int c = 0; c < 128; ++c)
+        if (present[c] && sc.has[c]) {
+            sc.plut[c] = (uint8_t)sc.KE;
+            sc.pdense[sc.KE] = sc.lut[c];
+            ++sc.KE;
+        }
 }
 
 namespace {
@@ -230,15 +322,36 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
     }
     uint64_t ttot = 0;
     uint32_t nmmax = 0;
+    const bool seq = use_seq(ctx, nj);
     for (const auto& jb : jobs) {
         nmmax = std::max(nmmax, jb.n + jb.m);
         out.cells += (uint64_t)jb.n * jb.m;
-        out.cells_exec += (uint64_t)((jb.n + nwk::BAND - 1) / nwk::BAND) * nwk::BAND * jb.m;
-        ttot += (uint64_t)jb.m * ((jb.n + 15) & ~15u);
+        out.cells_exec += (seq ? seq_rows(jb.n) : (uint64_t)((jb.n + nwk::BAND - 1) / nwk::BAND) * nwk::BAND) * jb.m;
+        ttot += trace_bytes(jb, seq);
     }
     if (nj == 0) return;
-    const int64_t bound = ((int64_t)nmmax + 2) * (sc.maxabs + std::llabs(sc.open) + std::llabs(sc.extend)) * 4;
+    // tagged units: 4 * score (ring kernel), 256 * score (throughput kernel)
+    const int64_t bound = ((int64_t)nmmax + 2) * (sc.maxabs + std::llabs(sc.open) + std::llabs(sc.extend)) *
+                          (seq ? 256 : 4);
     const bool wide = bound >= (1ll << 28);
+    SeqDev sd;
+    const bool prof = seq && sc.KE > 0 && sc.KE <= 8;
+    if (seq) {  // 256-scaled table (TAB) or profile table K x KE (PROF), and the column map
+        std::vector<int32_t> t256((size_t)sc.K * sc.Kp, 0);
+        for (int x = 0; x < sc.K; ++x)
+            for (int y = 0; y < sc.K; ++y) t256[(size_t)x * sc.Kp + y] = 256 * sc.score[(size_t)x * sc.K + y];
+        std::vector<int32_t> pt((size_t)sc.K * std::max(sc.KE, 1), 0);
+        for (int x = 0; x < sc.K; ++x)
+            for (int c = 0; c < sc.KE; ++c) pt[(size_t)x * sc.KE + c] = 256 * sc.score[(size_t)x * sc.K + sc.pdense[c]];
+        char* buf = (char*)ctx->nw_seqtab.get(t256.size() * 4 + pt.size() * 4 + 128 + 64);
+        int32_t* d_t = (int32_t*)buf;
+        int32_t* d_p = d_t + t256.size();
+        uint8_t* d_pl = (uint8_t*)(d_p + pt.size());
+        DM_CUDA(cudaMemcpyAsync(d_t, t256.data(), t256.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+        DM_CUDA(cudaMemcpyAsync(d_p, pt.data(), pt.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+        DM_CUDA(cudaMemcpyAsync(d_pl, sc.plut, 128, cudaMemcpyHostToDevice, ctx->stream));
+        sd = SeqDev{d_t, d_p, d_pl};
+    }
     const size_t smem = (size_t)sc.K * sc.Kp * 4;
     const int32_t* d_table = ctx->nw_table.as<int32_t>(sc.table4.size());
     uint8_t* d_lut = (uint8_t*)ctx->aux2.get(128);
@@ -249,8 +362,8 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
     // Larger alignments first (better tail balance), grouped by warps per
     // alignment; chunked by a trace-memory budget.
     std::vector<NwJob> sj(jobs);
-    std::stable_sort(sj.begin(), sj.end(), [](const NwJob& x, const NwJob& y) {
-        const int gx = group_of(x.n), gy = group_of(y.n);
+    std::stable_sort(sj.begin(), sj.end(), [seq](const NwJob& x, const NwJob& y) {
+        const int gx = seq ? 0 : group_of(x.n), gy = seq ? 0 : group_of(y.n);
         if (gx != gy) return gx > gy;
         return (uint64_t)x.n * x.m > (uint64_t)y.n * y.m;
     });
@@ -260,7 +373,7 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
         size_t c1 = c0;
         uint64_t tb = 0;
         while (c1 < nj) {
-            const uint64_t t = (uint64_t)sj[c1].m * ((sj[c1].n + 15) & ~15u);
+            const uint64_t t = trace_bytes(sj[c1], seq);
             if (c1 > c0 && tb + t > budget) break;
             sj[c1].t_off = tb;
             tb += t;
@@ -275,6 +388,38 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
         if (time_kernels) DM_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
         size_t g0 = c0;
         int gi = 0;
+        if (seq) {  // one launch for the whole chunk
+            uint32_t mmax = 1;
+            for (size_t q = c0; q < c1; ++q) mmax = std::max(mmax, sj[q].m);
+            nwk::SeqArgs sa{};
+            sa.chars = d_chars;
+            sa.jobs = d_jobs;
+            sa.njobs = cnt;
+            sa.lut = d_lut;
+            sa.plut = sd.plut;
+            sa.table = sd.table;
+            sa.ptab = sd.ptab;
+            sa.K = sc.K;
+            sa.Kp = sc.Kp;
+            sa.KE = sc.KE;
+            sa.O = 256 * sc.open;
+            sa.E = 256 * sc.extend;
+            sa.trace = d_trace;
+            sa.res = out.d_res;
+            sa.counter = d_cnt;
+            sa.one = 1;
+            if (wide) {
+                if (prof) launch_seq<int64_t, true>(ctx, sa, mmax);
+                else launch_seq<int64_t, false>(ctx, sa, mmax);
+            } else {
+                if (prof) launch_seq<int32_t, true>(ctx, sa, mmax);
+                else launch_seq<int32_t, false>(ctx, sa, mmax);
+            }
+            DM_CUDA(cudaGetLastError());
+            out.launches += 1;
+            ctx->launches += 1;
+            g0 = c1;
+        }
         while (g0 < c1) {  // one launch per warps-per-alignment group
             const int grp = group_of(sj[g0].n);
             size_t g1 = g0;
@@ -300,7 +445,7 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
             out.fwd_ms += ms;
             DM_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
         }
-        TbArgs ta{d_jobs, cnt, d_trace, out.d_res, out.d_gaps, d_cnt + kGroups};
+        TbArgs ta{d_jobs, cnt, d_trace, out.d_res, out.d_gaps, d_cnt + kGroups, seq ? 1 : 0};
         const int tgrid = (int)std::max<uint64_t>(1, std::min<uint64_t>((cnt + 3) / 4, (uint64_t)ctx->sm_count * 8));
         nw_traceback_kernel<<<tgrid, 128, 0, ctx->stream>>>(ta);
         DM_CUDA(cudaGetLastError());
@@ -338,34 +483,49 @@ __global__ void compact_gaps_kernel(const uint32_t* __restrict__ gaps, const Com
 
 namespace {
 __global__ void bad_symbol_kernel(const uint8_t* __restrict__ b, uint64_t n, uint32_t hasmask0, uint32_t hasmask1,
-                                  uint32_t hasmask2, uint32_t hasmask3, unsigned long long* __restrict__ first) {
+                                  uint32_t hasmask2, uint32_t hasmask3, unsigned long long* __restrict__ first,
+                                  uint32_t* __restrict__ seen) {
     const uint32_t m[4] = {hasmask0, hasmask1, hasmask2, hasmask3};
+    uint32_t sm[4] = {0u, 0u, 0u, 0u};
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         const uint32_t c = b[i];
+        if (c < 128) sm[c >> 5] |= 1u << (c & 31);
         if (c >= 128 || !((m[c >> 5] >> (c & 31)) & 1u)) {
             atomicMin(first, (unsigned long long)i);
-            return;  // later bytes of this thread are larger indices
+            break;  // later bytes of this thread are larger indices
         }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t v = __reduce_or_sync(0xffffffffu, sm[k]);
+        if ((threadIdx.x & 31) == 0 && v) atomicOr(&seen[k], v);
     }
 }
 }  // namespace
 
-uint64_t nw_first_bad_symbol(dm_ctx* ctx, const uint8_t* d_bytes, uint64_t n, const bool* has) {
+uint64_t nw_first_bad_symbol(dm_ctx* ctx, const uint8_t* d_bytes, uint64_t n, const bool* has, bool* present) {
     if (n == 0) return UINT64_MAX;
     uint32_t m[4] = {0, 0, 0, 0};
     for (int c = 0; c < 128; ++c)
         if (has[c]) m[c >> 5] |= 1u << (c & 31);
-    unsigned long long* d_first = ctx->aux.as<unsigned long long>(1);
+    unsigned long long* d_first = ctx->aux.as<unsigned long long>(3);
+    uint32_t* d_seen = reinterpret_cast<uint32_t*>(d_first + 1);
     DM_CUDA(cudaMemsetAsync(d_first, 0xff, 8, ctx->stream));
+    DM_CUDA(cudaMemsetAsync(d_seen, 0, 16, ctx->stream));
     const int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)ctx->sm_count * 8);
-    bad_symbol_kernel<<<std::max(grid, 1), 256, 0, ctx->stream>>>(d_bytes, n, m[0], m[1], m[2], m[3], d_first);
+    bad_symbol_kernel<<<std::max(grid, 1), 256, 0, ctx->stream>>>(d_bytes, n, m[0], m[1], m[2], m[3], d_first,
+                                                                 d_seen);
     DM_CUDA(cudaGetLastError());
     ctx->launches += 1;
-    unsigned long long first = 0;
-    DM_CUDA(cudaMemcpyAsync(&first, d_first, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    unsigned long long h[3] = {0, 0, 0};
+    DM_CUDA(cudaMemcpyAsync(h, d_first, 24, cudaMemcpyDeviceToHost, ctx->stream));
     DM_CUDA(cudaStreamSynchronize(ctx->stream));
-    return first;
+    if (present) {
+        const uint32_t* sv = reinterpret_cast<const uint32_t*>(h + 1);
+        for (int c = 0; c < 128; ++c) present[c] = (sv[c >> 5] >> (c & 31)) & 1u;
+    }
+    return h[0];
 }
 
 void nw_compact_gaps(dm_ctx* ctx, const uint32_t* d_gaps, const std::vector<NwJob>& jobs,

@@ -32,12 +32,21 @@ struct NwScheme {
     uint8_t lut[128] = {};
     int K = 0, Kp = 1;
     std::vector<int32_t> table4;  // K x Kp
+    std::vector<int16_t> score;   // K x K raw scores (dense codes)
     int64_t open = 0, extend = 0;
     int maxabs = 0;
     bool has[128] = {};
+    // Column symbols known to occur (set_columns): the throughput kernel then
+    // keeps a per-lane query profile over them (nw_seq.cuh PROF) when KE <= 8.
+    int KE = 0;
+    uint8_t plut[128] = {};  // char -> profile symbol
+    uint8_t pdense[128] = {};  // profile symbol -> dense code
 };
 
 NwScheme make_scheme(const int16_t* table, const uint8_t* has_symbol, int open_surcharge, int gap_extend);
+// Restrict the column alphabet to the chars flagged in `present` (128
+// flags; chars the scheme does not score are ignored).
+void set_columns(NwScheme& sc, const bool* present);
 
 // Device outputs of one batch (valid until the next nw_run on this ctx).
 struct NwOut {
@@ -71,6 +80,8 @@ void nw_compact_gaps(dm_ctx* ctx, const uint32_t* d_gaps, const std::vector<NwJo
 // scheme (>= 128 or has[c] false), or UINT64_MAX; one scan on ctx->stream
 // and one host sync. (pairwise.cpp:288-297 checks on the host; the batch
 // checks the uploaded bytes instead.)
-uint64_t nw_first_bad_symbol(dm_ctx* ctx, const uint8_t* d_bytes, uint64_t n, const bool* has);
+// present (optional, 128 flags): set for every byte value < 128 found in d_bytes.
+uint64_t nw_first_bad_symbol(dm_ctx* ctx, const uint8_t* d_bytes, uint64_t n, const bool* has,
+                             bool* present = nullptr);
 
 }  // namespace dm

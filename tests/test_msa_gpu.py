@@ -11,6 +11,13 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+
+@pytest.fixture(autouse=True, params=["ring", "seq"])
+def nw_kernel(request, monkeypatch):
+    """MSA parity with the merges on either forward kernel (see test_nw_gpu.py)."""
+    monkeypatch.setenv("DM_NW_SEQ", "1" if request.param == "seq" else "0")
+    return request.param
+
 def rand_str(rng, n, alphabet="ACGT"):
     return "".join(rng.choice(alphabet) for _ in range(n))
 

@@ -11,6 +11,16 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+
+@pytest.fixture(autouse=True, params=["ring", "seq"])
+def nw_kernel(request, monkeypatch):
+    """Every test runs on both forward kernels: the multi-warp ring kernel
+    (nw_fwd.cuh, small batches) and the one-warp-per-alignment throughput
+    kernel (nw_seq.cuh, 256-scaled tags, query profiles, short last bands),
+    which the library picks for batches of >= 16 alignments per SM."""
+    monkeypatch.setenv("DM_NW_SEQ", "1" if request.param == "seq" else "0")
+    return request.param
+
 def rand_str(rng, n, alphabet="ACGT"):
     return "".join(rng.choice(alphabet) for _ in range(n))
 
@@ -192,3 +202,34 @@ def test_more_bands_than_warps_vs_reference(dm, ctx, ref):
     for (a, b), r in zip(big, dm.nw_batch(big, sc, ctx)):
         want = ref.nw_align(a, b, "custom", -32000, -20000, False, symbols=syms, matrix=flatm)
         assert as_tuple(r) == as_tuple(want)
+
+
+@pytest.mark.parametrize("kind", ["nt", "nt-iupac", "aa"])
+def test_last_band_heights_vs_reference(dm, ctx, ref, kind, nw_kernel):
+    """Rows around the last band's 128 / 256 / 512-row forms (4, 8, 16 rows per
+    lane) and column alphabets with and without gaps (query profile for <= 8
+    column symbols, table otherwise)."""
+    rng = random.Random({"nt": 1, "nt-iupac": 2, "aa": 3}[kind])
+    alpha = {"nt": "ACGT", "nt-iupac": "ACGTURYSWKMBDHVN", "aa": "ARNDCQEGHILKMFPSTWYV"}[kind]
+    sc = dm.ScoringScheme.protein() if kind == "aa" else dm.ScoringScheme.nucleotide()
+    pairs = []
+    for la in (1, 4, 5, 127, 128, 129, 255, 256, 257, 383, 384, 385, 511, 512, 513, 640, 641, 768, 769,
+               1023, 1024, 1025, 1153, 1300):
+        a = rand_str(rng, la, alpha)
+        b = list(a)
+        for _ in range(max(1, la // 12)):
+            p = rng.randrange(len(b))
+            op = rng.randrange(4)
+            if op == 0:
+                b[p] = rng.choice(alpha)
+            elif op == 1 and len(b) > 1:
+                del b[p]
+            elif op == 2:
+                b.insert(p, rng.choice(alpha))
+            else:
+                b[p] = "-"
+        pairs.append((a, "".join(b)))
+        pairs.append(("".join(b), a[: max(1, la - 7)]))
+    got = dm.nw_batch(pairs, sc, ctx)
+    for (a, b), r in zip(pairs, got):
+        assert as_tuple(r) == as_tuple(ref.nw_align(a, b, "aa" if kind == "aa" else "nt")), (len(a), len(b))
