@@ -68,19 +68,12 @@ __device__ __forceinline__ uint4 trace_chunk16(const uint8_t* T, uint32_t n, uin
         const uint32_t g = l / 16;
         return *reinterpret_cast<const uint4*>(base + (uint64_t)(j + g - 1) * 512 + g * 16);
     }
+    // 12 / 8 / 4 rows per lane: each 4-row word lies inside one lane's rows
     uint32_t w[4];
-    if (rr == 8) {
-        for (int h = 0; h < 2; ++h) {
-            const uint32_t g = l / 8 + h;
-            const uint2 v = *reinterpret_cast<const uint2*>(base + (uint64_t)(j + g - 1) * 256 + g * 8);
-            w[2 * h] = v.x;
-            w[2 * h + 1] = v.y;
-        }
-    } else {
-        for (int h = 0; h < 4; ++h) {
-            const uint32_t g = l / 4 + h;
-            w[h] = *reinterpret_cast<const uint32_t*>(base + (uint64_t)(j + g - 1) * 128 + g * 4);
-        }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t row = l + 4 * q, g = row / rr, r = row - g * rr;
+        w[q] = *reinterpret_cast<const uint32_t*>(base + (uint64_t)(j + g - 1) * 32 * rr + g * rr + r);
     }
     return make_uint4(w[0], w[1], w[2], w[3]);
 }

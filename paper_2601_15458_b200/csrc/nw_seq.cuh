@@ -21,9 +21,9 @@
 //    rows' scores with RR/4 conflict-free LDS.128 from one base address
 //    instead of RR address IMADs + RR LDS.32 (which conflicted on 61 % of
 //    their wavefronts); TAB (protein, custom schemes) reads the K x Kp table;
-//  * the last band of an alignment uses 8 or 4 rows per lane when it has at
-//    most 256 / 128 rows, so the padded rows per alignment drop from up to
-//    511 to at most 127 (cells_executed).
+//  * the last band of an alignment uses 12, 8 or 4 rows per lane when it has
+//    at most 384 / 256 / 128 rows, so the padded rows per alignment drop from
+//    up to 511 to at most 127 (cells_executed).
 // Same recurrence, tie-breaks and trace byte (tagM | tagGB << 2 | tagGA << 4)
 // as nw_fwd.cuh / pairwise.cpp:332-372; the traceback kernel is shared.
 #pragma once
@@ -51,7 +51,11 @@ __device__ __forceinline__ uint32_t imad_u(uint32_t a, uint32_t b, uint32_t c) {
 
 // rows per lane of an alignment's last band holding `left` rows (1..512)
 __host__ __device__ __forceinline__ uint32_t seq_tail_rr(uint32_t left) {
+#ifdef DM_NW_SEQ_NO12
     return left > 256 ? 16u : left > 128 ? 8u : 4u;
+#else
+    return left > 384 ? 16u : left > 256 ? 12u : left > 128 ? 8u : 4u;
+#endif
 }
 
 struct SeqArgs {
@@ -286,6 +290,11 @@ __device__ __forceinline__ void seq_band(const SeqArgs& a, const NwJob& job, uin
         // outside their columns store don't-care bytes no traceback reads)
         if constexpr (RR == 16) *reinterpret_cast<uint4*>(tptr) = make_uint4(tw[0], tw[1], tw[2], tw[3]);
         else if constexpr (RR == 8) *reinterpret_cast<uint2*>(tptr) = make_uint2(tw[0], tw[1]);
+        else if constexpr (RR == 12) {
+            reinterpret_cast<uint32_t*>(tptr)[0] = tw[0];
+            reinterpret_cast<uint32_t*>(tptr)[1] = tw[1];
+            reinterpret_cast<uint32_t*>(tptr)[2] = tw[2];
+        }
         else *reinterpret_cast<uint32_t*>(tptr) = tw[0];
         tptr += 32 * RR;
         iM = xM;
@@ -353,10 +362,16 @@ __global__ void __launch_bounds__(SEQ_WARPS * 32, sizeof(V) == 4 ? DM_NW_SEQ_MIN
         const uint32_t nb = (job.n + BAND - 1) / BAND;
         for (uint32_t band = 0; band < nb; ++band) {
             const uint32_t left = job.n - band * BAND;
-            if (left > 256)
+            const uint32_t rr = seq_tail_rr(left > BAND ? BAND : left);
+            if (rr == 16)
                 seq_band<V, PROF, 16>(a, job, band, hin, s_dyn, s_prof, s_plut, s_lut, s_fifo_all[w], keep,
                                       four, sixteen);
-            else if (left > 128)
+#ifndef DM_NW_SEQ_NO12
+            else if (rr == 12)
+                seq_band<V, PROF, 12>(a, job, band, hin, s_dyn, s_prof, s_plut, s_lut, s_fifo_all[w], keep,
+                                      four, sixteen);
+#endif
+            else if (rr == 8)
                 seq_band<V, PROF, 8>(a, job, band, hin, s_dyn, s_prof, s_plut, s_lut, s_fifo_all[w], keep,
                                       four, sixteen);
             else
