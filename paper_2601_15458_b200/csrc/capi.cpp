@@ -70,6 +70,11 @@ int dm_ctx_create(int device, dm_ctx** out) {
             throw dm::cuda_error(std::string("libdmb200 is built for sm_100a; device is ") + prop.name);
         }
         c->sm_count = prop.multiProcessorCount;
+        {
+            size_t fr = 0, tot = 0;
+            DM_CUDA(cudaMemGetInfo(&fr, &tot));
+            c->free_at_create = fr;
+        }
         // sequence sets are stream-ordered allocations: keep freed memory in the
         // pool so repeated create/destroy (one per batch) never returns to the driver
         cudaMemPool_t pool;

@@ -95,6 +95,7 @@ struct dm_ctx {
     cudaStream_t stream = nullptr;      // stream every call is issued on
     cudaStream_t own_stream = nullptr;  // created by dm_ctx_create (null once replaced)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    uint64_t free_at_create = 0;  // device memory free when the context was created (sizes trace budgets)
     int rank = 0, world = 1;   // NCCL shard of this context (dm_ctx_attach_nccl)
     int sim_world = 1;         // >1: run the sharded path on this one GPU (tests)
     void* nccl = nullptr;      // ncclComm_t

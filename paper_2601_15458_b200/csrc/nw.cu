@@ -360,7 +360,13 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
         if (gx != gy) return gx > gy;
         return (uint64_t)x.n * x.m > (uint64_t)y.n * y.m;
     });
-    const uint64_t budget = std::max<uint64_t>(std::min<uint64_t>(ttot, 6ull << 30), 1);
+    // Trace budget: up to ~45 % of the device's free memory (every chunk ends
+    // with a host sync and a half-empty last wave, so one chunk per batch is
+    // best: a cfg4 merge level holds up to 2.4e10 cells = 24 GB of trace),
+    // at least 6 GB; DM_NW_TRACE_GB caps it (tests).
+    uint64_t cap = std::max<uint64_t>(6ull << 30, ctx->free_at_create / 100 * 45);
+    if (const char* e = std::getenv("DM_NW_TRACE_GB")) cap = std::max<uint64_t>(1, (uint64_t)(std::atof(e) * (1ull << 30)));
+    const uint64_t budget = std::max<uint64_t>(std::min<uint64_t>(ttot, cap), 1);
     size_t c0 = 0;
     while (c0 < nj) {
         size_t c1 = c0;

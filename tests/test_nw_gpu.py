@@ -233,3 +233,21 @@ def test_last_band_heights_vs_reference(dm, ctx, ref, kind, nw_kernel):
     got = dm.nw_batch(pairs, sc, ctx)
     for (a, b), r in zip(pairs, got):
         assert as_tuple(r) == as_tuple(ref.nw_align(a, b, "aa" if kind == "aa" else "nt")), (len(a), len(b))
+
+
+def test_trace_budget_chunks_vs_reference(dm, ctx, ref, monkeypatch, nw_kernel):
+    """A small trace budget splits the batch into many chunks (forward +
+    traceback per chunk, the trace buffer reused); results unchanged."""
+    monkeypatch.setenv("DM_NW_TRACE_GB", "0.002")
+    rng = random.Random(77)
+    pairs = []
+    for _ in range(40):
+        la = rng.randint(200, 1400)
+        a = rand_str(rng, la)
+        b = list(a)
+        for _ in range(la // 20):
+            b[rng.randrange(len(b))] = rng.choice("ACGT")
+        pairs.append((a, "".join(b[: max(1, la - rng.randint(0, 50))])))
+    got = dm.nw_batch(pairs, dm.ScoringScheme.nucleotide(), ctx)
+    for (a, b), r in zip(pairs, got):
+        assert as_tuple(r) == as_tuple(ref.nw_align(a, b)), (len(a), len(b))
