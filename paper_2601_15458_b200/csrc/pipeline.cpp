@@ -5,7 +5,11 @@
 // de-duplication keeping first occurrences (seq_io.cpp:168-186), then
 // build_tree + align_all on the device, then duplicate re-expansion in tree or
 // input row order (pipeline.cpp:130-146).
+#include <algorithm>
+#include <atomic>
+#include <cctype>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -13,6 +17,7 @@
 #include <unordered_map>
 
 #include "capi_guard.h"
+#include "host_par.h"
 #include "nw.h"
 #include "pipeline.h"
 
@@ -23,16 +28,27 @@ constexpr std::string_view kNucleotide = "ACGTURYSWKMBDHVN";
 constexpr std::string_view kProtein = "ARNDCQEGHILKMFPSTWYVBZX*";
 
 int detect_alphabet(const char* data, uint64_t nbytes) {  // alphabet.cpp:37-57; 0 nt, 1 aa
-    uint64_t total = 0, nt = 0;
-    for (uint64_t i = 0; i < nbytes; ++i) {
-        const char raw = data[i];
-        if (raw == '-') continue;
-        const char c = (char)std::toupper((unsigned char)raw);
-        ++total;
-        switch (c) {
-            case 'A': case 'C': case 'G': case 'T': case 'U': case 'N': ++nt; break;
-            default: break;
+    // counted in parallel chunks (the same totals as the reference's loop)
+    const uint64_t chunk = 1 << 20, nc = (nbytes + chunk - 1) / chunk;
+    std::vector<uint64_t> tot(nc, 0), ntc(nc, 0);
+    host_parallel_for(nc, 1, [&](uint64_t k) {
+        uint64_t t = 0, c = 0;
+        for (uint64_t i = k * chunk, e = std::min(nbytes, i + chunk); i < e; ++i) {
+            const char raw = data[i];
+            if (raw == '-') continue;
+            ++t;
+            switch ((char)std::toupper((unsigned char)raw)) {
+                case 'A': case 'C': case 'G': case 'T': case 'U': case 'N': ++c; break;
+                default: break;
+            }
         }
+        tot[k] = t;
+        ntc[k] = c;
+    });
+    uint64_t total = 0, nt = 0;
+    for (uint64_t k = 0; k < nc; ++k) {
+        total += tot[k];
+        nt += ntc[k];
     }
     if (total == 0) return 0;
     return nt * 10 > total * 9 ? 0 : 1;
@@ -52,6 +68,15 @@ AlignCore align_core(dm_ctx* ctx, const char* data, const uint64_t* offsets, uin
                      dm_stats* st) {
     AlignCore res;
     const auto t0 = std::chrono::steady_clock::now();
+    const bool trace = std::getenv("DM_TRACE") != nullptr;
+    auto tlast = t0;
+    auto mark = [&](const char* what) {
+        if (!trace) return;
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[dm align_sequences] %s %.2f ms\n", what,
+                     std::chrono::duration<double, std::milli>(t - tlast).count());
+        tlast = t;
+    };
     if (n == 0) throw runtime_error("no sequences to align");
     if (gap_open > gap_extend || gap_extend > 0)
         throw invalid_argument("gap penalties must satisfy gap_open <= gap_extend <= 0");
@@ -60,10 +85,29 @@ AlignCore align_core(dm_ctx* ctx, const char* data, const uint64_t* offsets, uin
     auto rec = [ids](uint32_t i) {
         return "record '" + (ids ? (*ids)[i] : "seq" + std::to_string(i)) + "'";
     };
-    if (!custom_table) {
-        bool member[256] = {};
+    // First record (in input order) failing a byte-class test, checked in
+    // parallel over records; the message is then built sequentially for it,
+    // so errors read exactly as the reference's in-order loops report them.
+    auto first_bad_record = [&](const bool* bad) -> uint32_t {
+        std::atomic<uint32_t> first{UINT32_MAX};
+        host_parallel_for(n, 256, [&](uint64_t i) {
+            if (i >= first.load(std::memory_order_relaxed)) return;
+            for (uint64_t p = offsets[i]; p < offsets[i + 1]; ++p)
+                if (bad[(unsigned char)data[p]]) {
+                    uint32_t cur = first.load();
+                    while (i < cur && !first.compare_exchange_weak(cur, (uint32_t)i)) {
+                    }
+                    return;
+                }
+        });
+        return first.load();
+    };
+    if (!custom_table) {  // validate_residues (seq_io.cpp:148-166)
+        bool member[256] = {}, bad[256];
         for (char c : (kind == 0 ? kNucleotide : kProtein)) member[(unsigned char)c] = true;
-        for (uint32_t i = 0; i < n; ++i)
+        for (int c = 0; c < 256; ++c) bad[c] = !member[c];
+        const uint32_t i = first_bad_record(bad);
+        if (i != UINT32_MAX)
             for (uint64_t p = offsets[i]; p < offsets[i + 1]; ++p) {
                 const char c = data[p];
                 if (c == '-') throw runtime_error(rec(i) + " contains gap symbol '-' in unaligned input");
@@ -83,42 +127,62 @@ AlignCore align_core(dm_ctx* ctx, const char* data, const uint64_t* offsets, uin
         const int rc = dm_scheme_default(kind, gap_open, gap_extend, flat, table, has, &osur);
         if (rc != DM_OK) throw invalid_argument(last_error());
     }
-    for (uint32_t i = 0; i < n; ++i)
-        for (uint64_t p = offsets[i]; p < offsets[i + 1]; ++p) {
-            const unsigned char c = (unsigned char)data[p];
-            if (c >= 128 || !has[c])
-                throw runtime_error(rec(i) + " contains character '" + std::string(1, (char)c) +
-                                    "' that the substitution matrix does not score");
+    {  // every residue scored by the scheme (pipeline.cpp:92-100)
+        bool bad[256];
+        for (int c = 0; c < 256; ++c) bad[c] = c >= 128 || !has[c];
+        const uint32_t i = first_bad_record(bad);
+        if (i != UINT32_MAX)
+            for (uint64_t p = offsets[i]; p < offsets[i + 1]; ++p) {
+                const unsigned char c = (unsigned char)data[p];
+                if (bad[c])
+                    throw runtime_error(rec(i) + " contains character '" + std::string(1, (char)c) +
+                                        "' that the substitution matrix does not score");
+            }
+    }
+    mark("validate");
+    // deduplicate: first occurrences in order (seq_io.cpp:168-186); the
+    // records' hashes are computed in parallel, the first-occurrence pass is
+    // sequential over them
+    std::vector<uint64_t> hv(n);
+    host_parallel_for(n, 256, [&](uint64_t i) {
+        hv[i] = std::hash<std::string_view>{}(std::string_view(data + offsets[i], offsets[i + 1] - offsets[i]));
+    });
+    struct KeyHash {
+        const std::vector<uint64_t>* h;
+        size_t operator()(uint32_t i) const { return (size_t)(*h)[i]; }
+    };
+    struct KeyEq {
+        const char* d;
+        const uint64_t* o;
+        bool operator()(uint32_t a, uint32_t b) const {
+            const uint64_t la = o[a + 1] - o[a], lb = o[b + 1] - o[b];
+            return la == lb && std::memcmp(d + o[a], d + o[b], la) == 0;
         }
-    // deduplicate: first occurrences in order (seq_io.cpp:168-186)
-    std::unordered_map<std::string_view, uint32_t> first;
-    first.reserve(n * 2);
+    };
+    std::unordered_map<uint32_t, uint32_t, KeyHash, KeyEq> first(n * 2, KeyHash{&hv}, KeyEq{data, offsets});
     std::vector<uint32_t> reps;
     std::vector<std::vector<uint32_t>> dups;
     for (uint32_t i = 0; i < n; ++i) {
-        std::string_view sv(data + offsets[i], offsets[i + 1] - offsets[i]);
-        auto it = first.find(sv);
+        auto it = first.find(i);
         if (it == first.end()) {
-            first.emplace(sv, (uint32_t)reps.size());
+            first.emplace(i, (uint32_t)reps.size());
             reps.push_back(i);
             dups.emplace_back();
         } else {
             dups[it->second].push_back(i);
         }
     }
-    std::vector<uint64_t> roff(reps.size() + 1);
-    std::string rdata;
-    uint64_t tot = 0;
-    for (size_t r = 0; r < reps.size(); ++r) tot += offsets[reps[r] + 1] - offsets[reps[r]];
-    rdata.reserve(tot);
-    for (size_t r = 0; r < reps.size(); ++r) {
-        roff[r] = rdata.size();
-        rdata.append(data + offsets[reps[r]], offsets[reps[r] + 1] - offsets[reps[r]]);
-    }
-    roff[reps.size()] = rdata.size();
+    std::vector<uint64_t> roff(reps.size() + 1, 0);
+    for (size_t r = 0; r < reps.size(); ++r) roff[r + 1] = roff[r] + (offsets[reps[r] + 1] - offsets[reps[r]]);
+    std::string rdata(roff[reps.size()], '\0');
+    host_parallel_for(reps.size(), 256, [&](uint64_t r) {
+        std::memcpy(&rdata[roff[r]], data + offsets[reps[r]], roff[r + 1] - roff[r]);
+    });
     res.reps = reps;
     res.dups = dups;
+    mark("dedup");
     dm_seqset* s = seqset_create(ctx, rdata.data(), roff.data(), (uint32_t)reps.size());
+    mark("seqset");
     try {
         const NwScheme sc = make_scheme(table, has, osur, gap_extend);
         std::vector<dm_node> nodes;
@@ -129,6 +193,7 @@ AlignCore align_core(dm_ctx* ctx, const char* data, const uint64_t* offsets, uin
         const auto p1 = std::chrono::steady_clock::now();
         res.msa.reset(align_all(ctx, s, nodes, order, sc, st ? &as : nullptr));
         const auto p2 = std::chrono::steady_clock::now();
+        mark("tree+align");
         // re-expand duplicates (pipeline.cpp:130-146): output slot -> (input record, MSA row)
         res.slot_input.assign(n, 0);
         res.slot_row.assign(n, 0);
@@ -143,6 +208,7 @@ AlignCore align_core(dm_ctx* ctx, const char* data, const uint64_t* offsets, uin
             place(reps[rep]);
             for (uint32_t d : dups[rep]) place(d);
         }
+        mark("expand");
         res.summary.input_count = n;
         res.summary.unique_count = reps.size();
         res.summary.duplicate_count = n - reps.size();
@@ -188,7 +254,9 @@ int dm_align_sequences(dm_ctx* ctx, const char* data, const uint64_t* offsets, u
         const uint64_t W = res.msa->width;
         char* out = (char*)std::malloc(std::max<uint64_t>((uint64_t)n * W, 1));
         if (!out) throw std::bad_alloc();
-        for (uint32_t k = 0; k < n; ++k) std::memcpy(out + (uint64_t)k * W, res.msa->rows.data() + (uint64_t)res.slot_row[k] * W, W);
+        dm::host_parallel_for(n, 64, [&](uint64_t k) {
+            std::memcpy(out + k * W, res.msa->rows.data() + (uint64_t)res.slot_row[k] * W, W);
+        });
         *rows_out = out;
         *width_out = W;
         if (summary) *summary = res.summary;
