@@ -205,10 +205,15 @@ def msa_bench(dm, ctx, cfgs, reps, world, rank):
         match = None if g is None else best["sha"] == g["rows_sha256"]
         if match is False:
             raise SystemExit(f"bench: {key} MSA rows differ from the reference's (rank {rank})")
+        if world > 1:
+            from paper_2601_15458_b200.dist import comm_stats
+            best["comm"] = comm_stats(ctx)
         entry = {"n": n, "width": best["width"], "wall_s": best["wall_s"], "tree_ms": best["tree_ms"],
                  "align_ms": best["align_ms"], "cells": best["cells"],
                  "gcups_e2e": best["cells"] / best["wall_s"] / 1e9, "gpu_launches": best["launches"],
                  "n_gpus": world, "rows_sha256_matches_reference": match}
+        if "comm" in best:
+            entry["comm_rank0_cumulative"] = best["comm"]
         if g is not None:
             entry["reference_cpu"] = {"wall_s": g["tree_s"] + g["align_s"], "tree_s": g["tree_s"],
                                       "align_s": g["align_s"], "threads": g["threads"],
@@ -581,7 +586,12 @@ def main():
             from paper_2601_15458_b200 import dist as dmdist
             dmdist.attach_from_torch(ctx)
         cfgs = [(int(c), 1.0) for c in args.msa.split(",") if c]
-        line["msa"] = msa_bench(dm, ctx, cfgs, args.msa_reps, world, rank)
+        try:
+            line["msa"] = msa_bench(dm, ctx, cfgs, args.msa_reps, world, rank)
+        except SystemExit:
+            raise
+        except Exception as e:  # noqa: BLE001 -- the distance metric above stands; record why msa failed
+            line["msa"] = {"error": f"{type(e).__name__}: {e}"}
         line["msa_scaling"] = "strong (one MSA job sharded across the ranks)" if world > 1 else "1 GPU"
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -78,12 +78,31 @@ int dm_ctx_set_stream(dm_ctx* ctx, void* stream);
 int dm_int32_peak(dm_ctx* ctx, int mode, double* lane_ops_per_s);
 /* Multi-GPU (one process per GPU): rank 0 makes an NCCL unique id, the caller
  * broadcasts its 128 bytes (e.g. torch.distributed), every rank attaches.
- * Afterwards dm_build_tree / dm_align_all / dm_msa split each distance
- * batch and each merge level across the ranks (contiguous ranges) and
- * exchange the results with ncclAllGather / ncclAllReduce; every rank ends
- * with the full, identical tree and MSA. */
+ * Afterwards dm_build_tree / dm_align_all / dm_msa / dm_align_sequences
+ * split the work across the ranks: the top tree levels' distance batches
+ * and the top merge levels' NW batches in work-balanced ranges (results
+ * all-gathered), and below a split level whole subtrees per rank (tree
+ * nodes, order slices and MSA row blocks all-gathered once); every rank
+ * ends with the full, identical tree and MSA. */
 int dm_nccl_unique_id(uint8_t* id128);
 int dm_ctx_attach_nccl(dm_ctx* ctx, const uint8_t* id128, int rank, int world);
+/* The same sharded execution with the collectives done by the caller on
+ * host memory: fn all-gathers `bytes_per_rank` bytes from every rank into
+ * recv (rank order) and returns 0 on success. Lets several processes share
+ * one GPU in tests (torch.distributed over gloo), or a caller bring its own
+ * transport. */
+typedef int (*dm_allgather_fn)(const void* send, void* recv, uint64_t bytes_per_rank, void* user);
+int dm_ctx_attach_host_comm(dm_ctx* ctx, int rank, int world, dm_allgather_fn fn, void* user);
+/* The shard plan the library uses, for callers and tests: bounds[0..world]
+ * splits n jobs of the given costs into contiguous, cost-balanced ranges;
+ * owner[i] assigns n whole items to ranks, largest cost first to the least
+ * loaded rank (ties to the lower rank). Pure host functions. */
+int dm_shard_bounds(const uint64_t* cost, uint64_t n, int world, uint64_t* bounds);
+/* Counters of this context since creation: out4 = {collective calls, bytes
+ * this rank contributed to them, subtrees it owned in guide trees, subtrees
+ * it owned in merge passes}. */
+int dm_ctx_comm_stats(dm_ctx* ctx, uint64_t* out4);
+int dm_assign_owners(const uint64_t* cost, uint64_t n, int world, int32_t* owner);
 /* Run the sharded code path with `world` shards on this one GPU (tests). */
 int dm_ctx_simulate_world(dm_ctx* ctx, int world);
 /* Record (rank, world) without a communicator (independent shards, e.g. the

@@ -104,6 +104,10 @@ SIGNATURES = {
                                C.POINTER(_P), C.POINTER(dm_stats)]),
     "dm_align_all_progress": (C.c_int, [_P, _P, C.POINTER(dm_node), C.c_uint64, _u32p, _i16p, _u8p, C.c_int, C.c_int,
                                         C.c_void_p, C.c_void_p, C.POINTER(_P), C.POINTER(dm_stats)]),
+    "dm_ctx_attach_host_comm": (C.c_int, [_P, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
+    "dm_shard_bounds": (C.c_int, [_u64p, C.c_uint64, C.c_int, _u64p]),
+    "dm_ctx_comm_stats": (C.c_int, [_P, _u64p]),
+    "dm_assign_owners": (C.c_int, [_u64p, C.c_uint64, C.c_int, C.POINTER(C.c_int32)]),
     "dm_format_tree": (C.c_int, [C.POINTER(dm_node), C.c_uint64, C.c_char_p, _u64p, C.c_uint64,
                                  C.POINTER(C.c_void_p), _u64p]),
     "dm_msa": (C.c_int, [_P, _P, C.c_uint64, C.c_uint64, _i16p, _u8p, C.c_int, C.c_int, C.POINTER(_P),

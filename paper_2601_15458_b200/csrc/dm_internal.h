@@ -99,8 +99,14 @@ struct dm_ctx {
     int rank = 0, world = 1;   // NCCL shard of this context (dm_ctx_attach_nccl)
     int sim_world = 1;         // >1: run the sharded path on this one GPU (tests)
     void* nccl = nullptr;      // ncclComm_t
+    dm_allgather_fn host_allgather = nullptr;  // host-callback collectives (dm_ctx_attach_host_comm)
+    void* host_comm_user = nullptr;
+    dm::PinnedBuf* comm_pin = nullptr;         // staging for host-callback collectives
+    // multi-rank counters (dm_ctx_comm_stats): collectives issued, bytes each
+    // rank contributed, subtrees this rank owned in the tree / the merges
+    uint64_t coll_calls = 0, coll_bytes = 0, own_tree = 0, own_msa = 0;
     // scratch for the distance engine
-    dm::DevBuf items, out, counter, aux, aux2, aux3, lev_all, lev_items;
+    dm::DevBuf items, out, counter, aux, aux2, aux3, lev_all, lev_items, comm_dev, shard_buf;
     // multi-pass distance jobs (lev.cu run_long): plain cudaMalloc (not
     // stream-ordered: they are used on the side streams)
     dm::DevBuf lev_long_off, lev_long_h;
@@ -128,7 +134,7 @@ struct dm_ctx {
     cudaEvent_t stage_ev[2] = {};
     // scratch for the aligner / merge scheduler
     dm::DevBuf nw_in, nw_table, nw_jobs, nw_trace, nw_res, nw_gaps, nw_wrap, rows_a, rows_b, colmap, tree_buf,
-        nw_seqtab;
+        nw_seqtab, nw_shard, nw_shard_gaps;
     uint64_t launches = 0;
     // Every C ABI call on a context holds this lock (capi_guard.h), so one
     // context may be shared by host threads (the reference's functions are
@@ -139,10 +145,11 @@ struct dm_ctx {
 
 private:
     void attach(cudaStream_t* s) {
-        for (dm::DevBuf* b : {&items, &out, &counter, &aux, &aux2, &aux3, &lev_all, &lev_items,
+        for (dm::DevBuf* b : {&items, &out, &counter, &aux, &aux2, &aux3, &lev_all, &lev_items, &comm_dev, &shard_buf,
                               &stream_pairs, &stream_out, &stream_offs, &stream_flags, &nw_in, &nw_table,
                               &nw_jobs, &nw_trace, &nw_wrap,
-                              &nw_res, &nw_gaps, &rows_a, &rows_b, &colmap, &tree_buf, &nw_seqtab, &ss_meta, &ss_codes,
+                              &nw_res, &nw_gaps, &rows_a, &rows_b, &colmap, &tree_buf, &nw_seqtab, &nw_shard, &nw_shard_gaps, &ss_meta,
+                              &ss_codes,
                               &ss_planes})
             b->sp = s;
         for (dm::DevBuf& b : stage) b.sp = s;
@@ -228,8 +235,9 @@ struct LevTotals {
 
 // Run a batch of device-resident items (already oriented, bucket-sorted
 // by the planner). d_out is indexed by item.slot.
+// local: run the whole batch on this rank (subtrees it owns), never sharded.
 void lev_run_host_items(dm_ctx* ctx, const dm_seqset* s, std::vector<LevItem>& items,
-                        uint32_t* d_out, LevTotals* tot, bool time_kernels);
+                        uint32_t* d_out, LevTotals* tot, bool time_kernels, bool local = false);
 // Pairs (2i, 2i+1) of a packed HOST buffer, streamed in chunks (stream.cu).
 // speculate: chunks may be sent raw and planned as A/C/G/T, verified on the
 // device; the pair ranges of chunks that failed go to *redo (the caller runs

@@ -747,48 +747,48 @@ void lev_warm() {
 }
 
 namespace {
-// all[r * maxc + k] holds job lo_r + k of shard r; route it to its slot.
+// all[r * maxc + k] holds job bounds[r] + k of shard r; route it to its slot.
 __global__ void scatter_shards(const uint32_t* __restrict__ all, const LevItem* __restrict__ items, uint64_t n,
-                               int w, uint64_t maxc, uint32_t* __restrict__ out) {
+                               const uint64_t* __restrict__ bounds, int w, uint64_t maxc, uint32_t* __restrict__ out) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         int r = 0;
-        while (r + 1 < w && n * (uint64_t)(r + 1) / (uint64_t)w <= i) ++r;
-        const uint64_t lo = n * (uint64_t)r / (uint64_t)w;
-        out[items[i].slot] = all[(uint64_t)r * maxc + (i - lo)];
+        while (r + 1 < w && bounds[r + 1] <= i) ++r;
+        out[items[i].slot] = all[(uint64_t)r * maxc + (i - bounds[r])];
     }
 }
 }  // namespace
 
 void lev_run_host_items(dm_ctx* ctx, const dm_seqset* s, std::vector<LevItem>& items,
-                        uint32_t* d_out, LevTotals* tot, bool time_kernels) {
+                        uint32_t* d_out, LevTotals* tot, bool time_kernels, bool local) {
     if (items.empty()) return;
     const uint64_t n = items.size();
-    const int w = shard_world(ctx);
+    const int w = local ? 1 : shard_world(ctx);
     if (w == 1) {
         LevItem* d_items = ctx->aux3.as<LevItem>(n);
         DM_CUDA(cudaMemcpyAsync(d_items, items.data(), n * sizeof(LevItem), cudaMemcpyHostToDevice, ctx->stream));
         run_planned(ctx, s, nullptr, nullptr, d_items, n, d_out, tot, time_kernels);
         return;
     }
-    // Sharded batch: each rank computes a contiguous range of jobs into its
-    // row of `all`, the rows are all-gathered, and every rank scatters the
-    // full result to the slots (decisions stay replicated).
-    uint64_t maxc = 0;
-    for (int r = 0; r < w; ++r) {
-        uint64_t lo, hi;
-        shard_range(n, r, w, &lo, &hi);
-        maxc = std::max(maxc, hi - lo);
-    }
+    // Sharded batch: rank r computes the cost-balanced range [bounds[r],
+    // bounds[r+1]) (cost |a| * |b|) into its row of `all`, the rows are
+    // all-gathered, and every rank scatters the full result to the slots
+    // (decisions stay replicated).
+    std::vector<uint64_t> cost(n), bounds;
+    for (uint64_t i = 0; i < n; ++i) cost[i] = (uint64_t)s->len[items[i].pat] * s->len[items[i].txt];
+    shard_bounds(cost.data(), n, w, bounds);
+    uint64_t maxc = 1;
+    for (int r = 0; r < w; ++r) maxc = std::max(maxc, bounds[r + 1] - bounds[r]);
     uint32_t* d_all = ctx->lev_all.as<uint32_t>((uint64_t)w * maxc + 1);
     LevItem* d_global = ctx->lev_items.as<LevItem>(n);
+    uint64_t* d_bounds = ctx->shard_buf.as<uint64_t>((uint64_t)w + 1);
     DM_CUDA(cudaMemcpyAsync(d_global, items.data(), n * sizeof(LevItem), cudaMemcpyHostToDevice, ctx->stream));
-    const bool real = ctx->world > 1;
+    DM_CUDA(cudaMemcpyAsync(d_bounds, bounds.data(), (w + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+    const bool real = comm_real(ctx);
     std::vector<LevItem> sub;
     for (int r = 0; r < w; ++r) {
         if (real && r != ctx->rank) continue;
-        uint64_t lo, hi;
-        shard_range(n, r, w, &lo, &hi);
+        const uint64_t lo = bounds[r], hi = bounds[r + 1];
         if (hi == lo) continue;
         sub.assign(items.begin() + lo, items.begin() + hi);
         for (uint64_t k = 0; k < sub.size(); ++k) sub[k].slot = k;
@@ -796,11 +796,11 @@ void lev_run_host_items(dm_ctx* ctx, const dm_seqset* s, std::vector<LevItem>& i
         DM_CUDA(cudaMemcpyAsync(d_items, sub.data(), sub.size() * sizeof(LevItem), cudaMemcpyHostToDevice,
                                 ctx->stream));
         run_planned(ctx, s, nullptr, nullptr, d_items, sub.size(), d_all + (uint64_t)r * maxc, tot, time_kernels);
-        if (!real) DM_CUDA(cudaStreamSynchronize(ctx->stream));  // host `sub` reused
+        DM_CUDA(cudaStreamSynchronize(ctx->stream));  // host `sub` reused / shard done before the exchange
     }
     if (real) comm_allgather(ctx, d_all + (uint64_t)ctx->rank * maxc, d_all, maxc * sizeof(uint32_t));
     const int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)ctx->sm_count * 8);
-    scatter_shards<<<std::max(grid, 1), 256, 0, ctx->stream>>>(d_all, d_global, n, w, maxc, d_out);
+    scatter_shards<<<std::max(grid, 1), 256, 0, ctx->stream>>>(d_all, d_global, n, d_bounds, w, maxc, d_out);
     DM_CUDA(cudaGetLastError());
     ctx->launches += 1;
 }

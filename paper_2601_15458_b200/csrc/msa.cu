@@ -24,6 +24,7 @@
 #include <cstring>
 #include <numeric>
 
+#include "comm.h"
 #include "dm_internal.h"
 #include "host_copy.h"
 #include "nw.h"
@@ -141,6 +142,92 @@ void apply_sides(dm_ctx* ctx, std::vector<SideDesc>& sides, const uint32_t* d_ga
     ctx->launches += 2;
 }
 
+// Row blocks of whole subtrees: block i = rows [r0, r0 + nrows) x width
+// bytes, packed contiguously at buf_off (one warp per row).
+struct BlockDesc {
+    uint32_t r0, nrows, width, pad;
+    uint64_t buf_off;
+};
+__global__ void pack_blocks_kernel(const BlockDesc* __restrict__ d, uint32_t nb, const uint32_t* __restrict__ rprefix,
+                                   uint32_t total_rows, uint8_t* __restrict__ rows, uint64_t pitch,
+                                   uint8_t* __restrict__ buf, int unpack) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t t = warp; t < total_rows; t += nwarps) {
+        uint32_t lo = 0, hi = nb;  // block holding packed row t
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (rprefix[mid] <= t) lo = mid;
+            else hi = mid;
+        }
+        const BlockDesc b = d[lo];
+        const uint32_t k = t - rprefix[lo];
+        uint8_t* row = rows + (uint64_t)(b.r0 + k) * pitch;
+        uint8_t* pk = buf + b.buf_off + (uint64_t)k * b.width;
+        if (unpack)
+            for (uint32_t c = lane; c < b.width; c += 32) row[c] = pk[c];
+        else
+            for (uint32_t c = lane; c < b.width; c += 32) pk[c] = row[c];
+    }
+}
+
+void run_blocks(dm_ctx* ctx, const std::vector<BlockDesc>& blocks, uint8_t* rows, uint64_t pitch, uint8_t* buf,
+                bool unpack) {
+    if (blocks.empty()) return;
+    std::vector<uint32_t> prefix(blocks.size() + 1, 0);
+    for (size_t i = 0; i < blocks.size(); ++i) prefix[i + 1] = prefix[i] + blocks[i].nrows;
+    BlockDesc* d_b = (BlockDesc*)ctx->aux.get(blocks.size() * sizeof(BlockDesc) + prefix.size() * 4 + 16);
+    uint32_t* d_p = reinterpret_cast<uint32_t*>(d_b + blocks.size());
+    DM_CUDA(cudaMemcpyAsync(d_b, blocks.data(), blocks.size() * sizeof(BlockDesc), cudaMemcpyHostToDevice,
+                            ctx->stream));
+    DM_CUDA(cudaMemcpyAsync(d_p, prefix.data(), prefix.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    const int grid = (int)std::max<uint32_t>(1, std::min<uint32_t>((prefix.back() + 7) / 8, ctx->sm_count * 16u));
+    pack_blocks_kernel<<<grid, 256, 0, ctx->stream>>>(d_b, (uint32_t)blocks.size(), d_p, prefix.back(), rows, pitch,
+                                                      buf, unpack ? 1 : 0);
+    DM_CUDA(cudaGetLastError());
+    DM_CUDA(cudaStreamSynchronize(ctx->stream));  // descriptors reused by the next call
+    ++ctx->launches;
+}
+
+// After each rank merged its own cut subtrees: every rank gets every cut
+// subtree's width (host all-gather) and row block (device all-gather of the
+// packed blocks, padded to the largest rank's bytes).
+void exchange_blocks(dm_ctx* ctx, const std::vector<dm_node>& nodes, const std::vector<uint32_t>& cut,
+                     const std::vector<int>& region, std::vector<uint64_t>& W, DevBuf& rowsbuf, uint64_t& pitch,
+                     uint32_t n) {
+    const int w = ctx->world;
+    std::vector<uint64_t> mine(cut.size(), 0), all(cut.size() * (size_t)w);
+    for (size_t i = 0; i < cut.size(); ++i)
+        if (region[cut[i]] == ctx->rank) mine[i] = W[cut[i]];
+    comm_allgather_host(ctx, mine.data(), all.data(), mine.size() * sizeof(uint64_t));
+    uint64_t wmax = 0;
+    std::vector<uint64_t> bytes((size_t)w, 0);
+    for (size_t i = 0; i < cut.size(); ++i) {
+        const int r = region[cut[i]];
+        W[cut[i]] = all[(size_t)r * cut.size() + i];
+        wmax = std::max(wmax, W[cut[i]]);
+        bytes[r] += (uint64_t)(nodes[cut[i]].end - nodes[cut[i]].begin) * W[cut[i]];
+    }
+    grow_rows(ctx, rowsbuf, pitch, n, wmax);
+    uint64_t mx = 16;
+    for (uint64_t b : bytes) mx = std::max(mx, b);
+    uint8_t* buf = (uint8_t*)ctx->comm_dev.get(mx * (uint64_t)(w + 1) + 64);
+    std::vector<std::vector<BlockDesc>> per((size_t)w);
+    std::vector<uint64_t> at((size_t)w, 0);
+    for (size_t i = 0; i < cut.size(); ++i) {
+        const int r = region[cut[i]];
+        const dm_node& nd = nodes[cut[i]];
+        per[r].push_back(BlockDesc{nd.begin, nd.end - nd.begin, (uint32_t)W[cut[i]], 0, (uint64_t)r * mx + at[r]});
+        at[r] += (uint64_t)(nd.end - nd.begin) * W[cut[i]];
+    }
+    run_blocks(ctx, per[ctx->rank], (uint8_t*)rowsbuf.p, pitch, buf, false);
+    comm_allgather(ctx, buf + (uint64_t)ctx->rank * mx, buf, mx);
+    std::vector<BlockDesc> others;
+    for (int r = 0; r < w; ++r)
+        if (r != ctx->rank) others.insert(others.end(), per[r].begin(), per[r].end());
+    run_blocks(ctx, others, (uint8_t*)rowsbuf.p, pitch, buf, true);
+}
+
 }  // namespace
 
 dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node>& nodes,
@@ -202,9 +289,11 @@ dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node
                 if (nd.left < 0) progress(++done, total, progress_user);
         float fwd_ms = 0, tb_ms = 0;
         uint64_t cells = 0, nw_calls = 0, launches = 0;
-        for (int d = (int)by_depth.size() - 1; d >= 0; --d) {
-            const auto& lvl = by_depth[d];
-            if (lvl.empty()) continue;
+        // One tree level's merges (lvl): NW of the children's center rows,
+        // then every child row rewritten through its column map. local: the
+        // batch is this rank's own (subtree ownership), never sharded.
+        auto run_level = [&](const std::vector<uint32_t>& lvl, int d, bool local) {
+            if (lvl.empty()) return;
             std::vector<NwJob> jobs(lvl.size());
             for (size_t k = 0; k < lvl.size(); ++k) {
                 const dm_node& nd = nodes[lvl[k]];
@@ -218,7 +307,7 @@ dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node
             }
             NwOut no;
             const auto h0 = std::chrono::steady_clock::now();
-            nw_run_sharded(ctx, (const uint8_t*)rowsbuf.p, jobs, scc, no, st != nullptr || trace);
+            nw_run_sharded(ctx, (const uint8_t*)rowsbuf.p, jobs, scc, no, st != nullptr || trace, local);
             fwd_ms += no.fwd_ms;
             tb_ms += no.tb_ms;
             cells += no.cells;
@@ -261,8 +350,82 @@ dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node
                 const double ms =
                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
                 std::fprintf(stderr,
-                             "[dm align] depth %d merges %zu cells %.3e fwd %.3f ms tb %.3f ms insert %.3f ms level %.3f ms\n",
-                             d, jobs.size(), (double)no.cells, no.fwd_ms, no.tb_ms, ins, ms);
+                             "[dm align] depth %d merges %zu cells %.3e fwd %.3f ms tb %.3f ms insert %.3f ms level %.3f ms%s\n",
+                             d, jobs.size(), (double)no.cells, no.fwd_ms, no.tb_ms, ins, ms, local ? " (own)" : "");
+            }
+        };
+        // Subtree ownership (several attached ranks): subtrees of at most
+        // n / (DM_OWN_SPLIT x world) rows are cut off and assigned to ranks by
+        // their merge work (sum of the children's center lengths' products);
+        // each rank merges its own (no collective), the finished row blocks
+        // and widths are all-gathered once, and the levels above the cut run
+        // on every rank with their NW batches sharded.
+        std::vector<int> region(nodes.size(), -1);  // owner rank of the node's cut subtree; -1 above the cut
+        std::vector<uint32_t> cut;
+        if (comm_real(ctx) && n >= 4u * (uint32_t)ctx->world) {
+            const uint64_t split = [] {
+                const char* e = std::getenv("DM_OWN_SPLIT");
+                return e ? (uint64_t)std::max(1, std::atoi(e)) : (uint64_t)8;
+            }();
+            const uint64_t lim = std::max<uint64_t>(2, n / (split * (uint64_t)ctx->world));
+            // nodes are numbered parent before child (BFS): one pass finds the cut
+            std::vector<uint8_t> below(nodes.size(), 0);
+            for (size_t v = 0; v < nodes.size(); ++v) {
+                const dm_node& nd = nodes[v];
+                const bool above_parent = nd.parent < 0 || !below[nd.parent];
+                if (above_parent && nd.end - nd.begin <= lim) {
+                    cut.push_back((uint32_t)v);
+                    below[v] = 1;
+                } else if (!above_parent) {
+                    below[v] = 1;
+                }
+            }
+            if (cut.size() >= (size_t)ctx->world) {
+                // merge work per node, children before parents (reverse BFS order)
+                std::vector<uint64_t> work(nodes.size(), 0);
+                for (size_t v = nodes.size(); v-- > 0;) {
+                    const dm_node& nd = nodes[v];
+                    if (nd.left < 0) continue;
+                    work[v] = work[nd.left] + work[nd.right] +
+                              (uint64_t)s->len[nodes[nd.left].center] * s->len[nodes[nd.right].center] + 1;
+                }
+                std::vector<uint64_t> cost(cut.size());
+                for (size_t i = 0; i < cut.size(); ++i) cost[i] = work[cut[i]] + 1;
+                std::vector<int> own;
+                assign_lpt(cost.data(), cost.size(), ctx->world, own);
+                for (size_t i = 0; i < cut.size(); ++i) {
+                    region[cut[i]] = own[i];
+                    ctx->own_msa += own[i] == ctx->rank;
+                }
+                for (size_t v = 0; v < nodes.size(); ++v)  // descendants inherit (parents come first)
+                    if (region[v] < 0 && nodes[v].parent >= 0 && below[v] && region[nodes[v].parent] >= 0)
+                        region[v] = region[nodes[v].parent];
+            } else {
+                cut.clear();
+            }
+        }
+        if (cut.empty()) {
+            for (int d = (int)by_depth.size() - 1; d >= 0; --d) run_level(by_depth[d], d, false);
+        } else {
+            // phase A: this rank's subtrees, deepest level first
+            for (int d = (int)by_depth.size() - 1; d >= 0; --d) {
+                std::vector<uint32_t> mine;
+                for (uint32_t v : by_depth[d])
+                    if (region[v] == ctx->rank) mine.push_back(v);
+                run_level(mine, d, true);
+            }
+            // phase B: widths and row blocks of every cut subtree from its owner
+            exchange_blocks(ctx, nodes, cut, region, W, rowsbuf, pitch, n);
+            if (progress)
+                for (size_t v = 0; v < nodes.size(); ++v)
+                    if (nodes[v].left >= 0 && region[v] >= 0 && region[v] != ctx->rank)
+                        progress(++done, total, progress_user);
+            // phase C: the levels above the cut, on every rank
+            for (int d = (int)by_depth.size() - 1; d >= 0; --d) {
+                std::vector<uint32_t> up;
+                for (uint32_t v : by_depth[d])
+                    if (region[v] < 0) up.push_back(v);
+                run_level(up, d, false);
             }
         }
         const uint64_t width = W[0];

@@ -478,6 +478,18 @@ __global__ void compact_gaps_kernel(const uint32_t* __restrict__ gaps, const Com
         for (uint32_t t = lane; t < c.nb; t += 32) out[c.dst + c.na + t] = gaps[c.src_b + t];
     }
 }
+// inverse of compact_gaps_kernel: compacted entries back to the job's slots
+__global__ void expand_gaps_kernel(const uint32_t* __restrict__ in, const CompactDesc* __restrict__ d, uint64_t n,
+                                   uint32_t* __restrict__ gaps) {
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t k = warp; k < n; k += nwarps) {
+        const CompactDesc c = d[k];
+        for (uint32_t t = lane; t < c.na; t += 32) gaps[c.src_a + t] = in[c.dst + t];
+        for (uint32_t t = lane; t < c.nb; t += 32) gaps[c.src_b + t] = in[c.dst + c.na + t];
+    }
+}
 }  // namespace
 
 namespace {
@@ -549,9 +561,15 @@ void nw_compact_gaps(dm_ctx* ctx, const uint32_t* d_gaps, const std::vector<NwJo
     DM_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
+// Sharded batch: rank r aligns the cost-balanced range [bounds[r],
+// bounds[r+1]) (cost n * m) into the batch's result layout; the ranks then
+// all-gather the NwRes records and the COMPACTED gap lists (nga + ngb
+// entries per job, not the m + n capacity), and every rank expands them into
+// the layout, so all hold every result. Simulated worlds run the ranges in
+// turn into the shared buffers (no exchange needed).
 void nw_run_sharded(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const NwScheme& sc,
-                    NwOut& out, bool time_kernels) {
-    const int w = shard_world(ctx);
+                    NwOut& out, bool time_kernels, bool local) {
+    const int w = local ? 1 : shard_world(ctx);
     if (w == 1 || jobs.size() < 2) {
         nw_run(ctx, d_chars, jobs, sc, out, time_kernels);
         return;
@@ -562,13 +580,13 @@ void nw_run_sharded(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& job
     out.d_res = ctx->nw_res.as<NwRes>(nj);
     out.d_gaps = ctx->nw_gaps.as<uint32_t>(std::max<uint64_t>(gtot, 1));
     out.gaps_total = gtot;
-    DM_CUDA(cudaMemsetAsync(out.d_res, 0, nj * sizeof(NwRes), ctx->stream));
-    DM_CUDA(cudaMemsetAsync(out.d_gaps, 0, std::max<uint64_t>(gtot, 1) * 4, ctx->stream));
-    const bool real = ctx->world > 1;
+    std::vector<uint64_t> cost(nj), bounds;
+    for (size_t k = 0; k < nj; ++k) cost[k] = (uint64_t)jobs[k].n * jobs[k].m;
+    shard_bounds(cost.data(), nj, w, bounds);
+    const bool real = comm_real(ctx);
     for (int r = 0; r < w; ++r) {
         if (real && r != ctx->rank) continue;
-        uint64_t lo, hi;
-        shard_range(nj, r, w, &lo, &hi);
+        const uint64_t lo = bounds[r], hi = bounds[r + 1];
         if (hi == lo) continue;
         std::vector<NwJob> sub(jobs.begin() + lo, jobs.begin() + hi);
         NwOut part;
@@ -582,11 +600,64 @@ void nw_run_sharded(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& job
         out.cells_exec += part.cells_exec;
         out.launches += part.launches;
     }
-    if (real) {
-        static_assert(sizeof(NwRes) % 8 == 0, "NwRes is reduced as int64 words");
-        comm_allreduce_sum_i64(ctx, out.d_res, nj * sizeof(NwRes) / 8);
-        comm_allreduce_sum_u32(ctx, out.d_gaps, gtot);
+    if (!real) return;
+    // 1. results: all-gather each rank's NwRes range (padded to the largest)
+    uint64_t maxc = 1;
+    for (int r = 0; r < w; ++r) maxc = std::max<uint64_t>(maxc, bounds[r + 1] - bounds[r]);
+    const uint64_t lo = bounds[ctx->rank], hi = bounds[ctx->rank + 1];
+    NwRes* d_all = (NwRes*)ctx->nw_shard.get((uint64_t)(w + 1) * maxc * sizeof(NwRes));
+    if (hi > lo)
+        DM_CUDA(cudaMemcpyAsync(d_all + (uint64_t)ctx->rank * maxc, out.d_res + lo, (hi - lo) * sizeof(NwRes),
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+    comm_allgather(ctx, d_all + (uint64_t)ctx->rank * maxc, d_all, maxc * sizeof(NwRes));
+    for (int r = 0; r < w; ++r)
+        if (r != ctx->rank && bounds[r + 1] > bounds[r])
+            DM_CUDA(cudaMemcpyAsync(out.d_res + bounds[r], d_all + (uint64_t)r * maxc,
+                                    (bounds[r + 1] - bounds[r]) * sizeof(NwRes), cudaMemcpyDeviceToDevice,
+                                    ctx->stream));
+    std::vector<NwRes> res(nj);
+    DM_CUDA(cudaMemcpyAsync(res.data(), out.d_res, nj * sizeof(NwRes), cudaMemcpyDeviceToHost, ctx->stream));
+    DM_CUDA(cudaStreamSynchronize(ctx->stream));
+    // 2. gap lists: each rank compacts its own jobs', the compacted lists are
+    // all-gathered (padded to the largest) and expanded into the layout
+    std::vector<uint64_t> coff(nj + 1, 0), rank_g((size_t)w, 0);
+    std::vector<CompactDesc> desc(nj);
+    for (int r = 0; r < w; ++r) {
+        uint64_t acc = 0;
+        for (uint64_t k = bounds[r]; k < bounds[r + 1]; ++k) {
+            coff[k] = acc;
+            acc += res[k].nga + res[k].ngb;
+        }
+        rank_g[r] = acc;
     }
+    uint64_t maxg = 1;
+    for (int r = 0; r < w; ++r) maxg = std::max(maxg, rank_g[r]);
+    uint32_t* d_cg = ctx->nw_shard_gaps.as<uint32_t>((uint64_t)(w + 1) * maxg);
+    uint32_t* mine = d_cg + (uint64_t)ctx->rank * maxg;
+    CompactDesc* d_desc = (CompactDesc*)ctx->aux.get(std::max<size_t>(nj, 1) * sizeof(CompactDesc));
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((nj + 7) / 8, (uint64_t)ctx->sm_count * 16));
+    if (hi > lo) {
+        for (uint64_t k = lo; k < hi; ++k)
+            desc[k - lo] = CompactDesc{jobs[k].ga_off, jobs[k].gb_off, coff[k], res[k].nga, res[k].ngb};
+        DM_CUDA(cudaMemcpyAsync(d_desc, desc.data(), (hi - lo) * sizeof(CompactDesc), cudaMemcpyHostToDevice,
+                                ctx->stream));
+        compact_gaps_kernel<<<grid, 256, 0, ctx->stream>>>(out.d_gaps, d_desc, hi - lo, mine);
+        DM_CUDA(cudaGetLastError());
+    }
+    comm_allgather(ctx, mine, d_cg, maxg * sizeof(uint32_t));
+    uint64_t nd = 0;
+    for (int r = 0; r < w; ++r) {
+        if (r == ctx->rank) continue;
+        for (uint64_t k = bounds[r]; k < bounds[r + 1]; ++k)
+            desc[nd++] = CompactDesc{jobs[k].ga_off, jobs[k].gb_off, (uint64_t)r * maxg + coff[k], res[k].nga,
+                                     res[k].ngb};
+    }
+    if (nd) {
+        DM_CUDA(cudaMemcpyAsync(d_desc, desc.data(), nd * sizeof(CompactDesc), cudaMemcpyHostToDevice, ctx->stream));
+        expand_gaps_kernel<<<grid, 256, 0, ctx->stream>>>(d_cg, d_desc, nd, out.d_gaps);
+        DM_CUDA(cudaGetLastError());
+    }
+    ctx->launches += 2;
 }
 
 }  // namespace dm

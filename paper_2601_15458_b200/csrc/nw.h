@@ -65,11 +65,12 @@ struct NwOut {
 // point at the (shared) result buffers — used by nw_run_sharded.
 void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const NwScheme& sc,
             NwOut& out, bool time_kernels, bool layout_given = false);
-// Same results, with the jobs split across the context's shards (NCCL ranks
-// or the simulated world): each rank aligns its range into zeroed shared
-// buffers, which are then all-reduced (sum) so every rank holds all results.
+// Same results, with the jobs split across the context's shards (attached
+// ranks or the simulated world) in cost-balanced ranges; the ranks exchange
+// the results and compacted gap lists, so every rank holds all of them.
+// local: this rank aligns the whole batch (merges inside its own subtrees).
 void nw_run_sharded(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const NwScheme& sc,
-                    NwOut& out, bool time_kernels);
+                    NwOut& out, bool time_kernels, bool local = false);
 
 // Gathers each job's nga + ngb gap entries (path order, gaps_into_a first)
 // into one compact host array; off[k] = start of job k's entries.

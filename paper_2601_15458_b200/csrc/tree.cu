@@ -21,6 +21,17 @@
 // sorted (rng.hpp:14-59). Ties: argmin/argmax go to the lowest SEQUENCE index
 // (:48-50, :159-163); the partition is stable (:98-109); children are numbered
 // left then right in frontier order (:212-231) by a final BFS renumbering.
+//
+// Several attached ranks: the top levels (few nodes with many
+// members) shard every distance batch across the ranks (cost-balanced
+// ranges, results all-gathered, decisions replicated); once a level holds
+// enough nodes (>= DM_OWN_MIN x world, none larger than 1/(DM_OWN_BAL x
+// world) of the members) the nodes -- with their whole subtrees -- are assigned to ranks
+// (largest first to the least loaded), each rank builds its subtrees with no
+// collective, and the ranks exchange the finished subtrees once (node
+// records and order slices). Pool ids may differ between ranks; the final
+// BFS renumbering depends only on the tree's links, so every rank returns
+// the same nodes and order.
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
@@ -30,6 +41,7 @@
 #include <random>
 #include <unordered_set>
 
+#include "comm.h"
 #include "dm_internal.h"
 #include "rng.h"
 
@@ -355,6 +367,70 @@ struct TreeScratch {
 
 const char* kDedupMsg = "cluster contains identical sequences; input was not de-duplicated";
 
+// Subtree ownership exchange (several ranks): rank blobs hold
+//   [n_roots u64][n_new u64] { root pool id u32, PNode } x n_roots
+//   PNode x n_new { order slice of each root } x n_roots
+// with node links < P0 global pool ids and >= P0 the sender's local ids.
+void put(std::vector<uint8_t>& b, const void* p, size_t n) {
+    const uint8_t* c = static_cast<const uint8_t*>(p);
+    b.insert(b.end(), c, c + n);
+}
+template <class T>
+T take(const std::vector<uint8_t>& b, size_t& at) {
+    T v;
+    std::memcpy(&v, b.data() + at, sizeof(T));
+    at += sizeof(T);
+    return v;
+}
+
+void exchange_subtrees(dm_ctx* ctx, std::vector<PNode>& pool, std::vector<uint32_t>& order, uint32_t P0,
+                       const std::vector<uint32_t>& roots, const std::vector<int>& owner) {
+    std::vector<uint8_t> mine;
+    uint64_t nr = 0;
+    for (size_t i = 0; i < roots.size(); ++i) nr += owner[i] == ctx->rank;
+    const uint64_t nn = pool.size() - P0;
+    put(mine, &nr, 8);
+    put(mine, &nn, 8);
+    for (size_t i = 0; i < roots.size(); ++i)
+        if (owner[i] == ctx->rank) {
+            put(mine, &roots[i], 4);
+            put(mine, &pool[roots[i]], sizeof(PNode));
+        }
+    if (nn) put(mine, &pool[P0], nn * sizeof(PNode));
+    for (size_t i = 0; i < roots.size(); ++i)
+        if (owner[i] == ctx->rank) {
+            const PNode& p = pool[roots[i]];
+            put(mine, order.data() + p.begin, (size_t)(p.end - p.begin) * 4);
+        }
+    std::vector<std::vector<uint8_t>> all;
+    comm_allgatherv_host(ctx, mine, all);
+    for (int r = 0; r < ctx->world; ++r) {
+        if (r == ctx->rank) continue;
+        const std::vector<uint8_t>& b = all[r];
+        size_t at = 0;
+        const uint64_t rn = take<uint64_t>(b, at), rnew = take<uint64_t>(b, at);
+        const uint32_t base = (uint32_t)pool.size();
+        auto remap = [&](int32_t l) -> int32_t { return l < (int32_t)P0 ? l : (int32_t)(base + (uint32_t)l - P0); };
+        auto fix = [&](PNode p) {
+            p.left = p.left < 0 ? -1 : remap(p.left);
+            p.right = p.right < 0 ? -1 : remap(p.right);
+            p.parent = p.parent < 0 ? -1 : remap(p.parent);
+            return p;
+        };
+        std::vector<uint32_t> rid(rn);
+        for (uint64_t k = 0; k < rn; ++k) {
+            rid[k] = take<uint32_t>(b, at);
+            pool[rid[k]] = fix(take<PNode>(b, at));
+        }
+        for (uint64_t k = 0; k < rnew; ++k) pool.push_back(fix(take<PNode>(b, at)));
+        for (uint64_t k = 0; k < rn; ++k) {
+            const PNode& p = pool[rid[k]];
+            std::memcpy(order.data() + p.begin, b.data() + at, (size_t)(p.end - p.begin) * 4);
+            at += (size_t)(p.end - p.begin) * 4;
+        }
+    }
+}
+
 }  // namespace
 
 void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_cap_in,
@@ -393,7 +469,56 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
     auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
         return std::chrono::duration<double, std::milli>(b - a).count();
     };
+    // subtree ownership (several attached ranks), see the header
+    const bool real = comm_real(ctx);
+    const int wr = ctx->world;
+    const uint64_t own_min = [] {
+        const char* e = std::getenv("DM_OWN_MIN");
+        return e ? (uint64_t)std::max(1, std::atoi(e)) : (uint64_t)4;
+    }();
+    // no owned node may exceed 1/(DM_OWN_BAL x world) of the level's members (0: no limit)
+    const uint64_t own_bal = [] {
+        const char* e = std::getenv("DM_OWN_BAL");
+        return e ? (uint64_t)std::max(0, std::atoi(e)) : (uint64_t)2;
+    }();
+    bool owned = false;
+    uint32_t P0 = 0;
+    std::vector<uint32_t> own_roots;
+    std::vector<int> own_of;
+    auto try_own = [&] {
+        if (!real || owned) return;
+        uint64_t members = 0, mx = 0;
+        for (uint32_t id : big) {
+            const uint64_t m = pool[id].end - pool[id].begin;
+            members += m;
+            mx = std::max(mx, m);
+        }
+        if (big.size() < own_min * (uint64_t)wr || mx * own_bal * (uint64_t)wr > members) return;
+        own_roots.assign(big.begin(), big.end());
+        own_roots.insert(own_roots.end(), small.begin(), small.end());
+        std::vector<uint64_t> cost(own_roots.size());
+        for (size_t i = 0; i < own_roots.size(); ++i) {
+            const uint64_t m = pool[own_roots[i]].end - pool[own_roots[i]].begin;
+            uint64_t lg = 0;
+            while ((m >> lg) > 128) ++lg;
+            cost[i] = m * (64 + 3 * lg);  // sweeps per level + median/all-pairs work, per member
+        }
+        assign_lpt(cost.data(), cost.size(), wr, own_of);
+        std::vector<uint32_t> nb2, ns2;
+        for (size_t i = 0; i < own_roots.size(); ++i)
+            if (own_of[i] == ctx->rank) (i < big.size() ? nb2 : ns2).push_back(own_roots[i]);
+        big.swap(nb2);
+        small.swap(ns2);
+        owned = true;
+        ctx->own_tree += big.size() + small.size();
+        P0 = (uint32_t)pool.size();
+        if (trace)
+            std::fprintf(stderr, "[dm tree] rank %d/%d owns %zu + %zu of %zu subtrees\n", ctx->rank, wr, big.size(),
+                         small.size(), own_roots.size());
+    };
     int level = 0;
+    int err_flag = 0;
+    try_own();
     while (!big.empty()) {
         const size_t B = big.size();
         const auto t0 = tnow();
@@ -426,7 +551,7 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
             mtot += (uint64_t)k * k;
         }
         uint32_t* d_mat = sc.mat.as<uint32_t>(mtot);
-        lev_run_host_items(ctx, s, items, d_mat, &tot, timing);
+        lev_run_host_items(ctx, s, items, d_mat, &tot, timing, owned);
         const auto t_med = tnow();
         uint32_t* d_center = sc.res1.as<uint32_t>(B);
         median_argmin_kernel<<<(unsigned)B, 128, 0, stream>>>(
@@ -444,7 +569,7 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
             items.clear();
             for (size_t v = 0; v < B; ++v)
                 for (uint32_t p = nb[v]; p < ne[v]; ++p) items.push_back(LevItem{from[v], order[p], p});
-            lev_run_host_items(ctx, s, items, d_dist, &tot, timing);
+            lev_run_host_items(ctx, s, items, d_dist, &tot, timing, owned);
         };
         uint32_t* d_max = sc.res2.as<uint32_t>(B);
         uint32_t* d_arg = sc.res3.as<uint32_t>(B);
@@ -459,8 +584,13 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
         DM_CUDA(cudaGetLastError());
         download(ctx, pole_r, d_arg, B);
         DM_CUDA(cudaStreamSynchronize(stream));
-        for (size_t v = 0; v < B; ++v)
-            if (pole_r[v] == pole_l[v]) throw runtime_error(kDedupMsg);
+        bool dup = false;
+        for (size_t v = 0; v < B; ++v) dup = dup || pole_r[v] == pole_l[v];
+        if (dup) {
+            if (!owned) throw runtime_error(kDedupMsg);
+            err_flag = 1;  // reported by every rank after the exchange
+            break;
+        }
         sweep(pole_r, d_dr);
         uint32_t* d_mid = sc.res1.as<uint32_t>(B);
         partition_kernel<<<(unsigned)B, 256, 0, stream>>>(d_order, d_tmp, d_dl, d_dr, d_nb, d_ne, d_mid);
@@ -504,10 +634,11 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
         }
         ++level;
         big.swap(next);
+        try_own();
     }
 
     // ---- small subtrees: one all-pairs matrix each, resolved on the device
-    if (!small.empty()) {
+    if (!small.empty() && !err_flag) {
         const size_t S = small.size();
         std::vector<uint32_t> sb(S), sk(S);
         std::vector<uint64_t> moff(S), roff(S);
@@ -529,7 +660,7 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
         }
         const auto s0 = tnow();
         uint32_t* d_mat = sc.sub_mat.as<uint32_t>(mtot);
-        lev_run_host_items(ctx, s, items, d_mat, &tot, timing);
+        lev_run_host_items(ctx, s, items, d_mat, &tot, timing, owned);
         const auto s1 = tnow();
         if (trace)
             std::fprintf(stderr, "[dm tree] small subtrees %zu pairs %zu all-pairs %.3f ms\n", S, items.size(),
@@ -551,7 +682,8 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
         DM_CUDA(cudaMemcpyAsync(&err, d_err, sizeof(int), cudaMemcpyDeviceToHost, stream));
         DM_CUDA(cudaMemcpyAsync(order.data(), d_order, (size_t)n * 4, cudaMemcpyDeviceToHost, stream));
         DM_CUDA(cudaStreamSynchronize(stream));
-        if (err) throw runtime_error(kDedupMsg);
+        if (err && !owned) throw runtime_error(kDedupMsg);
+        if (err) err_flag = 1;
         for (size_t r = 0; r < S; ++r) {
             const uint32_t root = small[r];
             const uint32_t k = sk[r];
@@ -579,6 +711,15 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
                 p.depth = d0 + R[h].depth;
             }
         }
+    }
+
+    if (owned) {
+        int bad = err_flag;  // a duplicate found by any rank fails every rank
+        std::vector<int> allbad((size_t)wr);
+        comm_allgather_host(ctx, &bad, allbad.data(), sizeof(int));
+        for (int b : allbad)
+            if (b) throw runtime_error(kDedupMsg);
+        exchange_subtrees(ctx, pool, order, P0, own_roots, own_of);
     }
 
     // ---- BFS renumbering = the reference's level-synchronous numbering

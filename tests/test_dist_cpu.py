@@ -1,11 +1,13 @@
-"""CPU, world_size 2 over gloo: the host side of the multi-GPU sharding.
-
-Each rank computes its contiguous range of a distance batch (here with the
-CPU oracle standing in for the GPU kernel), the ranges are all-gathered with
-padding exactly as comm.cpp / lev.cu do with ncclAllGather, every rank
-routes the rows back to job order (scatter_shards) and must hold the full,
-identical result. The NW result exchange (zeroed buffers + sum all-reduce)
-and the NCCL-id broadcast are exercised the same way."""
+"""CPU, world_size 2/3 over gloo: the host side of the multi-GPU sharding,
+driven by the library's own plan functions (libdmb200 dm_shard_bounds /
+dm_assign_owners, pure host code). Each rank computes its cost-balanced
+range of a distance batch (the CPU oracle standing in for the kernel), the
+ranges are all-gathered with padding as comm.cpp / lev.cu do, and every
+rank must hold the full, identical result; subtree ownership must be
+identical and balanced on every rank; compacted variable-length gap lists
+go through the padded all-gather nw.cu uses. The full multi-rank GPU path
+(these collectives inside libdmb200, several processes on one GPU) is
+tests/test_multirank_gpu.py."""
 import os
 import random
 import socket
@@ -31,35 +33,49 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import oracle
-        from paper_2601_15458_b200.dist import gather_sharded, owner_of, shard_range
+        from paper_2601_15458_b200.dist import assign_owners, shard_bounds
         orc = oracle.restatement()
         rng = random.Random(17)
         seqs = ["".join(rng.choice("ACGT") for _ in range(rng.randint(0, 60))) for _ in range(80)]
         jobs = [(rng.randrange(80), rng.randrange(80)) for _ in range(101)]  # odd count: uneven shards
         n = len(jobs)
-        maxc = max(shard_range(n, r, world)[1] - shard_range(n, r, world)[0] for r in range(world))
-        lo, hi = shard_range(n, rank, world)
-        mine = np.zeros(maxc, dtype=np.int64)
+        # the library's own plan (dm_shard_bounds), cost |a| * |b| as lev.cu uses
+        cost = np.array([len(seqs[a]) * len(seqs[b]) for a, b in jobs], dtype=np.uint64)
+        bounds = shard_bounds(cost, world)
+        plans = [None] * world
+        dist.all_gather_object(plans, bounds.tolist())
+        ok_plan = all(p == bounds.tolist() for p in plans) and bounds[0] == 0 and bounds[-1] == n
+        maxc = int(max(bounds[r + 1] - bounds[r] for r in range(world)))
+        lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+        mine = np.zeros(max(maxc, 1), dtype=np.int64)
         for k, (a, b) in enumerate(jobs[lo:hi]):
             mine[k] = orc.levenshtein(seqs[a], seqs[b])
-        parts = [torch.zeros(maxc, dtype=torch.int64) for _ in range(world)]
+        parts = [torch.zeros(max(maxc, 1), dtype=torch.int64) for _ in range(world)]
         dist.all_gather(parts, torch.from_numpy(mine))
-        got = gather_sharded([p.numpy() for p in parts], n, world)
+        got = np.empty(n, dtype=np.int64)  # lev.cu scatter_shards: rank r's row -> its range
+        for r in range(world):
+            b0, b1 = int(bounds[r]), int(bounds[r + 1])
+            got[b0:b1] = parts[r].numpy()[: b1 - b0]
         want = np.array([orc.levenshtein(seqs[a], seqs[b]) for a, b in jobs])
         ok_lev = bool(np.array_equal(got, want))
-        ok_owner = all(shard_range(n, owner_of(i, n, world), world)[0] <= i <
-                       shard_range(n, owner_of(i, n, world), world)[1] for i in range(n))
-        # NW-style exchange: each rank writes its slots into a zeroed buffer, sum all-reduce
-        buf = torch.zeros(n, dtype=torch.int64)
-        for i in range(lo, hi):
-            buf[i] = int(want[i]) - 7  # signed values survive the sum
-        dist.all_reduce(buf)
-        ok_sum = bool(np.array_equal(buf.numpy(), want - 7))
-        # NCCL-id broadcast path (128 opaque bytes from rank 0)
-        obj = [bytes(range(128)) if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        ok_uid = obj[0] == bytes(range(128))
-        q.put((rank, ok_lev, ok_owner, ok_sum, ok_uid))
+        # subtree ownership (dm_assign_owners): identical on every rank, LPT balanced
+        sizes = np.array([rng.randint(2, 5000) for _ in range(40)], dtype=np.uint64)
+        own = assign_owners(sizes, world)
+        owns = [None] * world
+        dist.all_gather_object(owns, own.tolist())
+        load = [int(sizes[own == r].sum()) for r in range(world)]
+        ok_own = all(o == own.tolist() for o in owns) and max(load) - min(load) <= int(sizes.max())
+        # the compacted-gap exchange of nw.cu: variable lengths, padded all-gather
+        mygaps = np.arange(rank * 7, rank * 7 + 3 + rank, dtype=np.int64)
+        sz = [None] * world
+        dist.all_gather_object(sz, len(mygaps))
+        mx = max(sz)
+        pad = np.zeros(mx, dtype=np.int64)
+        pad[: len(mygaps)] = mygaps
+        gp = [torch.zeros(mx, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(gp, torch.from_numpy(pad))
+        ok_gaps = all(np.array_equal(gp[r].numpy()[: sz[r]], np.arange(r * 7, r * 7 + 3 + r)) for r in range(world))
+        q.put((rank, ok_plan, ok_lev, ok_own, ok_gaps))
     finally:
         dist.destroy_process_group()
 
@@ -76,18 +92,19 @@ def test_sharded_exchange_gloo(world):
         p.join(120)
     results = sorted(q.get(timeout=5) for _ in range(world))
     assert [r[0] for r in results] == list(range(world))
-    for rank, ok_lev, ok_owner, ok_sum, ok_uid in results:
-        assert ok_lev and ok_owner and ok_sum and ok_uid, (rank, ok_lev, ok_owner, ok_sum, ok_uid)
+    for rank, ok_plan, ok_lev, ok_own, ok_gaps in results:
+        assert ok_plan and ok_lev and ok_own and ok_gaps, (rank, ok_plan, ok_lev, ok_own, ok_gaps)
 
 
-def test_shard_range_matches_device_rule():
-    from paper_2601_15458_b200.dist import owner_of, shard_range
+def test_shard_bounds_balance_cost():
+    """dm_shard_bounds: contiguous, complete, each range ~1/w of the cost."""
+    from paper_2601_15458_b200.dist import shard_bounds
+    rng = np.random.default_rng(3)
     for n in (0, 1, 5, 101, 4950):
         for w in (1, 2, 3, 8):
-            covered = []
-            for r in range(w):
-                lo, hi = shard_range(n, r, w)
-                covered.extend(range(lo, hi))
-                for i in range(lo, hi):
-                    assert owner_of(i, n, w) == r
-            assert covered == list(range(n))
+            cost = rng.integers(1, 10**6, n).astype(np.uint64)
+            b = shard_bounds(cost, w)
+            assert b[0] == 0 and b[-1] == n and all(b[k] <= b[k + 1] for k in range(w))
+            if n >= 50 * w:
+                parts = [int(cost[b[k]:b[k + 1]].sum()) for k in range(w)]
+                assert max(parts) - min(parts) <= 2 * int(cost.max())
