@@ -1,6 +1,7 @@
 // extern "C" boundary of libdmb200.so (include/dm_b200.h). Maps internal
 // exceptions onto status codes + a thread-local message, so no C++ exception
 // ever crosses the ABI.
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -17,6 +18,13 @@ namespace dm {
 std::string& last_error() {
     thread_local std::string e;
     return e;
+}
+
+void trace_bytes(const char* kernel, uint64_t read, uint64_t written) {
+    static const bool on = std::getenv("DM_TRACE_BYTES") != nullptr;
+    if (on)
+        std::fprintf(stderr, "[dm bytes] %s %llu %llu\n", kernel, (unsigned long long)read,
+                     (unsigned long long)written);
 }
 
 int occupancy(const void* kern, int threads, size_t smem) {

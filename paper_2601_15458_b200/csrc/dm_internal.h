@@ -212,6 +212,11 @@ struct dm_msa_out {
 
 namespace dm {
 
+// DM_TRACE_BYTES=1: one stderr line per launch of the memory-bound passes
+// with its algorithmic bytes (read, written), matched against ncu's DRAM
+// bytes by tools/prof_mem.py.
+void trace_bytes(const char* kernel, uint64_t read, uint64_t written);
+
 // Resident blocks per SM of `kern` at (threads, dynamic smem) on the current
 // device, cached per (kernel, device, threads, smem) and thread-safe; opts the
 // kernel into more than 48 KB of dynamic shared memory on that device when

@@ -182,6 +182,11 @@ std::string format_on_device(dm_ctx* ctx, const uint8_t* d_res, const std::vecto
     fasta_format_kernel<<<grid, 256, 0, ctx->stream>>>(d_res, d_hdr, d_recs, n, d_out);
     DM_CUDA(cudaGetLastError());
     ++ctx->launches;
+    {
+        uint64_t rd = hdrs.size() + n * sizeof(FmtRec);
+        for (uint64_t k = 0; k < n; ++k) rd += len[k];
+        trace_bytes("fasta_format_kernel", rd, total);
+    }
     download_host(ctx, text.data(), d_out, total, ctx->stream);
     DM_CUDA(cudaStreamSynchronize(ctx->stream));
     return text;

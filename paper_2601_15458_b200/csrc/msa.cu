@@ -131,6 +131,16 @@ void apply_sides(dm_ctx* ctx, std::vector<SideDesc>& sides, const uint32_t* d_ga
     DM_CUDA(cudaMemcpyAsync(d_prefix, prefix.data(), prefix.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
     colmap_kernel<<<(unsigned)sides.size(), 256, 0, ctx->stream>>>(d_sides, d_gaps, d_maps);
     DM_CUDA(cudaGetLastError());
+    {
+        uint64_t g = 0, rd = 0, wr = 0;
+        for (const SideDesc& d : sides) {
+            g += d.ngaps;
+            rd += (uint64_t)(d.r1 - d.r0) * d.w_old;
+            wr += (uint64_t)(d.r1 - d.r0) * d.w_new;
+        }
+        trace_bytes("colmap_kernel", g * 4 * 2, mtot * 4);
+        trace_bytes("insert_rows_kernel", rd, wr);
+    }
     const uint32_t total = prefix.back();
     const size_t smem = std::max<uint64_t>(max_w_old, 16);
     if (smem > 48 * 1024)

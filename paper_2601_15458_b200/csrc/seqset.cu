@@ -372,6 +372,7 @@ dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets,
             census_kernel<<<std::max(grid, 1), 256, 0, st>>>(d_raw, nbytes,
                                                              reinterpret_cast<unsigned long long*>(d_present));
             DM_CUDA(cudaGetLastError());
+            trace_bytes("census_kernel", nbytes, 0);
         }
         unsigned int present[8];
         DM_CUDA(cudaMemcpyAsync(present, d_present, 32, cudaMemcpyDeviceToHost, st));
@@ -411,6 +412,7 @@ dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets,
             else
                 recode_kernel<<<grid, 256, 0, st>>>(d_raw, d_raw_off, s->d_off, n, d_lut, s->d_codes);
             DM_CUDA(cudaGetLastError());
+            trace_bytes(s->planes == 2 ? "recode2_kernel" : "recode_kernel", nbytes, o);
         }
         if (b) {
             const int grid = (int)std::min<uint64_t>((b + 255) / 256, (uint64_t)ctx->sm_count * 16);
@@ -421,6 +423,7 @@ dm_seqset* seqset_create(dm_ctx* ctx, const char* data, const uint64_t* offsets,
             else
                 planes_kernel<8><<<grid, 256, 0, st>>>(s->d_codes, s->d_off, s->d_len, s->d_blk, n, s->d_planes);
             DM_CUDA(cudaGetLastError());
+            trace_bytes("planes_kernel", o, b * s->planes * 8);
         }
         ctx->launches += 3;
         DM_CUDA(cudaStreamSynchronize(st));

@@ -522,6 +522,7 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
     while (!big.empty()) {
         const size_t B = big.size();
         const auto t0 = tnow();
+        const float k0 = tot.kernel_ms;
         // ---- phase 1: median candidates (host seeds) + all-pairs batch
         std::vector<uint64_t> mat_off(B), cand_off(B);
         std::vector<uint32_t> kk(B), cand, nb(B), ne(B);
@@ -565,11 +566,17 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
         uint32_t* d_ne = upload(ctx, sc.ne, ne);
 
         // ---- phases 2-4: sweeps from center, pole_l, pole_r
+        double sw_build = 0, sw_run = 0;
         auto sweep = [&](const std::vector<uint32_t>& from, uint32_t* d_dist) {
+            const auto a0 = tnow();
             items.clear();
             for (size_t v = 0; v < B; ++v)
                 for (uint32_t p = nb[v]; p < ne[v]; ++p) items.push_back(LevItem{from[v], order[p], p});
+            const auto a1 = tnow();
             lev_run_host_items(ctx, s, items, d_dist, &tot, timing, owned);
+            const auto a2 = tnow();
+            sw_build += ms(a0, a1);
+            sw_run += ms(a1, a2);
         };
         uint32_t* d_max = sc.res2.as<uint32_t>(B);
         uint32_t* d_arg = sc.res3.as<uint32_t>(B);
@@ -629,8 +636,11 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
             const auto t5 = tnow();
             uint64_t mem = 0;
             for (size_t v = 0; v < B; ++v) mem += ne[v] - nb[v];
-            std::fprintf(stderr, "[dm tree] level %d big %zu members %llu median %.3f ms sweeps %.3f ms total %.3f ms\n",
-                         level, B, (unsigned long long)mem, ms(t0, t_med), ms(t_med, t5), ms(t0, t5));
+            std::fprintf(stderr,
+                         "[dm tree] level %d big %zu members %llu median %.3f ms sweeps %.3f ms (items %.3f, distance "
+                         "batches %.3f) total %.3f ms, distance kernels %.3f ms\n",
+                         level, B, (unsigned long long)mem, ms(t0, t_med), ms(t_med, t5), sw_build, sw_run, ms(t0, t5),
+                         tot.kernel_ms - k0);
         }
         ++level;
         big.swap(next);
