@@ -112,11 +112,13 @@ struct dm_ctx {
     dm::DevBuf lev_long_off, lev_long_h;
     dm::PinnedBuf pin_long;
     cudaStream_t copy_stream = nullptr;  // host->device staging of streamed batches
-    static constexpr int kStreamSlots = 4;  // chunks of a streamed batch in flight
+    static constexpr int kStreamSlots = 6;  // chunks of a streamed batch in flight
     dm::DevBuf stage[kStreamSlots], stream_pairs, stream_out, stream_offs, stream_flags;
     dm::DevBuf stage_packed[kStreamSlots];  // 2-bit nucleotide chunks as uploaded
     dm::DevBuf ss_meta, ss_codes, ss_planes;  // planner contexts: the chunk's sequence set (reused)
     dm::PinnedBuf pin_pack[kStreamSlots];   // host side of the same
+    dm::DevBuf stage_plan[kStreamSlots];    // host-planned chunks: counters, sorted items, lengths, offsets
+    dm::PinnedBuf pin_plan[kStreamSlots];
     dm_ctx* prep[kStreamSlots] = {};  // planner contexts of the streamed path (own stream + scratch)
     // words per lane the lane count per pair is chosen for on this context
     // (0: the alphabet's maximum; patterns too long for it still use up to
@@ -154,6 +156,7 @@ private:
             b->sp = s;
         for (dm::DevBuf& b : stage) b.sp = s;
         for (dm::DevBuf& b : stage_packed) b.sp = s;
+        for (dm::DevBuf& b : stage_plan) b.sp = s;
     }
 };
 
@@ -258,6 +261,22 @@ void lev_plan_then_launch(dm_ctx* prep, dm_ctx* ctx, const dm_seqset* s, const u
                           const uint32_t* d_ib, uint64_t n, uint32_t* d_out, cudaEvent_t planned,
                           LevTotals* tot, const uint64_t* pair_offs = nullptr);
 // Pairs given as device arrays (bench path): builds items on the device.
+// Host-planned streamed chunks (stream.cu): pairs (2i, 2i+1) of `cnt`
+// sequences with host offsets offs[0..2cnt]; items get slots slot0 + i.
+// False when a pair needs the multi-pass bucket (the chunk then takes the
+// device-planned path). `tmp` is scratch.
+constexpr int kLevBuckets = 6 * 32;
+constexpr int kLevSrcCodes = 1, kLevSrcRaw = 2;  // = kSrcCodes, kSrcRaw (lev_kernel.cuh)
+bool lev_plan_host_pairs(const uint64_t* offs, uint64_t cnt, uint64_t slot0, int sm_count, int wsel_cap,
+                         LevItem* items, unsigned int* hist, unsigned long long* cells, std::vector<uint32_t>& tmp);
+// Launches a host-planned chunk (items + zeroed per-bucket counters already
+// on the device) after `after`; src: 1 = 2-bit codes, 2 = raw A/C/G/T bytes.
+int lev_launch_host_planned(dm_ctx* ctx, const LevItem* d_items, uint32_t* d_counters, const unsigned int* hist,
+                            int src, const uint8_t* d_codes, const uint64_t* d_off, const uint32_t* d_len,
+                            uint32_t* d_out, cudaEvent_t after);
+struct LevArgs;
+void lev_launch_bucket_src(int src, int w, const LevArgs& a, int sm_count, cudaStream_t st);
+void lev_warm_src();
 void lev_run_device_pairs(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia,
                           const uint32_t* d_ib, uint64_t n, uint32_t* d_out, LevTotals* tot,
                           bool time_kernels);

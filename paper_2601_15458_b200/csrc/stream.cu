@@ -217,24 +217,26 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
     struct Handoff {
         std::mutex mu;
         std::condition_variable cv;
-        uint64_t issued = 0, launched = 0;
+        uint64_t issued = 0, launched = 0, planned = 0;
         bool abort = false;
         std::exception_ptr err;
     } hs;
-    std::thread packer;
+    std::thread packer, planner;
     auto stop_packer = [&] {
-        if (!packer.joinable()) return;
+        if (!packer.joinable() && !planner.joinable()) return;
         {
             std::lock_guard<std::mutex> g(hs.mu);
             hs.abort = true;
         }
         hs.cv.notify_all();
-        packer.join();
+        if (packer.joinable()) packer.join();
+        if (planner.joinable()) planner.join();
     };
     try {
         // every buffer the side streams touch is (re)allocated on ctx->stream first
         uint8_t* stage[NB];
-        for (int b = 0; b < NB; ++b) stage[b] = (uint8_t*)ctx->stage[b].get(maxbytes + 16);
+        // +64: the raw-byte kernels read whole aligned words past a sequence's end
+        for (int b = 0; b < NB; ++b) stage[b] = (uint8_t*)ctx->stage[b].get(maxbytes + 64);
         uint64_t* d_offs = ctx->stream_offs.as<uint64_t>(NB * oslot);
         uint64_t* h_offs = ctx->pin_items.as<uint64_t>(NB * oslot);
         uint32_t* d_ab = ctx->stream_pairs.as<uint32_t>(2 * per + 2);
@@ -265,6 +267,88 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
             }
         } evg{h2d_done};
         uint64_t h2d_bytes = 0;
+        // Host-planned chunks (packed or speculative, all pairs within one
+        // pass): the host orients, buckets and sorts the pairs and lays out
+        // the chunk's per-sequence offsets and lengths; the plan goes up on the
+        // copy stream just before the chunk's residues, and the chunk's
+        // kernels (2-bit code / raw byte sources) wait only for the upload --
+        // no planner kernels, no host sync. Plan slot layout: per-bucket
+        // counters (zero) | items | lengths | offsets.
+        constexpr uint64_t kPlanHead = 1024;
+        static_assert(kLevBuckets * 4 <= kPlanHead, "plan header");
+        auto plan_layout = [](uint64_t cnt, uint64_t& len_at, uint64_t& off_at) {
+            len_at = kPlanHead + cnt * sizeof(LevItem);
+            off_at = len_at + ((2 * cnt * 4 + 7) & ~uint64_t(7));
+            return off_at + 2 * cnt * 8;
+        };
+        uint64_t l_at = 0, o_at = 0;
+        const uint64_t plan_cap = plan_layout(per, l_at, o_at);
+        uint8_t* d_plan[NB];
+        uint8_t* h_plan[NB];
+        for (int b = 0; b < NB; ++b) {
+            d_plan[b] = (uint8_t*)ctx->stage_plan[b].get(plan_cap);
+            h_plan[b] = (uint8_t*)ctx->pin_plan[b].get(plan_cap);
+        }
+        const bool host_plan = [] {
+            const char* e = std::getenv("DM_STREAM_HOSTPLAN");
+            return !(e && e[0] == '0');
+        }();
+        const int hwsel = [] {
+            const char* e = std::getenv("DM_STREAM_HWSEL");
+            return e ? std::max(1, std::atoi(e)) : 16;
+        }();
+        std::vector<char> hp_ok(nchunks, 0);
+        std::vector<uint64_t> hp_bytes(nchunks, 0);
+        std::vector<unsigned int> hp_hist(nchunks * kLevBuckets);
+        std::vector<unsigned long long> hp_cells(2 * nchunks);
+        std::vector<uint32_t> hp_tmp;
+        cudaEvent_t plan_up[NB] = {};  // slot's pinned plan read by the copy engine
+        for (int b = 0; b < NB; ++b) DM_CUDA(cudaEventCreateWithFlags(&plan_up[b], cudaEventDisableTiming));
+        EvGuard evp{plan_up};
+        auto plan_chunk = [&](uint64_t p) {  // planner thread, ahead of the packer
+            const int b = (int)(p % NB);
+            if (p >= NB) {  // chunk p - NB's plan has gone up from this slot
+                {
+                    std::unique_lock<std::mutex> g(hs.mu);
+                    hs.cv.wait(g, [&] { return hs.abort || hs.issued > p - NB; });
+                    if (hs.abort) return false;
+                }
+                DM_CUDA(cudaEventSynchronize(plan_up[b]));
+            }
+            const uint64_t lo = cb[p], hi = cb[p + 1], cnt = hi - lo;
+            if (host_plan && (spec[p] || pack) && cnt > 0) {
+                uint8_t* hb = h_plan[b];
+                uint64_t la = 0, oa = 0;
+                const uint64_t bytes = plan_layout(cnt, la, oa);
+                std::memset(hb, 0, kPlanHead);
+                if (lev_plan_host_pairs(offsets + 2 * lo, cnt, lo, ctx->sm_count, hwsel,
+                                        reinterpret_cast<LevItem*>(hb + kPlanHead), &hp_hist[p * kLevBuckets],
+                                        &hp_cells[2 * p], hp_tmp)) {
+                    uint32_t* ln = reinterpret_cast<uint32_t*>(hb + la);
+                    uint64_t* of = reinterpret_cast<uint64_t*>(hb + oa);
+                    const uint64_t* o = offsets + 2 * lo;
+                    uint64_t at = 0;
+                    for (uint64_t k = 0; k < 2 * cnt; ++k) {
+                        const uint64_t L = o[k + 1] - o[k];
+                        ln[k] = (uint32_t)L;
+                        if (spec[p]) {
+                            of[k] = o[k] - o[0];  // raw bytes as uploaded
+                        } else {
+                            of[k] = at;  // host_pack.cpp's 2-bit layout
+                            at += code_bytes(L, 2);
+                        }
+                    }
+                    hp_ok[p] = 1;
+                    hp_bytes[p] = bytes;
+                }
+            }
+            {
+                std::lock_guard<std::mutex> g(hs.mu);
+                hs.planned = p + 1;
+            }
+            hs.cv.notify_all();
+            return true;
+        };
         // Chunk kinds (set before issued > c): kPacked — packed on the host,
         // the upload is its code buffer; kSpec — uploaded raw from the
         // caller's pinned buffer and planned as A/C/G/T, verified on the
@@ -286,6 +370,7 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
                 if (hs.abort) return false;
                 DM_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ev.done[b], 0));
             }
+
             DM_CUDA(cudaMemcpyAsync(d_offs + b * oslot, h_offs + b * oslot, (2 * (hi - lo) + 1) * 8,
                                     cudaMemcpyHostToDevice, ctx->copy_stream));
             h2d_bytes += (2 * (hi - lo) + 1) * 8;
@@ -307,6 +392,16 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
                 h2d_bytes += n;
             }
             DM_CUDA(cudaEventRecord(h2d_done[b], ctx->copy_stream));
+            {  // chunk c's host plan goes up behind its residues (the main thread plans ahead)
+                std::unique_lock<std::mutex> g(hs.mu);
+                hs.cv.wait(g, [&] { return hs.abort || hs.planned > c; });
+                if (hs.abort) return false;
+            }
+            if (hp_ok[c]) {
+                DM_CUDA(cudaMemcpyAsync(d_plan[b], h_plan[b], hp_bytes[c], cudaMemcpyHostToDevice, ctx->copy_stream));
+                h2d_bytes += hp_bytes[c];
+            }
+            DM_CUDA(cudaEventRecord(plan_up[b], ctx->copy_stream));
             if (trace) {
                 cudaEvent_t e;
                 cudaEventCreate(&e);
@@ -322,6 +417,18 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
             }
             return true;
         };
+        planner = std::thread([&] {
+            try {
+                DM_CUDA(cudaSetDevice(ctx->device));
+                for (uint64_t p = 0; p < nchunks; ++p)
+                    if (!plan_chunk(p)) return;
+            } catch (...) {
+                std::lock_guard<std::mutex> g(hs.mu);
+                if (!hs.err) hs.err = std::current_exception();
+                hs.abort = true;
+            }
+            hs.cv.notify_all();
+        });
         packer = std::thread([&] {
             try {
                 DM_CUDA(cudaSetDevice(ctx->device));
@@ -335,7 +442,7 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
                 }
             } catch (...) {
                 std::lock_guard<std::mutex> g(hs.mu);
-                hs.err = std::current_exception();
+                if (!hs.err) hs.err = std::current_exception();
                 hs.abort = true;
             }
             hs.cv.notify_all();
@@ -349,6 +456,49 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
                 hs.cv.wait(g, [&] { return hs.abort || hs.issued > c; });
                 if (hs.err) std::rethrow_exception(hs.err);
                 if (hs.issued <= c) throw cuda_error("streamed upload stopped");
+            }
+            if (kind[c] != kRaw && hp_ok[c]) {
+                // host-planned: the kernels wait for the upload alone
+                const double t0 = trace ? now_ms() : 0.0;
+                uint64_t la = 0, oa = 0;
+                plan_layout(cnt, la, oa);
+                if (kind[c] == kSpec) {  // the A/C/G/T assumption, checked on the device
+                    DM_CUDA(cudaStreamWaitEvent(P->stream, ev.copied[b], 0));
+                    const uint64_t nb = offsets[2 * hi] - offsets[2 * lo];
+                    const int vg = (int)std::min<uint64_t>((nb + 4095) / 4096 + 1, (uint64_t)ctx->sm_count * 8);
+                    verify_acgt_kernel<<<vg, 256, 0, P->stream>>>(stage[b], nb, d_flags + c);
+                    DM_CUDA(cudaGetLastError());
+                    DM_CUDA(cudaEventRecord(ev.planned[b], P->stream));
+                }
+                const int nl = lev_launch_host_planned(
+                    ctx, reinterpret_cast<const LevItem*>(d_plan[b] + kPlanHead), reinterpret_cast<uint32_t*>(d_plan[b]),
+                    &hp_hist[c * kLevBuckets], kind[c] == kPacked ? kLevSrcCodes : kLevSrcRaw,
+                    kind[c] == kPacked ? d_pack[b] : stage[b], reinterpret_cast<const uint64_t*>(d_plan[b] + oa),
+                    reinterpret_cast<const uint32_t*>(d_plan[b] + la), d_res, ev.copied[b]);
+                // the slot's buffers are reused once its kernels (and check) are done
+                if (kind[c] == kSpec) DM_CUDA(cudaStreamWaitEvent(ctx->stream, ev.planned[b], 0));
+                DM_CUDA(cudaEventRecord(ev.done[b], ctx->stream));
+                if (tot) {
+                    tot->cells += hp_cells[2 * c];
+                    tot->cells_exec += hp_cells[2 * c + 1];
+                    tot->launches += nl + (kind[c] == kSpec ? 1 : 0);
+                }
+                {
+                    std::lock_guard<std::mutex> g(hs.mu);
+                    hs.launched = c + 1;
+                }
+                hs.cv.notify_all();
+                if (trace) {
+                    cudaEvent_t a, k;
+                    cudaEventCreate(&a);
+                    cudaEventCreate(&k);
+                    cudaEventRecord(a, ctx->copy_stream);
+                    cudaEventRecord(k, ctx->stream);
+                    tl.push_back({a, k});
+                    std::fprintf(stderr, "[stream] chunk %llu pairs %llu: host-planned kind %d, launched %.2f..%.2f ms\n",
+                                 (unsigned long long)c, (unsigned long long)cnt, (int)kind[c], t0, now_ms());
+                }
+                continue;
             }
             DM_CUDA(cudaStreamWaitEvent(P->stream, ev.copied[b], 0));
             if (c >= NB) DM_CUDA(cudaStreamWaitEvent(P->stream, ev.done[b], 0));  // chunk c-NB's kernels
@@ -388,6 +538,7 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
                              (unsigned long long)c, (unsigned long long)cnt, t0, t1, now_ms());
         }
         packer.join();
+        planner.join();
         if (hs.err) std::rethrow_exception(hs.err);
         DM_CUDA(cudaMemcpyAsync(h_res, d_res, npairs * 4, cudaMemcpyDeviceToHost, ctx->stream));
         std::vector<uint32_t> flags(nchunks);

@@ -281,8 +281,14 @@ def test_packed_upload_matches_raw_upload(dm, ctx, orc, monkeypatch, chunk):
     monkeypatch.delenv("DM_STREAM_PACK")
     monkeypatch.setenv("DM_STREAM_RAW_FRAC", "0")
     assert np.array_equal(split, raw) and np.array_equal(full, raw)
-    # the host-counted bucket histogram (fully packed chunks) == the device one
-    assert (sf["cells"], sf["cells_executed"], sf["launches"]) == (sr["cells"], sr["cells_executed"], sr["launches"])
+    # the host plan of packed chunks (bucket histogram, cells) == the device planner's
+    assert (sf["cells"], sf["cells_executed"]) == (sr["cells"], sr["cells_executed"])
+    monkeypatch.setenv("DM_STREAM_HOSTPLAN", "0")
+    dev_planned, sdp = dm.lev_pairs_packed(data, offs, ctx, stats=True)
+    monkeypatch.delenv("DM_STREAM_HOSTPLAN")
+    assert np.array_equal(dev_planned, raw)
+    assert (sdp["cells"], sdp["cells_executed"], sdp["launches"]) == (sr["cells"], sr["cells_executed"], sr["launches"])
+    assert sf["launches"] < sr["launches"]  # no planner kernels on host-planned chunks
     assert sr["h2d_bytes"] >= len(data) + 8 * (len(offs) - 1)
     assert sf["h2d_bytes"] < 0.3 * len(data) + 8 * len(offs) + 64 * 1000
     assert sf["h2d_bytes"] < sp["h2d_bytes"] < sr["h2d_bytes"]
@@ -324,3 +330,40 @@ def test_packed_upload_odd_lengths(dm, ctx, orc, monkeypatch, n, alphabet, frac)
     offs[1:] = np.cumsum([len(x) for x in seqs])
     got = dm.lev_pairs_packed(data, offs, ctx)
     assert list(got) == [orc.levenshtein(seqs[2 * i], seqs[2 * i + 1]) for i in range(6)]
+
+
+@pytest.mark.parametrize("frac", ["0", "1"])
+@pytest.mark.parametrize("gpar", ["0", "2", "5"])
+def test_host_planned_chunks_every_bucket(dm, ctx, ref, monkeypatch, frac, gpar):
+    """Host-planned streamed chunks (patterns from 2-bit codes or from the raw
+    A/C/G/T bytes at any alignment, texts likewise) over every (G, W)
+    bucket: patterns of 1..48 words and up to 768 words, odd lengths, empty
+    sequences; one chunk longer than one warp's rows (multi-pass) falls back
+    to the device-planned path. Pinned buffer, so frac=1 sends every chunk
+    raw; compared with the compiled reference."""
+    import torch
+    monkeypatch.setenv("DM_LEV_GPAR", gpar)
+    monkeypatch.setenv("DM_STREAM_RAW_FRAC", frac)
+    monkeypatch.setenv("DM_STREAM_CHUNK_BYTES", "60000")
+    rng = random.Random(int(gpar) * 10 + len(frac))
+    seqs = []
+    words = list(range(1, 25)) + list(range(33, 49)) + [64, 96, 128, 192, 256, 384, 768]
+    for B in words:
+        for delta in (-17, -1, 0, 3):
+            la = max(1, 32 * B + delta)
+            a = rand_str(rng, la, "ACGT")
+            b = list(a)
+            for _ in range(max(1, la // 12)):
+                b[rng.randrange(len(b))] = rng.choice("ACGT")
+            b = "".join(b[:max(1, la - rng.randint(0, 50))]) + rand_str(rng, rng.randint(0, 50), "ACGT")
+            seqs += [a, b] if rng.random() < 0.5 else [b, a]
+    seqs += ["", "ACGT", "", ""]
+    seqs += [rand_str(rng, 25000, "ACGT"), rand_str(rng, 26000, "ACGT")]  # > 24,576 rows: multi-pass
+    data = "".join(seqs).encode()
+    offs = np.zeros(len(seqs) + 1, dtype=np.uint64)
+    offs[1:] = np.cumsum([len(x) for x in seqs])
+    pinned = torch.frombuffer(bytearray(data), dtype=torch.uint8).pin_memory()
+    got = dm.lev_pairs_packed(pinned, offs, ctx)
+    n = len(seqs) // 2
+    want = ref.lev_pairs(seqs, list(range(0, 2 * n, 2)), list(range(1, 2 * n, 2)))
+    assert np.array_equal(got, want)

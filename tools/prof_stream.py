@@ -14,6 +14,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--pageable", action="store_true", help="pass the Python bytes (pageable) instead of a pinned copy")
     a = ap.parse_args()
     import torch
     import paper_2601_15458_b200 as dm
@@ -32,10 +33,11 @@ def main():
     print(f"pinned H2D {nbytes / dt / 1e9:.1f} GB/s ({dt * 1e3:.1f} ms for {nbytes / 1e9:.2f} GB)")
     del dev
     ctx = dm.default_context(0)
-    dm.lev_pairs_packed(pinned, offs, ctx)
+    src = data if a.pageable else pinned
+    dm.lev_pairs_packed(src, offs, ctx)
     for _ in range(a.reps):
         t = time.perf_counter()
-        _, st = dm.lev_pairs_packed(pinned, offs, ctx, stats=True)
+        _, st = dm.lev_pairs_packed(src, offs, ctx, stats=True)
         dt = time.perf_counter() - t
         print(f"packed: {dt * 1e3:.1f} ms wall, {st['total_ms']:.1f} ms stream, "
               f"{st['cells'] / dt / 1e9:.0f} GCUPS e2e")
