@@ -277,6 +277,10 @@ int lev_launch_host_planned(dm_ctx* ctx, const LevItem* d_items, uint32_t* d_cou
 struct LevArgs;
 void lev_launch_bucket_src(int src, int w, const LevArgs& a, int sm_count, cudaStream_t st);
 void lev_warm_src();
+// Jobs already on the device (one rank: no sharding), e.g. generated by the
+// tree builder's item kernels.
+void lev_run_device_items(dm_ctx* ctx, const dm_seqset* s, const LevItem* d_items, uint64_t n, uint32_t* d_out,
+                          LevTotals* tot, bool time_kernels);
 void lev_run_device_pairs(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia,
                           const uint32_t* d_ib, uint64_t n, uint32_t* d_out, LevTotals* tot,
                           bool time_kernels);

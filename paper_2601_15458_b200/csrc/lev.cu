@@ -487,6 +487,11 @@ void lev_run_host_items(dm_ctx* ctx, const dm_seqset* s, std::vector<LevItem>& i
     ctx->launches += 1;
 }
 
+void lev_run_device_items(dm_ctx* ctx, const dm_seqset* s, const LevItem* d_items, uint64_t n, uint32_t* d_out,
+                          LevTotals* tot, bool time_kernels) {
+    run_planned(ctx, s, nullptr, nullptr, d_items, n, d_out, tot, time_kernels);
+}
+
 void lev_run_device_pairs(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia,
                           const uint32_t* d_ib, uint64_t n, uint32_t* d_out, LevTotals* tot,
                           bool time_kernels) {

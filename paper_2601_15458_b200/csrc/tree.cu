@@ -336,6 +336,34 @@ __global__ void __launch_bounds__(128) subtree_kernel(
     for (uint32_t t = threadIdx.x; t < k; t += blockDim.x) order[base + t] = ids[ord[t]];
 }
 
+// ------------------------------------------------------------ distance jobs on the device
+// All-pairs jobs (i < j) of each node's member list src[src_off[v] .. + k[v]),
+// result slot mat_off[v] + i k + j; node v's jobs start at item_off[v],
+// row i at i (2k - i - 1) / 2 -- the order the host loops produced.
+__global__ void pair_items_kernel(const uint32_t* __restrict__ src, const uint64_t* __restrict__ src_off,
+                                  const uint32_t* __restrict__ kk, const uint64_t* __restrict__ mat_off,
+                                  const uint64_t* __restrict__ item_off, LevItem* __restrict__ items) {
+    const uint32_t v = blockIdx.x, k = kk[v];
+    const uint32_t* c = src + src_off[v];
+    const uint64_t mo = mat_off[v];
+    for (uint32_t i = 0; i + 1 < k; ++i) {
+        LevItem* row = items + item_off[v] + (uint64_t)i * (2ull * k - i - 1) / 2 - (i + 1);
+        const uint32_t ci = c[i];
+        for (uint32_t j = i + 1 + threadIdx.x; j < k; j += blockDim.x)
+            row[j] = LevItem{ci, c[j], mo + (uint64_t)i * k + j};
+    }
+}
+
+// Sweep jobs: from[v] against every member of node v's slice of `order`,
+// result slot = the member's position (cluster_tree.cpp:31-41).
+__global__ void sweep_items_kernel(const uint32_t* __restrict__ from, const uint32_t* __restrict__ order,
+                                   const uint32_t* __restrict__ nb, const uint32_t* __restrict__ ne,
+                                   const uint64_t* __restrict__ item_off, LevItem* __restrict__ items) {
+    const uint32_t v = blockIdx.x, f = from[v], b = nb[v];
+    LevItem* out = items + item_off[v] - b;
+    for (uint32_t p = b + threadIdx.x; p < ne[v]; p += blockDim.x) out[p] = LevItem{f, order[p], p};
+}
+
 // ------------------------------------------------------------ host side
 struct PNode {
     uint32_t begin = 0, end = 0, center = kNo, radius = 0, pole_l = kNo, pole_r = kNo;
@@ -356,11 +384,12 @@ void download(dm_ctx* ctx, std::vector<T>& v, const T* d, size_t n) {
 }
 
 struct TreeScratch {
-    DevBuf order, tmp, dc, dl, dr, mat, matoff, kk, cand, candoff, nb, ne, res1, res2, res3, sub_begin, sub_k,
-        sub_mat, sub_matoff, sub_recoff, sub_recs, err;
+    DevBuf order, tmp, dc, dl, dr, mat, matoff, kk, cand, candoff, nb, ne, res1, res2, res3, res4, res5, res6, sub_begin,
+        sub_k, sub_mat, sub_matoff, sub_recoff, sub_recs, err, items, itemoff;
     explicit TreeScratch(cudaStream_t* s) {
         for (DevBuf* b : {&order, &tmp, &dc, &dl, &dr, &mat, &matoff, &kk, &cand, &candoff, &nb, &ne, &res1, &res2,
-                          &res3, &sub_begin, &sub_k, &sub_mat, &sub_matoff, &sub_recoff, &sub_recs, &err})
+                          &res3, &res4, &res5, &res6, &sub_begin, &sub_k, &sub_mat, &sub_matoff, &sub_recoff, &sub_recs, &err,
+                          &items, &itemoff})
             b->sp = s;
     }
 };
@@ -523,10 +552,15 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
         const size_t B = big.size();
         const auto t0 = tnow();
         const float k0 = tot.kernel_ms;
+        // One rank (or an owned subtree): the jobs of every batch are generated
+        // on the device from the candidate lists / node slices and the level's
+        // decisions stay there until one download at the end of the level.
+        // Several ranks sharing the level: host job lists, sharded by cost.
+        const bool dev = owned || shard_world(ctx) == 1;
         // ---- phase 1: median candidates (host seeds) + all-pairs batch
-        std::vector<uint64_t> mat_off(B), cand_off(B);
+        std::vector<uint64_t> mat_off(B), cand_off(B), item_off(B);
         std::vector<uint32_t> kk(B), cand, nb(B), ne(B);
-        uint64_t mtot = 0;
+        uint64_t mtot = 0, itot = 0;
         items.clear();
         for (size_t v = 0; v < B; ++v) {
             const PNode& nd = pool[big[v]];
@@ -545,30 +579,63 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
             const uint32_t k = (uint32_t)(cand.size() - cand_off[v]);
             kk[v] = k;
             mat_off[v] = mtot;
-            const uint32_t* c = cand.data() + cand_off[v];
-            for (uint32_t i = 0; i < k; ++i)
-                for (uint32_t j = i + 1; j < k; ++j)
-                    items.push_back(LevItem{c[i], c[j], mtot + (uint64_t)i * k + j});
+            item_off[v] = itot;
+            itot += (uint64_t)k * (k - 1) / 2;
+            if (!dev) {
+                const uint32_t* c = cand.data() + cand_off[v];
+                for (uint32_t i = 0; i < k; ++i)
+                    for (uint32_t j = i + 1; j < k; ++j)
+                        items.push_back(LevItem{c[i], c[j], mtot + (uint64_t)i * k + j});
+            }
             mtot += (uint64_t)k * k;
         }
         uint32_t* d_mat = sc.mat.as<uint32_t>(mtot);
-        lev_run_host_items(ctx, s, items, d_mat, &tot, timing, owned);
+        const uint32_t* d_cand = upload(ctx, sc.cand, cand);
+        const uint64_t* d_candoff = upload(ctx, sc.candoff, cand_off);
+        const uint32_t* d_kk = upload(ctx, sc.kk, kk);
+        const uint64_t* d_matoff = upload(ctx, sc.matoff, mat_off);
+        if (dev) {
+            LevItem* d_items = sc.items.as<LevItem>(std::max<uint64_t>(itot, 1));
+            pair_items_kernel<<<(unsigned)B, 128, 0, stream>>>(d_cand, d_candoff, d_kk, d_matoff,
+                                                               upload(ctx, sc.itemoff, item_off), d_items);
+            DM_CUDA(cudaGetLastError());
+            lev_run_device_items(ctx, s, d_items, itot, d_mat, &tot, timing);
+        } else {
+            lev_run_host_items(ctx, s, items, d_mat, &tot, timing, owned);
+        }
         const auto t_med = tnow();
         uint32_t* d_center = sc.res1.as<uint32_t>(B);
-        median_argmin_kernel<<<(unsigned)B, 128, 0, stream>>>(
-            d_mat, upload(ctx, sc.matoff, mat_off), upload(ctx, sc.kk, kk), upload(ctx, sc.cand, cand),
-            upload(ctx, sc.candoff, cand_off), d_center);
+        median_argmin_kernel<<<(unsigned)B, 128, 0, stream>>>(d_mat, d_matoff, d_kk, d_cand, d_candoff, d_center);
         DM_CUDA(cudaGetLastError());
         std::vector<uint32_t> center, radius, pole_l, pole_r, mids;
-        download(ctx, center, d_center, B);
-        DM_CUDA(cudaStreamSynchronize(stream));
+        if (!dev) {
+            download(ctx, center, d_center, B);
+            DM_CUDA(cudaStreamSynchronize(stream));
+        }
         uint32_t* d_nb = upload(ctx, sc.nb, nb);
         uint32_t* d_ne = upload(ctx, sc.ne, ne);
+        std::vector<uint64_t> sweep_off(B);
+        uint64_t nsweep = 0;
+        for (size_t v = 0; v < B; ++v) {
+            sweep_off[v] = nsweep;
+            nsweep += ne[v] - nb[v];
+        }
+        const uint64_t* d_sweepoff = dev ? upload(ctx, sc.itemoff, sweep_off) : nullptr;
 
         // ---- phases 2-4: sweeps from center, pole_l, pole_r
         double sw_build = 0, sw_run = 0;
-        auto sweep = [&](const std::vector<uint32_t>& from, uint32_t* d_dist) {
+        auto sweep = [&](const uint32_t* d_from, const std::vector<uint32_t>& from, uint32_t* d_dist) {
             const auto a0 = tnow();
+            if (dev) {
+                LevItem* d_items = sc.items.as<LevItem>(std::max<uint64_t>(nsweep, 1));
+                sweep_items_kernel<<<(unsigned)B, 256, 0, stream>>>(d_from, d_order, d_nb, d_ne, d_sweepoff, d_items);
+                DM_CUDA(cudaGetLastError());
+                const auto a1 = tnow();
+                lev_run_device_items(ctx, s, d_items, nsweep, d_dist, &tot, timing);
+                sw_build += ms(a0, a1);
+                sw_run += ms(a1, tnow());
+                return;
+            }
             items.clear();
             for (size_t v = 0; v < B; ++v)
                 for (uint32_t p = nb[v]; p < ne[v]; ++p) items.push_back(LevItem{from[v], order[p], p});
@@ -579,34 +646,56 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
             sw_run += ms(a1, a2);
         };
         uint32_t* d_max = sc.res2.as<uint32_t>(B);
-        uint32_t* d_arg = sc.res3.as<uint32_t>(B);
-        sweep(center, d_dc);
-        sweep_argmax_kernel<<<(unsigned)B, 256, 0, stream>>>(d_dc, d_order, d_nb, d_ne, d_max, d_arg);
+        uint32_t* d_pl = sc.res3.as<uint32_t>(B);
+        uint32_t* d_pr = sc.res4.as<uint32_t>(B);
+        uint32_t* d_max2 = sc.res6.as<uint32_t>(B);
+        sweep(d_center, center, d_dc);
+        sweep_argmax_kernel<<<(unsigned)B, 256, 0, stream>>>(d_dc, d_order, d_nb, d_ne, d_max, d_pl);
         DM_CUDA(cudaGetLastError());
-        download(ctx, radius, d_max, B);
-        download(ctx, pole_l, d_arg, B);
-        DM_CUDA(cudaStreamSynchronize(stream));
-        sweep(pole_l, d_dl);
-        sweep_argmax_kernel<<<(unsigned)B, 256, 0, stream>>>(d_dl, d_order, d_nb, d_ne, d_max, d_arg);
+        if (!dev) {
+            download(ctx, radius, d_max, B);
+            download(ctx, pole_l, d_pl, B);
+            DM_CUDA(cudaStreamSynchronize(stream));
+        }
+        sweep(d_pl, pole_l, d_dl);
+        sweep_argmax_kernel<<<(unsigned)B, 256, 0, stream>>>(d_dl, d_order, d_nb, d_ne, d_max2, d_pr);
         DM_CUDA(cudaGetLastError());
-        download(ctx, pole_r, d_arg, B);
+        auto dup_found = [&] {
+            bool dup = false;
+            for (size_t v = 0; v < B; ++v) dup = dup || pole_r[v] == pole_l[v];
+            return dup;
+        };
+        if (!dev) {
+            download(ctx, pole_r, d_pr, B);
+            DM_CUDA(cudaStreamSynchronize(stream));
+            if (dup_found()) {
+                if (!owned) throw runtime_error(kDedupMsg);
+                err_flag = 1;  // reported by every rank after the exchange
+                break;
+            }
+        }
+        // (one rank: with identical poles the last sweep and the partition are
+        // wasted work, the error is raised below before any node is made)
+        sweep(d_pr, pole_r, d_dr);
+        uint32_t* d_mid = sc.res5.as<uint32_t>(B);
+        partition_kernel<<<(unsigned)B, 256, 0, stream>>>(d_order, d_tmp, d_dl, d_dr, d_nb, d_ne, d_mid);
+        DM_CUDA(cudaGetLastError());
+        if (dev) {
+            download(ctx, center, d_center, B);
+            download(ctx, radius, d_max, B);
+            download(ctx, pole_l, d_pl, B);
+            download(ctx, pole_r, d_pr, B);
+        }
+        download(ctx, mids, d_mid, B);
+        DM_CUDA(cudaMemcpyAsync(order.data(), d_order, (size_t)n * 4, cudaMemcpyDeviceToHost, stream));
         DM_CUDA(cudaStreamSynchronize(stream));
-        bool dup = false;
-        for (size_t v = 0; v < B; ++v) dup = dup || pole_r[v] == pole_l[v];
-        if (dup) {
+        if (dev && dup_found()) {
             if (!owned) throw runtime_error(kDedupMsg);
             err_flag = 1;  // reported by every rank after the exchange
             break;
         }
-        sweep(pole_r, d_dr);
-        uint32_t* d_mid = sc.res1.as<uint32_t>(B);
-        partition_kernel<<<(unsigned)B, 256, 0, stream>>>(d_order, d_tmp, d_dl, d_dr, d_nb, d_ne, d_mid);
-        DM_CUDA(cudaGetLastError());
-        download(ctx, mids, d_mid, B);
-        DM_CUDA(cudaMemcpyAsync(order.data(), d_order, (size_t)n * 4, cudaMemcpyDeviceToHost, stream));
-        DM_CUDA(cudaStreamSynchronize(stream));
-        ctx->launches += 4;
-        tot.launches += 4;
+        ctx->launches += 4 + (dev ? 4 : 0);
+        tot.launches += 4 + (dev ? 4 : 0);
 
         // ---- children (cluster_tree.cpp:201-231)
         std::vector<uint32_t> next;
@@ -650,38 +739,55 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
     // ---- small subtrees: one all-pairs matrix each, resolved on the device
     if (!small.empty() && !err_flag) {
         const size_t S = small.size();
+        const bool dev = owned || shard_world(ctx) == 1;  // jobs generated on the device (see the level loop)
         std::vector<uint32_t> sb(S), sk(S);
-        std::vector<uint64_t> moff(S), roff(S);
-        uint64_t mtot = 0, rtot = 0;
+        std::vector<uint64_t> moff(S), roff(S), ioff(S), soff(S);
+        uint64_t mtot = 0, rtot = 0, itot = 0;
         items.clear();
         for (size_t r = 0; r < S; ++r) {
             const PNode& nd = pool[small[r]];
             const uint32_t k = nd.end - nd.begin;
             sb[r] = nd.begin;
+            soff[r] = nd.begin;
             sk[r] = k;
             moff[r] = mtot;
             roff[r] = rtot;
-            const uint32_t* mem = order.data() + nd.begin;
-            for (uint32_t i = 0; i < k; ++i)
-                for (uint32_t j = i + 1; j < k; ++j)
-                    items.push_back(LevItem{mem[i], mem[j], mtot + (uint64_t)i * k + j});
+            ioff[r] = itot;
+            itot += (uint64_t)k * (k - 1) / 2;
+            if (!dev) {
+                const uint32_t* mem = order.data() + nd.begin;
+                for (uint32_t i = 0; i < k; ++i)
+                    for (uint32_t j = i + 1; j < k; ++j)
+                        items.push_back(LevItem{mem[i], mem[j], mtot + (uint64_t)i * k + j});
+            }
             mtot += (uint64_t)k * k;
             rtot += 2ull * k - 1;
         }
         const auto s0 = tnow();
         uint32_t* d_mat = sc.sub_mat.as<uint32_t>(mtot);
-        lev_run_host_items(ctx, s, items, d_mat, &tot, timing, owned);
+        const uint32_t* d_sk = upload(ctx, sc.sub_k, sk);
+        const uint64_t* d_smatoff = upload(ctx, sc.sub_matoff, moff);
+        if (dev) {
+            LevItem* d_items = sc.items.as<LevItem>(std::max<uint64_t>(itot, 1));
+            pair_items_kernel<<<(unsigned)S, 128, 0, stream>>>(d_order, upload(ctx, sc.candoff, soff), d_sk, d_smatoff,
+                                                               upload(ctx, sc.itemoff, ioff), d_items);
+            DM_CUDA(cudaGetLastError());
+            lev_run_device_items(ctx, s, d_items, itot, d_mat, &tot, timing);
+            ctx->launches += 1;
+            tot.launches += 1;
+        } else {
+            lev_run_host_items(ctx, s, items, d_mat, &tot, timing, owned);
+        }
         const auto s1 = tnow();
         if (trace)
-            std::fprintf(stderr, "[dm tree] small subtrees %zu pairs %zu all-pairs %.3f ms\n", S, items.size(),
-                         ms(s0, s1));
+            std::fprintf(stderr, "[dm tree] small subtrees %zu pairs %llu all-pairs %.3f ms\n", S,
+                         (unsigned long long)itot, ms(s0, s1));
         SubRec* d_recs = sc.sub_recs.as<SubRec>(rtot);
         int* d_err = sc.err.as<int>(1);
         DM_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), stream));
         const size_t smem = (size_t)(T | 1u) * T * 4;
         DM_CUDA(cudaFuncSetAttribute(subtree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        subtree_kernel<<<(unsigned)S, 128, smem, stream>>>(d_order, upload(ctx, sc.sub_begin, sb),
-                                                           upload(ctx, sc.sub_k, sk), upload(ctx, sc.sub_matoff, moff),
+        subtree_kernel<<<(unsigned)S, 128, smem, stream>>>(d_order, upload(ctx, sc.sub_begin, sb), d_sk, d_smatoff,
                                                            d_mat, upload(ctx, sc.sub_recoff, roff), d_recs, d_err);
         DM_CUDA(cudaGetLastError());
         ctx->launches += 1;
