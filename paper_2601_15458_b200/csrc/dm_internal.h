@@ -315,7 +315,11 @@ void nw_warm();
 // align_all's ProgressFn (msa_merge.cpp:121-129): done = 1..nodes.size().
 dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node>& nodes,
                       const std::vector<uint32_t>& order, const NwScheme& sc, dm_stats* st,
-                      dm_progress_fn progress = nullptr, void* progress_user = nullptr);
+                      dm_progress_fn progress = nullptr, void* progress_user = nullptr, bool host_rows = true);
+// Rows sel[0..n) of the device row buffer `src` (pitch bytes per row), `width`
+// bytes each, gathered on the device and copied densely into host `out`.
+void gather_rows_to_host(dm_ctx* ctx, const uint8_t* src, uint64_t pitch, const uint32_t* sel, uint64_t n,
+                         uint64_t width, char* out);
 void insert_gap_columns(dm_ctx* ctx, const char* rows, uint64_t nrows, uint64_t width, const uint32_t* pos,
                         uint64_t npos, char* out);
 uint32_t geometric_median(dm_ctx* ctx, const dm_seqset* s, const uint32_t* members, uint64_t n,

@@ -285,7 +285,7 @@ int dm_run_align(dm_ctx* ctx, const char* input_path, const char* output_path, i
         }
         dm::AlignCore res = dm::align_core(ctx, data.data(), off.data(), (uint32_t)recs.size(), &ids, alphabet,
                                            gap_open, gap_extend, flat, custom_table, custom_has, seed, input_order,
-                                           st);
+                                           st, false);  // the formatter reads the device rows
         if (dump_dedup_path && *dump_dedup_path) {  // write_dedup_tsv (seq_io.cpp:227-249)
             std::string tsv;
             for (size_t r = 0; r < res.reps.size(); ++r)

@@ -84,13 +84,14 @@ __device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
 // instructions issued beats moving work off the ALU pipe here.
 // Two of its ops go to the FMA pipe (the kernel is ALU-bound, the FMA pipe
 // has room): word 0 = t0 * 2 + cin as an IMAD (the chain's own word 0 only
-// feeds the carry), and the bit shifted out = hi(t * 2) as an IMAD.HI.
+// feeds the carry), the bit shifted out = hi(t * 2) as an IMAD.HI, and the
+// top word's add (carry in, none out) as an IMAD.X (Chain::addm).
 template <int W>
-__device__ __forceinline__ uint32_t shl1(uint32_t (&v)[W], uint32_t cin, uint32_t two) {
+__device__ __forceinline__ uint32_t shl1(uint32_t (&v)[W], uint32_t cin, uint32_t two, uint32_t one) {
     uint32_t t[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) t[w] = v[w];
-    Chain<W>::add(v, t, t);
+    Chain<W>::addm(v, t, t, one);
     v[0] = imad(t[0], two, cin);
     return __umulhi(t[W - 1], two);
 }
@@ -287,7 +288,7 @@ __global__ void __launch_bounds__(256, NP == 2 ? (W <= 16 ? 3 : 2) : 1) lev_kern
                     X[w] = w == 0 ? lop3<0xA8>(e, hm, Pv[w]) : (e & Pv[w]);  // (e | hm) & Pv
                     if (w == 0) T0 = lop3<0xFE>(Pv[w], Xv[w], hm);
                 }
-                Chain<W>::add(S, X, Pv);
+                Chain<W>::addm(S, X, Pv, a.one);  // top word on the FMA pipe (IMAD.X)
 #pragma unroll
                 for (int w = 0; w < W; ++w) {
                     Mh[w] = lop3<0xBA>(Pv[w], S[w], X[w]);  // (Pv & ~S) | X
@@ -295,8 +296,8 @@ __global__ void __launch_bounds__(256, NP == 2 ? (W <= 16 ? 3 : 2) : 1) lev_kern
                     // terms are disjoint and the OR is an add -> FMA pipe
                     Ph[w] = w == 0 ? lop3<0xF1>(Mv[w], S[w], T0) : imad(lop3<0x01>(S[w], Pv[w], Xv[w]), a.one, Mv[w]);
                 }
-                const uint32_t hpo = shl1<W>(Ph, hp, two);
-                const uint32_t hmo = shl1<W>(Mh, hm, two);
+                const uint32_t hpo = shl1<W>(Ph, hp, two, a.one);
+                const uint32_t hmo = shl1<W>(Mh, hm, two, a.one);
 #pragma unroll
                 for (int w = 0; w < W; ++w) {
                     Pv[w] = lop3<0xF1>(Mh[w], Xv[w], Ph[w]);  // Mh | ~(Xv | Ph)

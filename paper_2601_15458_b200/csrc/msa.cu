@@ -242,7 +242,7 @@ void exchange_blocks(dm_ctx* ctx, const std::vector<dm_node>& nodes, const std::
 
 dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node>& nodes,
                       const std::vector<uint32_t>& order, const NwScheme& sc, dm_stats* st,
-                      dm_progress_fn progress, void* progress_user) {
+                      dm_progress_fn progress, void* progress_user, bool host_rows) {
     const uint32_t n = s->n;
     if (order.size() != n) throw invalid_argument("tree order does not match the sequence set");
     if (nodes.empty()) throw invalid_argument("empty tree");
@@ -441,8 +441,10 @@ dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node
         const uint64_t width = W[0];
         out->width = width;
         out->dev_pitch = pitch;
-        out->rows.resize((uint64_t)n * width);
-        if (width) download_rows(ctx, out->rows.data(), rowsbuf.p, width, pitch, n, stream);
+        if (host_rows) {  // (callers that read the device rows skip this copy)
+            out->rows.resize((uint64_t)n * width);
+            if (width) download_rows(ctx, out->rows.data(), rowsbuf.p, width, pitch, n, stream);
+        }
         DM_CUDA(cudaStreamSynchronize(stream));
         out->row_seq = order;
         out->nodes = nodes;
@@ -458,6 +460,42 @@ dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node
         throw;
     }
     return out;
+}
+
+namespace {
+// out[k] = src row sel[k] (warp per row, 16-byte loads from the pitched source)
+__global__ void gather_rows_kernel(const uint8_t* __restrict__ src, uint64_t pitch, const uint32_t* __restrict__ sel,
+                                   uint64_t n, uint64_t width, uint8_t* __restrict__ out) {
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t k = warp; k < n; k += nwarps) {
+        const uint8_t* r = src + (uint64_t)sel[k] * pitch;  // pitch is a multiple of 64
+        uint8_t* o = out + k * width;
+        for (uint64_t c = (uint64_t)lane * 16; c < width; c += 32 * 16) {
+            const uint4 v = *reinterpret_cast<const uint4*>(r + c);
+            const uint8_t* b = reinterpret_cast<const uint8_t*>(&v);
+            const uint64_t m = width - c < 16 ? width - c : 16;
+#pragma unroll
+            for (int t = 0; t < 16; ++t)
+                if ((uint64_t)t < m) o[c + t] = b[t];
+        }
+    }
+}
+}  // namespace
+
+void gather_rows_to_host(dm_ctx* ctx, const uint8_t* src, uint64_t pitch, const uint32_t* sel, uint64_t n,
+                         uint64_t width, char* out) {
+    if (n == 0 || width == 0) return;
+    uint32_t* d_sel = ctx->aux2.as<uint32_t>(n);
+    DM_CUDA(cudaMemcpyAsync(d_sel, sel, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    uint8_t* d_out = (uint8_t*)ctx->rows_b.get(n * width);
+    const uint64_t blocks = std::min<uint64_t>((n + 7) / 8, (uint64_t)ctx->sm_count * 16);
+    gather_rows_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(src, pitch, d_sel, n, width, d_out);
+    DM_CUDA(cudaGetLastError());
+    ctx->launches += 1;
+    trace_bytes("gather_rows_kernel", n * width, n * width);
+    download_host(ctx, out, d_out, n * width, ctx->stream);
 }
 
 void insert_gap_columns(dm_ctx* ctx, const char* rows, uint64_t nrows, uint64_t width, const uint32_t* pos,

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <string_view>
 #include <unordered_map>
@@ -65,7 +66,7 @@ namespace dm {
 AlignCore align_core(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint32_t n,
                      const std::vector<std::string>* ids, int alphabet, int gap_open, int gap_extend, int flat,
                      const int16_t* custom_table, const uint8_t* custom_has, uint64_t seed, int input_order,
-                     dm_stats* st) {
+                     dm_stats* st, bool host_rows) {
     AlignCore res;
     const auto t0 = std::chrono::steady_clock::now();
     const bool trace = std::getenv("DM_TRACE") != nullptr;
@@ -172,16 +173,21 @@ AlignCore align_core(dm_ctx* ctx, const char* data, const uint64_t* offsets, uin
             dups[it->second].push_back(i);
         }
     }
-    std::vector<uint64_t> roff(reps.size() + 1, 0);
-    for (size_t r = 0; r < reps.size(); ++r) roff[r + 1] = roff[r] + (offsets[reps[r] + 1] - offsets[reps[r]]);
-    std::string rdata(roff[reps.size()], '\0');
-    host_parallel_for(reps.size(), 256, [&](uint64_t r) {
-        std::memcpy(&rdata[roff[r]], data + offsets[reps[r]], roff[r + 1] - roff[r]);
-    });
     res.reps = reps;
     res.dups = dups;
     mark("dedup");
-    dm_seqset* s = seqset_create(ctx, rdata.data(), roff.data(), (uint32_t)reps.size());
+    dm_seqset* s = nullptr;
+    if (reps.size() == n) {  // no duplicates: the caller's buffer as it is
+        s = seqset_create(ctx, data, offsets, n);
+    } else {  // the distinct sequences, packed (no zero fill: every byte is copied)
+        std::vector<uint64_t> roff(reps.size() + 1, 0);
+        for (size_t r = 0; r < reps.size(); ++r) roff[r + 1] = roff[r] + (offsets[reps[r] + 1] - offsets[reps[r]]);
+        std::unique_ptr<char[]> rdata(new char[std::max<uint64_t>(roff[reps.size()], 1)]);
+        host_parallel_for(reps.size(), 256, [&](uint64_t r) {
+            std::memcpy(rdata.get() + roff[r], data + offsets[reps[r]], roff[r + 1] - roff[r]);
+        });
+        s = seqset_create(ctx, rdata.get(), roff.data(), (uint32_t)reps.size());
+    }
     mark("seqset");
     try {
         const NwScheme sc = make_scheme(table, has, osur, gap_extend);
@@ -191,7 +197,7 @@ AlignCore align_core(dm_ctx* ctx, const char* data, const uint64_t* offsets, uin
         const auto p0 = std::chrono::steady_clock::now();
         build_tree(ctx, s, seed, 100, nodes, order, st ? &ts : nullptr);
         const auto p1 = std::chrono::steady_clock::now();
-        res.msa.reset(align_all(ctx, s, nodes, order, sc, st ? &as : nullptr));
+        res.msa.reset(align_all(ctx, s, nodes, order, sc, st ? &as : nullptr, nullptr, nullptr, host_rows));
         const auto p2 = std::chrono::steady_clock::now();
         mark("tree+align");
         // re-expand duplicates (pipeline.cpp:130-146): output slot -> (input record, MSA row)
@@ -249,14 +255,14 @@ int dm_align_sequences(dm_ctx* ctx, const char* data, const uint64_t* offsets, u
                        uint64_t* width_out, dm_align_summary* summary, dm_stats* st) {
     return dm::guard(ctx, [&] {
         dm::require(ctx && offsets && rows_out && width_out, "null argument");
+        // rows stay on the device; output slot k = MSA row slot_row[k], gathered there
         dm::AlignCore res = dm::align_core(ctx, data, offsets, n, nullptr, alphabet, gap_open, gap_extend, flat,
-                                           custom_table, custom_has, seed, input_order, st);
+                                           custom_table, custom_has, seed, input_order, st, false);
         const uint64_t W = res.msa->width;
         char* out = (char*)std::malloc(std::max<uint64_t>((uint64_t)n * W, 1));
         if (!out) throw std::bad_alloc();
-        dm::host_parallel_for(n, 64, [&](uint64_t k) {
-            std::memcpy(out + k * W, res.msa->rows.data() + (uint64_t)res.slot_row[k] * W, W);
-        });
+        dm::gather_rows_to_host(ctx, (const uint8_t*)ctx->rows_a.p, res.msa->dev_pitch, res.slot_row.data(), n, W,
+                                out);
         *rows_out = out;
         *width_out = W;
         if (summary) *summary = res.summary;

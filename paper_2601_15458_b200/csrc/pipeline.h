@@ -22,6 +22,6 @@ struct AlignCore {
 AlignCore align_core(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint32_t n,
                      const std::vector<std::string>* ids, int alphabet, int gap_open, int gap_extend, int flat,
                      const int16_t* custom_table, const uint8_t* custom_has, uint64_t seed, int input_order,
-                     dm_stats* st);
+                     dm_stats* st, bool host_rows = true);
 
 }  // namespace dm
