@@ -79,7 +79,7 @@ __global__ void colmap_kernel(const SideDesc* __restrict__ sides, const uint32_t
 __global__ void insert_rows_kernel(const SideDesc* __restrict__ sides, const uint32_t* __restrict__ side_rows_prefix,
                                    uint32_t nsides, uint32_t total_rows, const int32_t* __restrict__ maps,
                                    uint8_t* __restrict__ rows, uint64_t pitch) {
-    extern __shared__ uint8_t srow[];
+    extern __shared__ __align__(16) uint8_t srow[];
     for (uint32_t t = blockIdx.x; t < total_rows; t += gridDim.x) {
         uint32_t lo = 0, hi = nsides;  // largest s with prefix[s] <= t
         while (hi - lo > 1) {
@@ -89,14 +89,23 @@ __global__ void insert_rows_kernel(const SideDesc* __restrict__ sides, const uin
         }
         const SideDesc d = sides[lo];
         const uint32_t r = d.r0 + (t - side_rows_prefix[lo]);
-        uint8_t* row = rows + (uint64_t)r * pitch;
+        uint8_t* row = rows + (uint64_t)r * pitch;  // 64-byte aligned, pitch >= round64(w_new)
         __syncthreads();
-        for (uint32_t c = threadIdx.x; c < d.w_old; c += blockDim.x) srow[c] = row[c];
+        // the old row into shared memory, 16 bytes per thread (bytes past w_old are never mapped)
+        for (uint32_t c = threadIdx.x * 16; c < d.w_old; c += blockDim.x * 16)
+            *reinterpret_cast<uint4*>(srow + c) = *reinterpret_cast<const uint4*>(row + c);
         __syncthreads();
+        // the new row, 4 bytes per thread per store (bytes past w_new up to the next
+        // multiple of 4 are padding no reader looks at)
         const int32_t* map = maps + d.map_off;
-        for (uint32_t o = threadIdx.x; o < d.w_new; o += blockDim.x) {
-            const int32_t src = map[o];
-            row[o] = src < 0 ? (uint8_t)'-' : srow[src];
+        for (uint32_t o = threadIdx.x * 4; o < d.w_new; o += blockDim.x * 4) {
+            uint32_t v = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int32_t src = o + k < d.w_new ? map[o + k] : -1;
+                v |= (uint32_t)(src < 0 ? (uint8_t)'-' : srow[src]) << (8 * k);
+            }
+            *reinterpret_cast<uint32_t*>(row + o) = v;
         }
     }
 }
@@ -142,7 +151,7 @@ void apply_sides(dm_ctx* ctx, std::vector<SideDesc>& sides, const uint32_t* d_ga
         trace_bytes("insert_rows_kernel", rd, wr);
     }
     const uint32_t total = prefix.back();
-    const size_t smem = std::max<uint64_t>(max_w_old, 16);
+    const size_t smem = std::max<uint64_t>((max_w_old + 15) & ~uint64_t(15), 16);
     if (smem > 48 * 1024)
         DM_CUDA(cudaFuncSetAttribute(insert_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int grid = (int)std::max<uint32_t>(1, std::min<uint32_t>(total, (uint32_t)ctx->sm_count * 16));

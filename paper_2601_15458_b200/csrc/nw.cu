@@ -35,6 +35,7 @@
 #include "nw.h"
 #include "nw_fwd.cuh"
 #include "nw_seq.cuh"
+#include "nw_clu.cuh"
 #include "comm.h"
 
 namespace dm {
@@ -197,6 +198,46 @@ bool use_seq(const dm_ctx* ctx, size_t cnt) {
     return cnt >= (size_t)ctx->sm_count * 16;
 }
 
+// Latency form across a cluster (nw_clu.cuh) for batches too small to fill
+// the GPU one alignment per CTA (the top merge levels): cluster size so that
+// cnt x CL <= SM count. 0 = not used. DM_NW_CLU=0 disables, =k forces k.
+constexpr uint32_t kCluMaxM = 4000;  // b and CL_NWW full-width rows in shared memory (52 B per column)
+int clu_size(const dm_ctx* ctx, size_t cnt, bool wide, uint32_t mmax, const NwScheme& sc) {
+    const char* e = std::getenv("DM_NW_CLU");
+    const int force = e ? std::atoi(e) : -1;
+    if (force == 0 || wide || cnt == 0 || mmax > kCluMaxM) return 0;
+    if (nwk::clu_smem_bytes(sc.K, sc.Kp, mmax) > 220 * 1024) return 0;
+    if (force == 2 || force == 4 || force == 8) return force;
+    // clusters of 8 need 8 free SMs of one GPC: beyond ~8 of them at once they
+    // queue (measured: 16 x 2,600^2 take 1.48 ms at 8, 0.95 ms at 4)
+    if (cnt <= 8) return 8;
+    if (cnt * 4 <= (size_t)ctx->sm_count - 20) return 4;
+    if (cnt * 2 <= (size_t)ctx->sm_count - 20) return 2;
+    return 0;
+}
+
+template <int CL>
+void launch_clu(dm_ctx* ctx, const nwk::FwdArgs& fa, const NwScheme& sc, uint32_t mmax) {  // mmax <= kCluMaxM
+    constexpr int RRT = 4;
+    auto kern = nwk::nw_clu_kernel<RRT, CL>;
+    const size_t smem = nwk::clu_smem_bytes(sc.K, sc.Kp, mmax);
+    if (smem > 48 * 1024)
+        DM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(fa.njobs * CL);
+    cfg.blockDim = dim3(nwk::CL_NWW * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    DM_CUDA(cudaLaunchKernelEx(&cfg, kern, fa));
+}
+
 struct SeqDev {
     const int32_t* table = nullptr;
     const int32_t* ptab = nullptr;
@@ -241,6 +282,9 @@ void nw_warm() {
     DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int64_t, 4>));
     DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int64_t, 8>));
     DM_CUDA(cudaFuncGetAttributes(&fa, nw_traceback_kernel));
+    DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_clu_kernel<4, 2>));
+    DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_clu_kernel<4, 4>));
+    DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_clu_kernel<4, 8>));
     DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_seq_kernel<int32_t, true>));
     DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_seq_kernel<int32_t, false>));
     DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_seq_kernel<int64_t, true>));
@@ -418,6 +462,22 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
             out.launches += 1;
             ctx->launches += 1;
             g0 = c1;
+        }
+        if (!seq) {
+            uint32_t mmax = 1;
+            for (size_t q = c0; q < c1; ++q) mmax = std::max(mmax, sj[q].m);
+            const int cl = clu_size(ctx, cnt, wide, mmax, sc);
+            if (cl) {  // one cluster per alignment, one launch for the chunk
+                nwk::FwdArgs fa{d_chars, d_jobs, cnt, d_lut, d_table, sc.K, sc.Kp, 4 * sc.open, 4 * sc.extend,
+                                d_trace, out.d_res, d_cnt, 1};
+                if (cl == 8) launch_clu<8>(ctx, fa, sc, mmax);
+                else if (cl == 4) launch_clu<4>(ctx, fa, sc, mmax);
+                else launch_clu<2>(ctx, fa, sc, mmax);
+                DM_CUDA(cudaGetLastError());
+                out.launches += 1;
+                ctx->launches += 1;
+                g0 = c1;
+            }
         }
         while (g0 < c1) {  // one launch per warps-per-alignment group
             const int grp = group_of(sj[g0].n);

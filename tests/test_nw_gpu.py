@@ -12,13 +12,16 @@ pytestmark = pytest.mark.gpu
 
 
 
-@pytest.fixture(autouse=True, params=["ring", "seq"])
+@pytest.fixture(autouse=True, params=["ring", "seq", "clu2", "clu8"])
 def nw_kernel(request, monkeypatch):
-    """Every test runs on both forward kernels: the multi-warp ring kernel
-    (nw_fwd.cuh, small batches) and the one-warp-per-alignment throughput
-    kernel (nw_seq.cuh, 256-scaled tags, query profiles, short last bands),
-    which the library picks for batches of >= 16 alignments per SM."""
+    """Every test runs on every forward kernel: the multi-warp ring kernel
+    (nw_fwd.cuh), the one-warp-per-alignment throughput kernel (nw_seq.cuh,
+    256-scaled tags, query profiles, short last bands; batches of >= 16
+    alignments per SM) and the cluster kernel (nw_clu.cuh, 128-row bands
+    across 2 or 8 CTAs with distributed-shared-memory rings and global wrap
+    rows; batches too small to fill the GPU one alignment per CTA)."""
     monkeypatch.setenv("DM_NW_SEQ", "1" if request.param == "seq" else "0")
+    monkeypatch.setenv("DM_NW_CLU", {"clu2": "2", "clu8": "8"}.get(request.param, "0"))
     return request.param
 
 def rand_str(rng, n, alphabet="ACGT"):
