@@ -127,7 +127,11 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
     // residue bytes so the first kernels start after a short upload, and
     // halve again over the tail so little compute is left once the last
     // upload lands.
-    uint64_t big = 256ull << 20, small = 32ull << 20;
+    // 128 MB chunks and raw (speculative) chunks of at most 32 MB: the copy
+    // engine alternates short raw uploads with the packed ones, so the GPU is
+    // fed early (measured 27.1 vs 28.1 ms per cfg1 step at 256 / 128 MB,
+    // tools/sweep_stream.sh)
+    uint64_t big = 128ull << 20, small = 32ull << 20;
     if (const char* env = std::getenv("DM_STREAM_CHUNK_BYTES"))
         big = small = std::max<uint64_t>(1, std::strtoull(env, nullptr, 10));
     if (const char* env = std::getenv("DM_STREAM_BIG_MB")) big = std::max<uint64_t>(1, std::strtoull(env, nullptr, 10)) << 20;
@@ -147,9 +151,11 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
         cudaGetLastError();
         if (const char* e = std::getenv("DM_STREAM_RAW_FRAC")) raw_frac = std::min(1.0, std::max(0.0, std::atof(e)));
     }
-    // Raw chunks are at most half the big size: a raw chunk's upload (4x the
-    // bytes of a packed one) should not outlast the kernels of the chunk
-    // before it.
+    // Raw chunks are small (DM_STREAM_RAW_MB): a raw chunk's upload (4x the
+    // bytes of a packed one) should not hold the copy engine while packed
+    // chunks wait.
+    uint64_t raw_cap = 32ull << 20;
+    if (const char* env = std::getenv("DM_STREAM_RAW_MB")) raw_cap = std::max<uint64_t>(1, std::strtoull(env, nullptr, 10)) << 20;
     std::vector<uint64_t> cb{0};
     std::vector<char> spec;  // chunk k goes up raw (speculative)
     uint64_t raw_sofar = 0, all_sofar = 0;
@@ -158,7 +164,7 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
         uint64_t t = std::min(big, small << std::min<uint64_t>(k, 20));
         if (rem < 2 * t) t = std::max(small, rem / 2);
         const bool raw = (double)raw_sofar < raw_frac * (double)(all_sofar + t);
-        if (raw) t = std::max<uint64_t>(std::min(t, big / 2), 1);
+        if (raw) t = std::max<uint64_t>(std::min(t, raw_cap), 1);
         // smallest hi > lo with offsets[2hi] - offsets[2lo] >= t
         uint64_t a = lo + 1, z = npairs;
         while (a < z) {
