@@ -91,6 +91,11 @@ int dm_ctx_create(int device, dm_ctx** out) {
         DM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
         DM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         c->own_stream = c->stream;
+        {
+            int least = 0, greatest = 0;
+            DM_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+            c->side_prio = greatest;
+        }
         DM_CUDA(cudaEventCreate(&c->ev0));
         DM_CUDA(cudaEventCreate(&c->ev1));
         dm::lev_warm();
@@ -105,16 +110,26 @@ int dm_ctx_destroy(dm_ctx* ctx) {
         if (!ctx) return;
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
-        for (dm_ctx*& p : ctx->prep) {  // planner contexts of the streamed path
-            if (!p) continue;
+        auto destroy_aux = [](dm_ctx*& p) {  // planner / background contexts
+            if (!p) return;
             cudaStreamSynchronize(p->stream);
+            for (int k = 0; k < dm_ctx::kLevSide; ++k) {
+                if (p->lev_side[k]) {
+                    cudaStreamSynchronize(p->lev_side[k]);
+                    cudaStreamDestroy(p->lev_side[k]);
+                }
+                if (p->lev_join[k]) cudaEventDestroy(p->lev_join[k]);
+            }
+            if (p->lev_fork) cudaEventDestroy(p->lev_fork);
             p->detach_buffers();
             cudaEventDestroy(p->ev0);
             cudaEventDestroy(p->ev1);
             cudaStreamDestroy(p->own_stream);
             delete p;
             p = nullptr;
-        }
+        };
+        for (dm_ctx*& p : ctx->prep) destroy_aux(p);  // planner contexts of the streamed path
+        destroy_aux(ctx->tree_bg);
         for (int k = 0; k < dm_ctx::kLevSide; ++k) {
             if (ctx->lev_side[k]) {
                 cudaStreamSynchronize(ctx->lev_side[k]);

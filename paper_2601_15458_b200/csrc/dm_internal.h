@@ -128,6 +128,8 @@ struct dm_ctx {
     // (32.5 / 32.9 / 34.1 ms per cfg1 step at 16 / 20 / 24)
     int lev_wmax_cap = 0;
     static constexpr int kLevSide = 8;  // side streams the distance buckets fan out on
+    int side_prio = 0;                  // their priority (dm_ctx_create: the greatest; 0 = default, the least)
+    dm_ctx* tree_bg = nullptr;          // low-priority context for the tree's background batches (tree.cu)
     cudaStream_t lev_side[kLevSide] = {};
     int lev_rr = 0;
     cudaEvent_t lev_fork = nullptr, lev_join[kLevSide] = {};

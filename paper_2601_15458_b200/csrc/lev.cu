@@ -335,13 +335,16 @@ int launch_plan(dm_ctx* ctx, const LevPlan& P, const LevSrc& S, uint32_t* d_out,
     // its buffers (run_long)
     // largest per-task work first: lanes per pair x words per lane
     std::stable_sort(order, order + nb, [](int x, int y) { return ((x % 32) << (x / 32)) > ((y % 32) << (y / 32)); });
-    const bool fork = nb > 1 || after != nullptr;
+    // (a context with prioritised side streams always fans out: its batches
+    // then take SM slots ahead of default-priority work, e.g. the tree's
+    // background batches)
+    const bool fork = nb > 1 || after != nullptr || ctx->side_prio != 0;
     int used[kLevSide], nused = 0;
     if (fork) {
         if (!ctx->lev_fork) {
             DM_CUDA(cudaEventCreateWithFlags(&ctx->lev_fork, cudaEventDisableTiming));
             for (int k = 0; k < kLevSide; ++k) {
-                DM_CUDA(cudaStreamCreateWithFlags(&ctx->lev_side[k], cudaStreamNonBlocking));
+                DM_CUDA(cudaStreamCreateWithPriority(&ctx->lev_side[k], cudaStreamNonBlocking, ctx->side_prio));
                 DM_CUDA(cudaEventCreateWithFlags(&ctx->lev_join[k], cudaEventDisableTiming));
             }
         }

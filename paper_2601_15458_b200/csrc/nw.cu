@@ -176,15 +176,20 @@ void launch_group(dm_ctx* ctx, int nww, const nwk::FwdArgs& fa, size_t smem, uin
     else if (nww == 2) launch_fwd<V, 2>(ctx, fa, smem, wrap_m);
     else if (nww == 3) launch_fwd<V, 3>(ctx, fa, smem, wrap_m);
     else if (nww == 4) launch_fwd<V, 4>(ctx, fa, smem, wrap_m);
+    else if (nww == 5) launch_fwd<V, 5>(ctx, fa, smem, wrap_m);
+    else if (nww == 6) launch_fwd<V, 6>(ctx, fa, smem, wrap_m);
+    else if (nww == 7) launch_fwd<V, 7>(ctx, fa, smem, wrap_m);
     else launch_fwd<V, 8>(ctx, fa, smem, wrap_m);
 }
 
-// warps per alignment: one band per warp up to 4 bands (a CTA's warps wait
-// for each other between alignments, so no idle warps there), then 8
-constexpr int kGroups = 5;
+// warps per alignment: one band per warp up to 8 bands (a CTA's warps wait
+// for each other between alignments, so no idle warps there), then 8 with
+// rounds (5-7 bands on 8 warps left 1-3 warps idle: 2,500-row merges ran at
+// half the throughput kernel's rate)
+constexpr int kGroups = 8;
 int group_of(uint32_t n) {
     const uint32_t nb = (n + nwk::BAND - 1) / nwk::BAND;
-    return nb <= 4 ? (int)std::max<uint32_t>(nb, 1) : 8;
+    return (int)std::min<uint32_t>(std::max<uint32_t>(nb, 1), 8);
 }
 
 // Throughput form (nw_seq.cuh): one warp per alignment, bands in sequence.
@@ -275,6 +280,9 @@ void nw_warm() {
     DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int32_t, 2>));
     DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int32_t, 3>));
     DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int32_t, 4>));
+    DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int32_t, 5>));
+    DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int32_t, 6>));
+    DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int32_t, 7>));
     DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int32_t, 8>));
     DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int64_t, 1>));
     DM_CUDA(cudaFuncGetAttributes(&fa, nwk::nw_fwd_kernel<int64_t, 2>));

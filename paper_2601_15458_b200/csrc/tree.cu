@@ -38,7 +38,13 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <condition_variable>
+#include <deque>
+#include <functional>
+#include <exception>
+#include <mutex>
 #include <random>
+#include <thread>
 #include <unordered_set>
 
 #include "comm.h"
@@ -462,6 +468,30 @@ void exchange_subtrees(dm_ctx* ctx, std::vector<PNode>& pool, std::vector<uint32
 
 }  // namespace
 
+// Low-priority context for the tree's background batches (one per context,
+// kept for reuse; destroyed with it): own stream, scratch and side streams at
+// the default (least) priority, while the context's own distance batches run
+// on side streams of the greatest priority.
+dm_ctx* tree_bg_context(dm_ctx* ctx) {
+    if (!ctx->tree_bg) {
+        auto* p = new dm_ctx;
+        p->device = ctx->device;
+        p->sm_count = ctx->sm_count;
+        int least = 0, greatest = 0;
+        DM_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        if (cudaStreamCreateWithPriority(&p->stream, cudaStreamNonBlocking, least) != cudaSuccess) {
+            delete p;
+            throw cuda_error("cannot create the tree's background stream");
+        }
+        p->own_stream = p->stream;
+        p->side_prio = 0;
+        DM_CUDA(cudaEventCreate(&p->ev0));
+        DM_CUDA(cudaEventCreate(&p->ev1));
+        ctx->tree_bg = p;
+    }
+    return ctx->tree_bg;
+}
+
 void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_cap_in,
                 std::vector<dm_node>& nodes_out, std::vector<uint32_t>& order, dm_stats* st) {
     const uint32_t n = s->n;
@@ -547,6 +577,108 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
     };
     int level = 0;
     int err_flag = 0;
+
+    // Background batches (one rank): the all-pairs matrices of the small
+    // subtrees a level creates are computed on a low-priority context while
+    // the later levels run, filling the SM slots their batches' tails leave
+    // idle; subtree_kernel resolves them all at the end. Every small
+    // subtree's matrix lies at its offset in one buffer (sum k^2 <= n T).
+    const bool bg_on = shard_world(ctx) == 1 && [] {
+        const char* e = std::getenv("DM_TREE_BG");
+        return !(e && e[0] == '0');
+    }();
+    dm_ctx* bg = bg_on ? tree_bg_context(ctx) : nullptr;
+    uint32_t* d_submat = bg_on ? sc.sub_mat.as<uint32_t>((uint64_t)n * T + 1) : nullptr;
+    struct BgJob {
+        cudaEvent_t ready = nullptr;
+        std::vector<uint64_t> soff, moff, ioff;
+        std::vector<uint32_t> sk;
+        uint64_t itot = 0;
+    };
+    struct BgState {
+        std::mutex mu;
+        std::condition_variable cv;
+        std::deque<BgJob> q;
+        bool done = false;
+        std::exception_ptr err;
+        LevTotals tot;
+    } bgs;
+    std::thread bg_thread;
+    size_t bg_sent = 0;
+    uint64_t bg_mtot = 0;
+    std::vector<cudaEvent_t> bg_events;
+    if (bg_on)
+        bg_thread = std::thread([&] {
+            try {
+                DM_CUDA(cudaSetDevice(ctx->device));
+                DevBuf b_soff(&bg->stream), b_sk(&bg->stream), b_moff(&bg->stream), b_ioff(&bg->stream),
+                    b_items(&bg->stream);
+                for (;;) {
+                    BgJob job;
+                    {
+                        std::unique_lock<std::mutex> g(bgs.mu);
+                        bgs.cv.wait(g, [&] { return bgs.done || !bgs.q.empty(); });
+                        if (bgs.q.empty()) return;
+                        job = std::move(bgs.q.front());
+                        bgs.q.pop_front();
+                    }
+                    DM_CUDA(cudaStreamWaitEvent(bg->stream, job.ready, 0));  // the level's partition is done
+                    const size_t S = job.sk.size();
+                    LevItem* d_items = b_items.as<LevItem>(std::max<uint64_t>(job.itot, 1));
+                    pair_items_kernel<<<(unsigned)S, 128, 0, bg->stream>>>(
+                        d_order, upload(bg, b_soff, job.soff), upload(bg, b_sk, job.sk), upload(bg, b_moff, job.moff),
+                        upload(bg, b_ioff, job.ioff), d_items);
+                    DM_CUDA(cudaGetLastError());
+                    lev_run_device_items(bg, s, d_items, job.itot, d_submat, &bgs.tot, false);
+                    bgs.tot.launches += 1;
+                }
+            } catch (...) {
+                std::lock_guard<std::mutex> g(bgs.mu);
+                bgs.err = std::current_exception();
+            }
+        });
+    auto stop_bg = [&] {
+        if (!bg_thread.joinable()) return;
+        {
+            std::lock_guard<std::mutex> g(bgs.mu);
+            bgs.done = true;
+        }
+        bgs.cv.notify_all();
+        bg_thread.join();
+    };
+    struct BgGuard {  // error paths: the worker is stopped before the scratch it uses goes away
+        std::function<void()> f;
+        ~BgGuard() { f(); }
+    } bg_guard{[&] {
+        stop_bg();
+        for (cudaEvent_t e : bg_events) cudaEventDestroy(e);
+        if (bg) cudaStreamSynchronize(bg->stream);
+    }};
+    // the small subtrees made so far go to the background worker (their slices
+    // of d_order are final once the work queued on `stream` so far is done)
+    auto dispatch_bg = [&] {
+        if (!bg_on || bg_sent == small.size()) return;
+        BgJob job;
+        for (size_t r = bg_sent; r < small.size(); ++r) {
+            const PNode& nd = pool[small[r]];
+            const uint32_t k = nd.end - nd.begin;
+            job.soff.push_back(nd.begin);
+            job.sk.push_back(k);
+            job.moff.push_back(bg_mtot);
+            job.ioff.push_back(job.itot);
+            job.itot += (uint64_t)k * (k - 1) / 2;
+            bg_mtot += (uint64_t)k * k;
+        }
+        DM_CUDA(cudaEventCreateWithFlags(&job.ready, cudaEventDisableTiming));
+        bg_events.push_back(job.ready);
+        DM_CUDA(cudaEventRecord(job.ready, stream));
+        {
+            std::lock_guard<std::mutex> g(bgs.mu);
+            bgs.q.push_back(std::move(job));
+        }
+        bgs.cv.notify_all();
+        bg_sent = small.size();
+    };
     try_own();
     while (!big.empty()) {
         const size_t B = big.size();
@@ -733,7 +865,26 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
         }
         ++level;
         big.swap(next);
+        dispatch_bg();
         try_own();
+    }
+    if (bg_on && !err_flag) {
+        dispatch_bg();  // the rest (e.g. a root small enough from the start)
+        stop_bg();
+        if (bgs.err) std::rethrow_exception(bgs.err);
+        DM_CUDA(cudaEventRecord(bg->ev1, bg->stream));
+        DM_CUDA(cudaStreamWaitEvent(stream, bg->ev1, 0));
+        if (trace) {
+            const auto w0 = std::chrono::steady_clock::now();
+            DM_CUDA(cudaEventSynchronize(bg->ev1));
+            std::fprintf(stderr, "[dm tree] background all-pairs: %zu small subtrees, waited %.3f ms after the levels\n",
+                         small.size(), ms(w0, std::chrono::steady_clock::now()));
+        }
+        tot.cells += bgs.tot.cells;
+        tot.cells_exec += bgs.tot.cells_exec;
+        tot.launches += bgs.tot.launches;
+        ctx->launches += bg->launches;
+        bg->launches = 0;
     }
 
     // ---- small subtrees: one all-pairs matrix each, resolved on the device
@@ -754,7 +905,7 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
             roff[r] = rtot;
             ioff[r] = itot;
             itot += (uint64_t)k * (k - 1) / 2;
-            if (!dev) {
+            if (!dev && !bg_on) {
                 const uint32_t* mem = order.data() + nd.begin;
                 for (uint32_t i = 0; i < k; ++i)
                     for (uint32_t j = i + 1; j < k; ++j)
@@ -764,10 +915,12 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
             rtot += 2ull * k - 1;
         }
         const auto s0 = tnow();
-        uint32_t* d_mat = sc.sub_mat.as<uint32_t>(mtot);
+        uint32_t* d_mat = bg_on ? d_submat : sc.sub_mat.as<uint32_t>(mtot);
         const uint32_t* d_sk = upload(ctx, sc.sub_k, sk);
         const uint64_t* d_smatoff = upload(ctx, sc.sub_matoff, moff);
-        if (dev) {
+        if (bg_on) {
+            // computed in the background (same order, same offsets)
+        } else if (dev) {
             LevItem* d_items = sc.items.as<LevItem>(std::max<uint64_t>(itot, 1));
             pair_items_kernel<<<(unsigned)S, 128, 0, stream>>>(d_order, upload(ctx, sc.candoff, soff), d_sk, d_smatoff,
                                                                upload(ctx, sc.itemoff, ioff), d_items);
