@@ -310,6 +310,8 @@ dm_seqset* seqset_create_device(dm_ctx* ctx, const uint8_t* d_raw, const uint64_
 void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_cap,
                 std::vector<dm_node>& nodes, std::vector<uint32_t>& order, dm_stats* st);
 double int32_peak(dm_ctx* ctx, int mode);
+// The context's side streams (created once, at ctx->side_prio) and their fork/join events.
+void ensure_side_streams(dm_ctx* ctx);
 void lev_warm();
 void nw_warm();
 // progress (optional): called once per node as it completes (leaves when the

@@ -341,13 +341,7 @@ int launch_plan(dm_ctx* ctx, const LevPlan& P, const LevSrc& S, uint32_t* d_out,
     const bool fork = nb > 1 || after != nullptr || ctx->side_prio != 0;
     int used[kLevSide], nused = 0;
     if (fork) {
-        if (!ctx->lev_fork) {
-            DM_CUDA(cudaEventCreateWithFlags(&ctx->lev_fork, cudaEventDisableTiming));
-            for (int k = 0; k < kLevSide; ++k) {
-                DM_CUDA(cudaStreamCreateWithPriority(&ctx->lev_side[k], cudaStreamNonBlocking, ctx->side_prio));
-                DM_CUDA(cudaEventCreateWithFlags(&ctx->lev_join[k], cudaEventDisableTiming));
-            }
-        }
+        ensure_side_streams(ctx);
         if (!after) {
             DM_CUDA(cudaEventRecord(ctx->lev_fork, st));
             after = ctx->lev_fork;
@@ -421,6 +415,15 @@ void run_planned(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const ui
 }
 
 }  // namespace
+
+void ensure_side_streams(dm_ctx* ctx) {
+    if (ctx->lev_fork) return;
+    DM_CUDA(cudaEventCreateWithFlags(&ctx->lev_fork, cudaEventDisableTiming));
+    for (int k = 0; k < dm_ctx::kLevSide; ++k) {
+        DM_CUDA(cudaStreamCreateWithPriority(&ctx->lev_side[k], cudaStreamNonBlocking, ctx->side_prio));
+        DM_CUDA(cudaEventCreateWithFlags(&ctx->lev_join[k], cudaEventDisableTiming));
+    }
+}
 
 // Loads every kernel instance up front (lazy module loading would otherwise
 // charge the first batch that hits a new bucket).

@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(128) nw_traceback_kernel(const TbArgs a) {
 // wrap_m: largest width of an alignment with more bands than NWW (0: none);
 // such launches get a per-CTA global row for the round-to-round hand-off.
 template <class V, int NWW>
-void launch_fwd(dm_ctx* ctx, const nwk::FwdArgs& fa, size_t smem, uint32_t wrap_m) {
+void launch_fwd(dm_ctx* ctx, const nwk::FwdArgs& fa, size_t smem, uint32_t wrap_m, cudaStream_t st) {
     const int occ = occupancy((const void*)nwk::nw_fwd_kernel<V, NWW>, NWW * 32, smem);
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(fa.njobs, (uint64_t)occ * ctx->sm_count));
     nwk::FwdArgs f = fa;
@@ -167,19 +167,19 @@ void launch_fwd(dm_ctx* ctx, const nwk::FwdArgs& fa, size_t smem, uint32_t wrap_
         f.wrap_stride = ((uint64_t)wrap_m + 1) * 3;
         f.wrap = ctx->nw_wrap.get((uint64_t)grid * f.wrap_stride * sizeof(V));
     }
-    nwk::nw_fwd_kernel<V, NWW><<<grid, NWW * 32, smem, ctx->stream>>>(f);
+    nwk::nw_fwd_kernel<V, NWW><<<grid, NWW * 32, smem, st>>>(f);
 }
 
 template <class V>
-void launch_group(dm_ctx* ctx, int nww, const nwk::FwdArgs& fa, size_t smem, uint32_t wrap_m) {
-    if (nww == 1) launch_fwd<V, 1>(ctx, fa, smem, 0);
-    else if (nww == 2) launch_fwd<V, 2>(ctx, fa, smem, wrap_m);
-    else if (nww == 3) launch_fwd<V, 3>(ctx, fa, smem, wrap_m);
-    else if (nww == 4) launch_fwd<V, 4>(ctx, fa, smem, wrap_m);
-    else if (nww == 5) launch_fwd<V, 5>(ctx, fa, smem, wrap_m);
-    else if (nww == 6) launch_fwd<V, 6>(ctx, fa, smem, wrap_m);
-    else if (nww == 7) launch_fwd<V, 7>(ctx, fa, smem, wrap_m);
-    else launch_fwd<V, 8>(ctx, fa, smem, wrap_m);
+void launch_group(dm_ctx* ctx, int nww, const nwk::FwdArgs& fa, size_t smem, uint32_t wrap_m, cudaStream_t st) {
+    if (nww == 1) launch_fwd<V, 1>(ctx, fa, smem, 0, st);
+    else if (nww == 2) launch_fwd<V, 2>(ctx, fa, smem, wrap_m, st);
+    else if (nww == 3) launch_fwd<V, 3>(ctx, fa, smem, wrap_m, st);
+    else if (nww == 4) launch_fwd<V, 4>(ctx, fa, smem, wrap_m, st);
+    else if (nww == 5) launch_fwd<V, 5>(ctx, fa, smem, wrap_m, st);
+    else if (nww == 6) launch_fwd<V, 6>(ctx, fa, smem, wrap_m, st);
+    else if (nww == 7) launch_fwd<V, 7>(ctx, fa, smem, wrap_m, st);
+    else launch_fwd<V, 8>(ctx, fa, smem, wrap_m, st);
 }
 
 // warps per alignment: one band per warp up to 8 bands (a CTA's warps wait
@@ -487,7 +487,29 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
                 g0 = c1;
             }
         }
-        while (g0 < c1) {  // one launch per warps-per-alignment group
+        // one launch per warps-per-alignment group, the groups side by side on
+        // the side streams (one after another, each small launch ran alone)
+        int ngroups = 0;
+        for (size_t q = g0; q < c1; ++q)
+            if (q == g0 || group_of(sj[q].n) != group_of(sj[q - 1].n)) ++ngroups;
+        const bool fork = ngroups > 1;
+        if (fork) {
+            // the wrap rows (group 8 only) are allocated before the fork: a
+            // stream-ordered allocation on ctx->stream after it would not be
+            // ordered before the side stream's kernel
+            uint64_t nwrap = 0, wm = 0;
+            for (size_t q = g0; q < c1; ++q)
+                if ((sj[q].n + nwk::BAND - 1) / nwk::BAND > 8) {
+                    ++nwrap;
+                    wm = std::max<uint64_t>(wm, sj[q].m);
+                }
+            if (nwrap) ctx->nw_wrap.get(nwrap * (wm + 1) * 3 * (wide ? 8 : 4));
+            ensure_side_streams(ctx);
+            DM_CUDA(cudaEventRecord(ctx->lev_fork, ctx->stream));
+            for (int k = 0; k < std::min(ngroups, dm_ctx::kLevSide); ++k)
+                DM_CUDA(cudaStreamWaitEvent(ctx->lev_side[k], ctx->lev_fork, 0));
+        }
+        while (g0 < c1) {
             const int grp = group_of(sj[g0].n);
             size_t g1 = g0;
             while (g1 < c1 && group_of(sj[g1].n) == grp) ++g1;
@@ -496,14 +518,20 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
             uint32_t wrap_m = 0;  // widest alignment with more bands than warps
             for (size_t q = g0; q < g1; ++q)
                 if ((sj[q].n + nwk::BAND - 1) / nwk::BAND > (uint32_t)grp) wrap_m = std::max(wrap_m, sj[q].m);
-            if (wide) launch_group<int64_t>(ctx, grp, fa, smem, wrap_m);
-            else launch_group<int32_t>(ctx, grp, fa, smem, wrap_m);
+            cudaStream_t gst = fork ? ctx->lev_side[gi % dm_ctx::kLevSide] : ctx->stream;
+            if (wide) launch_group<int64_t>(ctx, grp, fa, smem, wrap_m, gst);
+            else launch_group<int32_t>(ctx, grp, fa, smem, wrap_m, gst);
             DM_CUDA(cudaGetLastError());
             out.launches += 1;
             ctx->launches += 1;
             g0 = g1;
             ++gi;
         }
+        if (fork)
+            for (int k = 0; k < std::min(ngroups, dm_ctx::kLevSide); ++k) {
+                DM_CUDA(cudaEventRecord(ctx->lev_join[k], ctx->lev_side[k]));
+                DM_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->lev_join[k], 0));
+            }
         if (time_kernels) {
             DM_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
             DM_CUDA(cudaEventSynchronize(ctx->ev1));
