@@ -26,6 +26,7 @@
 
 #include "comm.h"
 #include "dm_internal.h"
+#include "nvtx.h"
 #include "host_copy.h"
 #include "nw.h"
 
@@ -252,6 +253,7 @@ void exchange_blocks(dm_ctx* ctx, const std::vector<dm_node>& nodes, const std::
 dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node>& nodes,
                       const std::vector<uint32_t>& order, const NwScheme& sc, dm_stats* st,
                       dm_progress_fn progress, void* progress_user, bool host_rows) {
+    NvtxRange nvtx_align("dm align_all");
     const uint32_t n = s->n;
     if (order.size() != n) throw invalid_argument("tree order does not match the sequence set");
     if (nodes.empty()) throw invalid_argument("empty tree");
@@ -313,6 +315,7 @@ dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node
         // batch is this rank's own (subtree ownership), never sharded.
         auto run_level = [&](const std::vector<uint32_t>& lvl, int d, bool local) {
             if (lvl.empty()) return;
+            NvtxRange nvtx_level("dm merge level");
             std::vector<NwJob> jobs(lvl.size());
             for (size_t k = 0; k < lvl.size(); ++k) {
                 const dm_node& nd = nodes[lvl[k]];

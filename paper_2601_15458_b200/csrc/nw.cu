@@ -32,6 +32,7 @@
 #include <cstring>
 
 #include "dm_internal.h"
+#include "nvtx.h"
 #include "nw.h"
 #include "nw_fwd.cuh"
 #include "nw_seq.cuh"
@@ -540,6 +541,7 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
             out.fwd_ms += ms;
             DM_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
         }
+        nvtxRangePushA("dm nw traceback");
         TbArgs ta{d_jobs, cnt, d_trace, out.d_res, out.d_gaps, d_cnt + kGroups, seq ? 1 : 0};
         const int tgrid = (int)std::max<uint64_t>(1, std::min<uint64_t>((cnt + 3) / 4, (uint64_t)ctx->sm_count * 8));
         nw_traceback_kernel<<<tgrid, 128, 0, ctx->stream>>>(ta);
@@ -553,6 +555,7 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
         }
         out.launches += 1;
         ctx->launches += 1;
+        nvtxRangePop();
         if (c1 < nj) DM_CUDA(cudaStreamSynchronize(ctx->stream));  // trace buffer reused by the next chunk
         c0 = c1;
     }

@@ -21,6 +21,7 @@
 #include "host_par.h"
 #include "nw.h"
 #include "pipeline.h"
+#include "nvtx.h"
 
 namespace dm {
 namespace {
@@ -68,6 +69,7 @@ AlignCore align_core(dm_ctx* ctx, const char* data, const uint64_t* offsets, uin
                      const int16_t* custom_table, const uint8_t* custom_has, uint64_t seed, int input_order,
                      dm_stats* st, bool host_rows) {
     AlignCore res;
+    NvtxRange nvtx_core("dm align_sequences");
     const auto t0 = std::chrono::steady_clock::now();
     const bool trace = std::getenv("DM_TRACE") != nullptr;
     auto tlast = t0;

@@ -38,6 +38,7 @@
 
 #include "capi_guard.h"
 #include "host_pack.h"
+#include "nvtx.h"
 
 namespace dm {
 namespace {
@@ -120,6 +121,7 @@ struct ChunkEvents {
 void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, uint64_t npairs, uint32_t* out,
                       LevTotals* tot, bool speculate, std::vector<std::pair<uint64_t, uint64_t>>* redo) {
     if (npairs == 0) return;
+    NvtxRange nvtx_stream("dm streamed pair batch");
     if (2 * npairs > 0xffffffffull) throw invalid_argument("too many sequences in one streamed batch");
     for (uint64_t i = 0; i < 2 * npairs; ++i)
         if (offsets[i + 1] < offsets[i]) throw invalid_argument("sequence offsets must be non-decreasing");
@@ -312,6 +314,7 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
         for (int b = 0; b < NB; ++b) DM_CUDA(cudaEventCreateWithFlags(&plan_up[b], cudaEventDisableTiming));
         EvGuard evp{plan_up};
         auto plan_chunk = [&](uint64_t p) {  // planner thread, ahead of the packer
+            NvtxRange nvtx_plan("dm host plan");
             const int b = (int)(p % NB);
             if (p >= NB) {  // chunk p - NB's plan has gone up from this slot
                 {
@@ -381,10 +384,13 @@ void lev_pairs_packed(dm_ctx* ctx, const char* data, const uint64_t* offsets, ui
                                     cudaMemcpyHostToDevice, ctx->copy_stream));
             h2d_bytes += (2 * (hi - lo) + 1) * 8;
             const double tp0 = trace ? now_ms() : 0.0;
+            bool pack_ok = false;
             uint64_t pb = 0;  // packed bytes
             if (spec[c]) {
                 kind[c] = kSpec;
-            } else if (pack && n >= 256 && pack_acgt_seqs(data, offsets + 2 * lo, 2 * (hi - lo), h_pack[b], &pb)) {
+            } else if (pack && n >= 256 && (nvtxRangePushA("dm pack chunk"),
+                                            pack_ok = pack_acgt_seqs(data, offsets + 2 * lo, 2 * (hi - lo), h_pack[b], &pb),
+                                            nvtxRangePop(), pack_ok)) {
                 kind[c] = kPacked;  // straight into the set's 2-bit code layout
             }
             if (trace)

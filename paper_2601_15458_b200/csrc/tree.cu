@@ -49,6 +49,7 @@
 
 #include "comm.h"
 #include "dm_internal.h"
+#include "nvtx.h"
 #include "rng.h"
 
 namespace dm {
@@ -494,6 +495,7 @@ dm_ctx* tree_bg_context(dm_ctx* ctx) {
 
 void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_cap_in,
                 std::vector<dm_node>& nodes_out, std::vector<uint32_t>& order, dm_stats* st) {
+    NvtxRange nvtx_tree("dm build_tree");
     const uint32_t n = s->n;
     if (n == 0) throw runtime_error("cannot build a cluster tree from zero sequences");
     const uint64_t exact_cap = std::max<uint64_t>(2, exact_cap_in);
@@ -681,6 +683,7 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
     };
     try_own();
     while (!big.empty()) {
+        NvtxRange nvtx_level("dm tree level");
         const size_t B = big.size();
         const auto t0 = tnow();
         const float k0 = tot.kernel_ms;
@@ -889,6 +892,7 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
 
     // ---- small subtrees: one all-pairs matrix each, resolved on the device
     if (!small.empty() && !err_flag) {
+        NvtxRange nvtx_small("dm tree small subtrees");
         const size_t S = small.size();
         const bool dev = owned || shard_world(ctx) == 1;  // jobs generated on the device (see the level loop)
         std::vector<uint32_t> sb(S), sk(S);
