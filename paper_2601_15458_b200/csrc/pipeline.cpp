@@ -12,10 +12,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <memory>
 #include <string>
 #include <string_view>
-#include <unordered_map>
 
 #include "capi_guard.h"
 #include "host_par.h"
@@ -88,28 +88,47 @@ AlignCore align_core(dm_ctx* ctx, const char* data, const uint64_t* offsets, uin
     auto rec = [ids](uint32_t i) {
         return "record '" + (ids ? (*ids)[i] : "seq" + std::to_string(i)) + "'";
     };
-    // First record (in input order) failing a byte-class test, checked in
-    // parallel over records; the message is then built sequentially for it,
-    // so errors read exactly as the reference's in-order loops report them.
-    auto first_bad_record = [&](const bool* bad) -> uint32_t {
-        std::atomic<uint32_t> first{UINT32_MAX};
-        host_parallel_for(n, 256, [&](uint64_t i) {
-            if (i >= first.load(std::memory_order_relaxed)) return;
-            for (uint64_t p = offsets[i]; p < offsets[i + 1]; ++p)
-                if (bad[(unsigned char)data[p]]) {
-                    uint32_t cur = first.load();
-                    while (i < cur && !first.compare_exchange_weak(cur, (uint32_t)i)) {
-                    }
-                    return;
-                }
-        });
-        return first.load();
+    // One parallel pass over the records: the byte classes each record holds
+    // (bit 0: outside the alphabet, validate_residues, seq_io.cpp:148-166;
+    // bit 1: not scored by the scheme, pipeline.cpp:92-100) and its hash for
+    // de-duplication. Errors are then reported for the first failing record
+    // in input order, with messages built sequentially, exactly as the
+    // reference's in-order loops report them (alphabet first, then the
+    // scheme's own validation, then unscored residues).
+    int16_t table[128 * 128];
+    uint8_t has[128];
+    int osur = 0;
+    std::exception_ptr scheme_err;
+    if (custom_table) {
+        std::memcpy(table, custom_table, sizeof(table));
+        std::memcpy(has, custom_has, sizeof(has));
+        osur = flat ? 0 : gap_open;
+    } else {
+        const int rc = dm_scheme_default(kind, gap_open, gap_extend, flat, table, has, &osur);
+        if (rc != DM_OK) scheme_err = std::make_exception_ptr(invalid_argument(last_error()));
+    }
+    bool member[256] = {};
+    for (char c : (kind == 0 ? kNucleotide : kProtein)) member[(unsigned char)c] = true;
+    uint8_t cls[256];
+    for (int c = 0; c < 256; ++c)
+        cls[c] = (uint8_t)((!custom_table && !member[c] ? 1 : 0) | (!scheme_err && (c >= 128 || !has[c]) ? 2 : 0));
+    std::vector<uint64_t> hv(n);
+    std::vector<uint8_t> rcls(n);
+    host_parallel_for(n, 256, [&](uint64_t i) {
+        const unsigned char* d = reinterpret_cast<const unsigned char*>(data + offsets[i]);
+        const uint64_t L = offsets[i + 1] - offsets[i];
+        uint8_t acc = 0;
+        for (uint64_t p = 0; p < L; ++p) acc |= cls[d[p]];
+        rcls[i] = acc;
+        hv[i] = std::hash<std::string_view>{}(std::string_view(data + offsets[i], L));
+    });
+    auto first_with = [&](uint8_t bit) -> uint32_t {
+        for (uint32_t i = 0; i < n; ++i)
+            if (rcls[i] & bit) return i;
+        return UINT32_MAX;
     };
     if (!custom_table) {  // validate_residues (seq_io.cpp:148-166)
-        bool member[256] = {}, bad[256];
-        for (char c : (kind == 0 ? kNucleotide : kProtein)) member[(unsigned char)c] = true;
-        for (int c = 0; c < 256; ++c) bad[c] = !member[c];
-        const uint32_t i = first_bad_record(bad);
+        const uint32_t i = first_with(1);
         if (i != UINT32_MAX)
             for (uint64_t p = offsets[i]; p < offsets[i + 1]; ++p) {
                 const char c = data[p];
@@ -119,60 +138,42 @@ AlignCore align_core(dm_ctx* ctx, const char* data, const uint64_t* offsets, uin
                                         (kind == 0 ? "nucleotide" : "protein") + " alphabet");
             }
     }
-    int16_t table[128 * 128];
-    uint8_t has[128];
-    int osur = 0;
-    if (custom_table) {
-        std::memcpy(table, custom_table, sizeof(table));
-        std::memcpy(has, custom_has, sizeof(has));
-        osur = flat ? 0 : gap_open;
-    } else {
-        const int rc = dm_scheme_default(kind, gap_open, gap_extend, flat, table, has, &osur);
-        if (rc != DM_OK) throw invalid_argument(last_error());
-    }
+    if (scheme_err) std::rethrow_exception(scheme_err);
     {  // every residue scored by the scheme (pipeline.cpp:92-100)
-        bool bad[256];
-        for (int c = 0; c < 256; ++c) bad[c] = c >= 128 || !has[c];
-        const uint32_t i = first_bad_record(bad);
+        const uint32_t i = first_with(2);
         if (i != UINT32_MAX)
             for (uint64_t p = offsets[i]; p < offsets[i + 1]; ++p) {
                 const unsigned char c = (unsigned char)data[p];
-                if (bad[c])
+                if (c >= 128 || !has[c])
                     throw runtime_error(rec(i) + " contains character '" + std::string(1, (char)c) +
                                         "' that the substitution matrix does not score");
             }
     }
     mark("validate");
-    // deduplicate: first occurrences in order (seq_io.cpp:168-186); the
-    // records' hashes are computed in parallel, the first-occurrence pass is
-    // sequential over them
-    std::vector<uint64_t> hv(n);
-    host_parallel_for(n, 256, [&](uint64_t i) {
-        hv[i] = std::hash<std::string_view>{}(std::string_view(data + offsets[i], offsets[i + 1] - offsets[i]));
-    });
-    struct KeyHash {
-        const std::vector<uint64_t>* h;
-        size_t operator()(uint32_t i) const { return (size_t)(*h)[i]; }
-    };
-    struct KeyEq {
-        const char* d;
-        const uint64_t* o;
-        bool operator()(uint32_t a, uint32_t b) const {
-            const uint64_t la = o[a + 1] - o[a], lb = o[b + 1] - o[b];
-            return la == lb && std::memcmp(d + o[a], d + o[b], la) == 0;
-        }
-    };
-    std::unordered_map<uint32_t, uint32_t, KeyHash, KeyEq> first(n * 2, KeyHash{&hv}, KeyEq{data, offsets});
+    // deduplicate: first occurrences in order (seq_io.cpp:168-186) through an
+    // open-addressing table of record indices keyed by the hashes above
+    uint64_t cap = 16;
+    while (cap < 2ull * n) cap <<= 1;
+    std::vector<uint32_t> slot_rec(cap, UINT32_MAX), slot_rep(cap, 0);
     std::vector<uint32_t> reps;
     std::vector<std::vector<uint32_t>> dups;
     for (uint32_t i = 0; i < n; ++i) {
-        auto it = first.find(i);
-        if (it == first.end()) {
-            first.emplace(i, (uint32_t)reps.size());
-            reps.push_back(i);
-            dups.emplace_back();
-        } else {
-            dups[it->second].push_back(i);
+        const uint64_t L = offsets[i + 1] - offsets[i];
+        uint64_t h = hv[i] & (cap - 1);
+        for (;; h = (h + 1) & (cap - 1)) {
+            const uint32_t j = slot_rec[h];
+            if (j == UINT32_MAX) {  // first occurrence
+                slot_rec[h] = i;
+                slot_rep[h] = (uint32_t)reps.size();
+                reps.push_back(i);
+                dups.emplace_back();
+                break;
+            }
+            if (hv[j] == hv[i] && offsets[j + 1] - offsets[j] == L &&
+                std::memcmp(data + offsets[j], data + offsets[i], L) == 0) {
+                dups[slot_rep[h]].push_back(i);
+                break;
+            }
         }
     }
     res.reps = reps;
