@@ -216,9 +216,10 @@ int clu_size(const dm_ctx* ctx, size_t cnt, bool wide, uint32_t mmax, const NwSc
     if (force == 2 || force == 4 || force == 8) return force;
     // clusters of 8 need 8 free SMs of one GPC: beyond ~8 of them at once they
     // queue (measured: 16 x 2,600^2 take 1.48 ms at 8, 0.95 ms at 4)
+    // (2,400^2 alignments, tools/nw_many.py: 32 of them 0.86 ms at 4 vs 1.26 ms
+    // on the ring kernel; 64 at 2: 1.31 vs 1.26 -- the ring kernel from there)
     if (cnt <= 8) return 8;
     if (cnt * 4 <= (size_t)ctx->sm_count - 20) return 4;
-    if (cnt * 2 <= (size_t)ctx->sm_count - 20) return 2;
     return 0;
 }
 
