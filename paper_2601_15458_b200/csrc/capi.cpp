@@ -198,7 +198,8 @@ int dm_seqset_destroy(dm_seqset* s) {
 uint32_t dm_seqset_count(const dm_seqset* s) { return s ? s->n : 0; }
 int dm_seqset_planes(const dm_seqset* s) { return s ? s->planes : 0; }
 
-static void fill_stats(dm_stats* st, const dm::LevTotals& t, float total_ms) {
+static void fill_stats(dm_stats* st, dm::LevTotals& t, float total_ms) {
+    dm::lev_finish_timing(t);
     if (!st) return;
     std::memset(st, 0, sizeof(*st));
     st->kernel_ms = t.kernel_ms;

@@ -241,7 +241,11 @@ struct LevTotals {
     uint64_t cells = 0, cells_exec = 0, launches = 0;
     uint64_t h2d_bytes = 0, d2h_bytes = 0;  // streamed path: bytes actually copied
     float kernel_ms = 0.f;
+    // timed batches whose event pairs are not read yet (no host sync per
+    // batch): kernel_ms is complete after lev_finish_timing
+    std::vector<cudaEvent_t> pend;
 };
+void lev_finish_timing(LevTotals& t);
 
 // Run a batch of device-resident items (already oriented, bucket-sorted
 // by the planner). d_out is indexed by item.slot.

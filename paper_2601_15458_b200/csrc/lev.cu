@@ -397,20 +397,22 @@ void run_planned(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const ui
     LevPlan P;
     plan_batch(ctx, s, d_ia, d_ib, d_in_items, n, P);
     cudaStream_t st = ctx->stream;
-    if (time_kernels) DM_CUDA(cudaEventRecord(ctx->ev0, st));
+    const bool timed = time_kernels && tot;  // event pairs read later (lev_finish_timing): no sync here
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timed) {
+        DM_CUDA(cudaEventCreate(&e0));
+        DM_CUDA(cudaEventCreate(&e1));
+        tot->pend.push_back(e0);
+        tot->pend.push_back(e1);
+        DM_CUDA(cudaEventRecord(e0, st));
+    }
     const int launches = launch_plan(ctx, P, src_of(s), d_out, st);
-    if (time_kernels) DM_CUDA(cudaEventRecord(ctx->ev1, st));
+    if (timed) DM_CUDA(cudaEventRecord(e1, st));
     ctx->launches += launches;
     if (tot) {
         tot->cells += P.hc[0];
         tot->cells_exec += P.hc[1];
         tot->launches += launches + 2;
-        if (time_kernels) {
-            DM_CUDA(cudaEventSynchronize(ctx->ev1));
-            float ms = 0;
-            DM_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-            tot->kernel_ms += ms;
-        }
     }
 }
 
@@ -423,6 +425,17 @@ void ensure_side_streams(dm_ctx* ctx) {
         DM_CUDA(cudaStreamCreateWithPriority(&ctx->lev_side[k], cudaStreamNonBlocking, ctx->side_prio));
         DM_CUDA(cudaEventCreateWithFlags(&ctx->lev_join[k], cudaEventDisableTiming));
     }
+}
+
+void lev_finish_timing(LevTotals& t) {
+    for (size_t i = 0; i + 1 < t.pend.size(); i += 2) {
+        DM_CUDA(cudaEventSynchronize(t.pend[i + 1]));
+        float ms = 0;
+        DM_CUDA(cudaEventElapsedTime(&ms, t.pend[i], t.pend[i + 1]));
+        t.kernel_ms += ms;
+    }
+    for (cudaEvent_t e : t.pend) cudaEventDestroy(e);
+    t.pend.clear();
 }
 
 // Loads every kernel instance up front (lazy module loading would otherwise

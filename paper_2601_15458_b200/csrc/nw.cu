@@ -194,14 +194,17 @@ int group_of(uint32_t n) {
 }
 
 // Throughput form (nw_seq.cuh): one warp per alignment, bands in sequence.
-// Used when a batch holds at least as many alignments as the GPU has
-// resident warps: every warp then has its own work and the multi-warp
-// form's ring hand-off (there to cut one alignment's latency) only costs.
+// Used when a batch holds at least ~4 alignments per SM: every warp then has
+// its own work and the multi-warp form's ring hand-off (there to cut one
+// alignment's latency) only costs.
 bool use_seq(const dm_ctx* ctx, size_t cnt) {
     const char* e = std::getenv("DM_NW_SEQ");  // tests / tuning: 1 always, 0 never
     const int force = e ? std::atoi(e) : -1;
     if (force >= 0) return force > 0;
-    return cnt >= (size_t)ctx->sm_count * 16;
+    // measured on 2,300^2 alignments (tools/nw_many.py): equal at 600, 1.37 vs
+    // 1.00 TCUPS at 1,000 (the ring kernel's per-alignment latency is shorter,
+    // its throughput lower)
+    return cnt >= (size_t)ctx->sm_count * 4;
 }
 
 // Latency form across a cluster (nw_clu.cuh) for batches too small to fill
@@ -534,13 +537,11 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
                 DM_CUDA(cudaEventRecord(ctx->lev_join[k], ctx->lev_side[k]));
                 DM_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->lev_join[k], 0));
             }
-        if (time_kernels) {
-            DM_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
-            DM_CUDA(cudaEventSynchronize(ctx->ev1));
-            float ms = 0;
-            DM_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-            out.fwd_ms += ms;
-            DM_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+        cudaEvent_t ev_fwd = nullptr, ev_tb = nullptr;
+        if (time_kernels) {  // read after the chunk (no host sync between forward and traceback)
+            DM_CUDA(cudaEventCreate(&ev_fwd));
+            DM_CUDA(cudaEventCreate(&ev_tb));
+            DM_CUDA(cudaEventRecord(ev_fwd, ctx->stream));
         }
         nvtxRangePushA("dm nw traceback");
         TbArgs ta{d_jobs, cnt, d_trace, out.d_res, out.d_gaps, d_cnt + kGroups, seq ? 1 : 0};
@@ -548,11 +549,15 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
         nw_traceback_kernel<<<tgrid, 128, 0, ctx->stream>>>(ta);
         DM_CUDA(cudaGetLastError());
         if (time_kernels) {
-            DM_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
-            DM_CUDA(cudaEventSynchronize(ctx->ev1));
-            float ms = 0;
-            DM_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-            out.tb_ms += ms;
+            DM_CUDA(cudaEventRecord(ev_tb, ctx->stream));
+            DM_CUDA(cudaEventSynchronize(ev_tb));
+            float f = 0, t = 0;
+            DM_CUDA(cudaEventElapsedTime(&f, ctx->ev0, ev_fwd));
+            DM_CUDA(cudaEventElapsedTime(&t, ev_fwd, ev_tb));
+            out.fwd_ms += f;
+            out.tb_ms += t;
+            cudaEventDestroy(ev_fwd);
+            cudaEventDestroy(ev_tb);
         }
         out.launches += 1;
         ctx->launches += 1;

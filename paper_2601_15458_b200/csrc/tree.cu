@@ -686,6 +686,7 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
         NvtxRange nvtx_level("dm tree level");
         const size_t B = big.size();
         const auto t0 = tnow();
+        if (trace) lev_finish_timing(tot);
         const float k0 = tot.kernel_ms;
         // One rank (or an owned subtree): the jobs of every batch are generated
         // on the device from the candidate lists / node slices and the level's
@@ -858,6 +859,7 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
         }
         if (trace) {
             const auto t5 = tnow();
+            lev_finish_timing(tot);
             uint64_t mem = 0;
             for (size_t v = 0; v < B; ++v) mem += ne[v] - nb[v];
             std::fprintf(stderr,
@@ -1029,6 +1031,7 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
         st->cells += tot.cells;
         st->cells_executed += tot.cells_exec;
         st->launches += tot.launches;
+        lev_finish_timing(tot);
         st->kernel_ms += tot.kernel_ms;
     }
 }
