@@ -174,6 +174,7 @@ def msa_bench(dm, ctx, cfgs, reps, world, rank):
         n = len(offs) - 1
         offs_c = np.ascontiguousarray(offs, dtype=np.uint64)
         best = None
+        first_wall = None
         for _ in range(reps):
             rows = C.c_void_p()
             width = C.c_uint64()
@@ -192,6 +193,8 @@ def msa_bench(dm, ctx, cfgs, reps, world, rank):
                 t = torch.tensor([wall], dtype=torch.float64, device="cuda")
                 torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
                 wall = float(t[0])
+            if first_wall is None:
+                first_wall = wall
             W = width.value
             buf = np.ctypeslib.as_array(C.cast(rows, C.POINTER(C.c_uint8)), shape=(max(1, n * W),))[:n * W]
             flat = np.concatenate([buf.reshape(n, W), np.full((n, 1), 10, np.uint8)], axis=1)
@@ -208,7 +211,9 @@ def msa_bench(dm, ctx, cfgs, reps, world, rank):
         if world > 1:
             from paper_2601_15458_b200.dist import comm_stats
             best["comm"] = comm_stats(ctx)
-        entry = {"n": n, "width": best["width"], "wall_s": best["wall_s"], "tree_ms": best["tree_ms"],
+        entry = {"n": n, "width": best["width"], "wall_s": best["wall_s"],
+                 # the first call on this context also maps the NW trace pool
+                 "wall_s_first_call": first_wall, "tree_ms": best["tree_ms"],
                  "align_ms": best["align_ms"], "cells": best["cells"],
                  "gcups_e2e": best["cells"] / best["wall_s"] / 1e9, "gpu_launches": best["launches"],
                  "n_gpus": world, "rows_sha256_matches_reference": match}
