@@ -545,13 +545,6 @@ void lev_plan_then_launch(dm_ctx* prep, dm_ctx* ctx, const dm_seqset* s, const u
 
 // ---- host-planned chunks of identity pairs (the streamed path, stream.cu)
 
-namespace {
-std::vector<uint32_t>& tmp2_of(const std::vector<uint32_t>& t) {  // second scratch, per planning thread
-    thread_local std::vector<uint32_t> v;
-    (void)t;
-    return v;
-}
-}  // namespace
 
 bool lev_plan_host_pairs(const uint64_t* offs, uint64_t cnt, uint64_t slot0, int sm_count, int wsel_cap,
                          LevItem* items, unsigned int* hist, unsigned long long* cells, std::vector<uint32_t>& tmp) {
@@ -606,7 +599,7 @@ bool lev_plan_host_pairs(const uint64_t* offs, uint64_t cnt, uint64_t slot0, int
     int dense[kBuckets], nd = 0;
     for (int bk = 0; bk < kBuckets; ++bk) dense[bk] = hist[bk] ? nd++ : -1;  // ascending bucket ids
     const uint32_t range = lbmax - lbmin + 1;
-    std::vector<uint32_t>& pos = tmp2_of(tmp);
+    thread_local std::vector<uint32_t> pos;  // counting-sort table, per planning thread
     pos.assign((size_t)nd * range + 1, 0u);
     for (uint64_t i = 0; i < cnt; ++i)
         ++pos[(size_t)dense[key[i] >> 13] * range + ((key[i] & (kLenBins - 1)) - lbmin) + 1];
