@@ -130,6 +130,7 @@ struct dm_ctx {
     static constexpr int kLevSide = 8;  // side streams the distance buckets fan out on
     int side_prio = 0;                  // their priority (dm_ctx_create: the greatest; 0 = default, the least)
     dm_ctx* tree_bg = nullptr;          // low-priority context for the tree's background batches (tree.cu)
+    uint32_t lev_waves = 0;             // distance-kernel grids in waves of resident blocks (0: default 4)
     cudaStream_t lev_side[kLevSide] = {};
     int lev_rr = 0;
     cudaEvent_t lev_fork = nullptr, lev_join[kLevSide] = {};

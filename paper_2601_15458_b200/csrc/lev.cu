@@ -378,6 +378,7 @@ int launch_plan(dm_ctx* ctx, const LevPlan& P, const LevSrc& S, uint32_t* d_out,
         a.out = d_out;
         a.counter = P.counters + b;
         a.one = 1u;
+        a.waves = ctx->lev_waves;
         cudaStream_t ls = fork ? ctx->lev_side[used[i % nused]] : st;
         if (S.src == kSrcPlanes) launch_bucket(S.np, b % 32, a, ctx->sm_count, ls);
         else lev_launch_bucket_src(S.src, b % 32, a, ctx->sm_count, ls);

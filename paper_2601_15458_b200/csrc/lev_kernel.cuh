@@ -26,6 +26,7 @@ struct LevArgs {
     uint32_t* counter;
     uint32_t one;        // == 1; opaque to ptxas so the carry chains stay on the FMA pipe
     uint32_t max_pulls;  // task pulls per warp before its block retires (see launch_one)
+    uint32_t waves;      // host only: grid in waves of resident blocks (0: DM_LEV_WAVES, default 4)
     // multi-pass mode (LONG kernels, patterns longer than one warp's rows):
     // pass `pass` covers pattern rows [pass * 1024 W, (pass + 1) * 1024 W);
     // hbuf + hoff[item] holds, per text column, the horizontal delta leaving
@@ -429,7 +430,7 @@ void launch_one(const LevArgs& a, int sm_count, cudaStream_t st) {
     const uint64_t tasks = ((uint64_t)a.nitems + (32u >> a.lgG) - 1) / (32u >> a.lgG);
     const uint64_t resident = (uint64_t)occ * sm_count;
     const uint64_t want = (tasks + 7) / 8;  // blocks if every warp pulled once
-    const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(want, resident * kWaves));
+    const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(want, resident * (a.waves ? a.waves : kWaves)));
     LevArgs b = a;
     b.max_pulls = (uint32_t)((tasks + grid * 8 - 1) / (grid * 8));
     lev_kernel<NP, W, LONG, SRC><<<(unsigned)grid, 256, smem, st>>>(b);

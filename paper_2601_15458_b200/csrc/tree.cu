@@ -486,6 +486,10 @@ dm_ctx* tree_bg_context(dm_ctx* ctx) {
         }
         p->own_stream = p->stream;
         p->side_prio = 0;
+        // short-lived blocks: the foreground batches' kernels (higher priority)
+        // take SM slots as soon as a background block retires -- there is no
+        // preemption, and 4-wave blocks held slots for ~1/4 of a batch
+        p->lev_waves = 32;
         DM_CUDA(cudaEventCreate(&p->ev0));
         DM_CUDA(cudaEventCreate(&p->ev1));
         ctx->tree_bg = p;
