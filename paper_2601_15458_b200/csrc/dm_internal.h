@@ -55,6 +55,18 @@ struct DevBuf {
     }
     template <class T>
     T* as(size_t count) { return static_cast<T*>(get(count * sizeof(T))); }
+    // grow to exactly `bytes` (no slack): for large one-off reservations
+    void reserve_exact(size_t bytes) {
+        if (bytes <= cap) return;
+        if (p) {
+            if (sp) cudaFreeAsync(p, *sp);
+            else cudaFree(p);
+        }
+        p = nullptr;
+        if (sp) DM_CUDA(cudaMallocAsync(&p, bytes, *sp));
+        else DM_CUDA(cudaMalloc(&p, bytes));
+        cap = bytes;
+    }
     DevBuf() = default;
     explicit DevBuf(cudaStream_t* s) : sp(s) {}
     DevBuf(const DevBuf&) = delete;

@@ -282,6 +282,34 @@ dm_msa_out* align_all(dm_ctx* ctx, const dm_seqset* s, const std::vector<dm_node
             by_depth[nd.depth].push_back((uint32_t)v);
             maxdepth = std::max(maxdepth, nd.depth);
         }
+        // The NW trace of the largest level, estimated from the tree and mapped
+        // once up front: growing the buffer level by level made the pool map
+        // fresh memory several times on a context's first call (~60 GB for
+        // cfg4). Widths are estimated as the subtree's longest sequence times
+        // 1 + 2 % per merge above it (cfg4: 2,620 measured vs ~2,800
+        // estimated at the root); an underestimate only means later growth.
+        {
+            std::vector<uint32_t> sub_len(nodes.size(), 0), height(nodes.size(), 0);
+            for (size_t v = nodes.size(); v-- > 0;) {  // BFS numbering: children after parents
+                const dm_node& nd = nodes[v];
+                if (nd.left < 0) {
+                    sub_len[v] = s->len[nd.center];
+                    continue;
+                }
+                sub_len[v] = std::max(sub_len[nd.left], sub_len[nd.right]);
+                height[v] = 1 + std::max(height[nd.left], height[nd.right]);
+            }
+            auto west = [&](size_t v) { return (double)sub_len[v] * (1.0 + 0.02 * height[v]) + 1.0; };
+            std::vector<double> lvl((size_t)maxdepth + 1, 0.0);
+            for (size_t v = 0; v < nodes.size(); ++v)
+                if (nodes[v].left >= 0)
+                    lvl[nodes[v].depth] += (west(nodes[v].left) + 32.0) * (west(nodes[v].right) + 32.0);
+            double mx = 0;
+            for (double x : lvl) mx = std::max(mx, x);
+            const uint64_t cap = std::max<uint64_t>(6ull << 30, ctx->free_at_create / 100 * 45);
+            const uint64_t want = std::min<uint64_t>((uint64_t)(mx * 1.05), cap);
+            if (want > (64ull << 20)) ctx->nw_trace.reserve_exact(want);
+        }
         uint64_t pitch = ((uint64_t)maxlen + maxlen / 2 + 64 + 63) & ~uint64_t(63);
         DevBuf& rowsbuf = ctx->rows_a;
         rowsbuf.get((uint64_t)n * pitch);
