@@ -12,10 +12,16 @@ pytestmark = pytest.mark.gpu
 
 
 
-@pytest.fixture(autouse=True, params=["ring", "seq"])
+@pytest.fixture(autouse=True, params=["default", "seq", "ring"])
 def nw_kernel(request, monkeypatch):
-    """MSA parity with the merges on either forward kernel (see test_nw_gpu.py)."""
-    monkeypatch.setenv("DM_NW_SEQ", "1" if request.param == "seq" else "0")
+    """MSA parity with the merges on the library's own kernel choice per level
+    (cluster / ring / throughput by batch size), on the throughput kernel
+    only, and on the ring kernel only (see test_nw_gpu.py)."""
+    if request.param == "seq":
+        monkeypatch.setenv("DM_NW_SEQ", "1")
+    elif request.param == "ring":
+        monkeypatch.setenv("DM_NW_SEQ", "0")
+        monkeypatch.setenv("DM_NW_CLU", "0")
     return request.param
 
 def rand_str(rng, n, alphabet="ACGT"):
@@ -122,6 +128,18 @@ def test_protein_vs_reference(dm, ctx, ref):
     seqs = unique(families(rng, 8, 40, 150, 0.1, "ARNDCQEGHILKMFPSTWYV"))
     m = dm.msa(dm.SeqSet(seqs, ctx), dm.ScoringScheme.protein())
     _check_same(m, _ref_msa(ref, seqs, kind="aa"))
+
+
+@pytest.mark.timeout(900)
+def test_long_sequences_vs_reference(dm, ctx, ref, nw_kernel):
+    """~3,800-residue families: merges of more than 4,096 rows (cluster kernel
+    rounds with the row hand-off reused in place, ring-kernel wrap rows),
+    traces of several hundred MB, byte-identical to the reference."""
+    rng = random.Random(3800)
+    seqs = unique(families(rng, 4, 10, 3800, 0.03))
+    m = dm.msa(dm.SeqSet(seqs, ctx), dm.ScoringScheme.nucleotide())
+    _check_same(m, _ref_msa(ref, seqs))
+    assert m.width > 4096
 
 
 def test_cfg0_full_vs_reference(dm, ctx, ref):
