@@ -135,8 +135,12 @@ def test_families_determinism(dm, ctx, ref):
     _same(t1, ref.build_tree(seqs, seed=5))
 
 
+@pytest.mark.parametrize("bg", ["1", "0"])
 @pytest.mark.parametrize("alphabet", ["ACGT", "ARNDCQEGHILKMFPSTWYV"])
-def test_medium_vs_reference(dm, ctx, ref, alphabet):
+def test_medium_vs_reference(dm, ctx, ref, alphabet, bg, monkeypatch):
+    """bg: the small subtrees' matrices on the background worker (default) or
+    in the foreground after the levels (DM_TREE_BG=0)."""
+    monkeypatch.setenv("DM_TREE_BG", bg)
     rng = random.Random(77)
     seqs = unique(mutation_families(rng, 10, 80, 120, 0.1, alphabet))
     ss = dm.SeqSet(seqs, ctx)
