@@ -57,6 +57,8 @@ typedef struct {
     double tree_ms, align_ms; /* dm_msa: phase times; dm_nw_*: align_ms = forward-pass kernel time */
     uint64_t lev_calls, nw_calls;
     uint64_t h2d_bytes, d2h_bytes; /* dm_lev_pairs_packed: bytes that crossed PCIe */
+    uint64_t cells_reused;   /* guide tree (ABI 2): cells of distance jobs answered from the
+                                build's table of pairs already computed (not in `cells`) */
 } dm_stats;
 
 const char* dm_last_error(void);

@@ -42,7 +42,7 @@ class dm_stats(C.Structure):
     _fields_ = [("kernel_ms", C.c_double), ("total_ms", C.c_double), ("cells", C.c_uint64),
                 ("cells_executed", C.c_uint64), ("launches", C.c_uint64), ("tree_ms", C.c_double),
                 ("align_ms", C.c_double), ("lev_calls", C.c_uint64), ("nw_calls", C.c_uint64),
-                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
+                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("cells_reused", C.c_uint64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

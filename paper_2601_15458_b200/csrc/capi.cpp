@@ -60,7 +60,7 @@ using dm::require;
 extern "C" {
 
 const char* dm_last_error(void) { return dm::last_error().c_str(); }
-int dm_abi_version(void) { return 1; }
+int dm_abi_version(void) { return 2; }
 
 int dm_ctx_create(int device, dm_ctx** out) {
     return guard([&] {

@@ -250,8 +250,31 @@ struct LevItem {
     uint64_t slot;  // 64-bit: per-level candidate matrices can exceed 2^32 cells
 };
 
+// Device table of distances already computed in one guide-tree build
+// (tree.cu): open addressing, key = min(a, b) << 32 | max(a, b) (sequence
+// ids; Levenshtein is symmetric), linear probing. The tree asks for the same
+// pair again across its phases -- a node's center is one of its median
+// candidates, a child's median sample and a small subtree's all-pairs matrix
+// overlap the parent's candidate matrix and pole sweeps -- and the planner
+// answers those jobs (and a == b: 0) from here instead of launching them.
+// Distances are deterministic, so a hit returns exactly what the kernel
+// would. Lookups may run concurrently with inserts (the tree's background
+// batches): a key whose value is still kCacheNone reads as a miss.
+struct DistCache {
+    unsigned long long* keys = nullptr;  // kCacheEmpty = free
+    uint32_t* vals = nullptr;            // kCacheNone = not written yet
+    unsigned int* fill = nullptr;        // inserted keys (device counter)
+    uint64_t mask = 0;                   // capacity - 1 (power of two)
+    unsigned int max_fill = 0;           // inserts stop here (load factor bound)
+    bool insert = false;                 // this batch adds its results
+    bool on() const { return keys != nullptr; }
+};
+constexpr unsigned long long kCacheEmpty = ~0ull;
+constexpr uint32_t kCacheNone = 0xffffffffu;
+
 struct LevTotals {
     uint64_t cells = 0, cells_exec = 0, launches = 0;
+    uint64_t reused = 0, cells_reused = 0;  // jobs answered by a DistCache (or a == b)
     uint64_t h2d_bytes = 0, d2h_bytes = 0;  // streamed path: bytes actually copied
     float kernel_ms = 0.f;
     // timed batches whose event pairs are not read yet (no host sync per
@@ -297,9 +320,11 @@ struct LevArgs;
 void lev_launch_bucket_src(int src, int w, const LevArgs& a, int sm_count, cudaStream_t st);
 void lev_warm_src();
 // Jobs already on the device (one rank: no sharding), e.g. generated by the
-// tree builder's item kernels.
+// tree builder's item kernels. cache (optional): jobs whose pair it holds,
+// and a == b, are answered by the planner and never launched; with
+// cache->insert the computed ones are added after the batch.
 void lev_run_device_items(dm_ctx* ctx, const dm_seqset* s, const LevItem* d_items, uint64_t n, uint32_t* d_out,
-                          LevTotals* tot, bool time_kernels);
+                          LevTotals* tot, bool time_kernels, const DistCache* cache = nullptr);
 void lev_run_device_pairs(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia,
                           const uint32_t* d_ib, uint64_t n, uint32_t* d_out, LevTotals* tot,
                           bool time_kernels);

@@ -115,6 +115,50 @@ void launch_bucket(int np, int w, const LevArgs& a, int sm, cudaStream_t st) {
 constexpr int kBuckets = 6 * 32;  // (log2 G) * 32 + W
 constexpr int kLevSide = dm_ctx::kLevSide;
 
+// ---- DistCache (dm_internal.h): open addressing, linear probing
+__device__ __forceinline__ unsigned long long cache_key(uint32_t a, uint32_t b) {
+    return a < b ? ((unsigned long long)a << 32 | b) : ((unsigned long long)b << 32 | a);
+}
+__device__ __forceinline__ uint64_t cache_slot(unsigned long long k, uint64_t mask) {
+    k ^= k >> 33;  // murmur3 finaliser
+    k *= 0xff51afd7ed558ccdull;
+    k ^= k >> 33;
+    k *= 0xc4ceb9fe1a85ec53ull;
+    k ^= k >> 33;
+    return k & mask;
+}
+constexpr int kCacheProbes = 64;  // bounded chains: a miss past them only costs the launch
+
+__device__ bool cache_find(const DistCache& dc, uint32_t a, uint32_t b, uint32_t& d) {
+    const unsigned long long key = cache_key(a, b);
+    uint64_t h = cache_slot(key, dc.mask);
+    for (int p = 0; p < kCacheProbes; ++p, h = (h + 1) & dc.mask) {
+        const unsigned long long k = *(volatile const unsigned long long*)(dc.keys + h);
+        if (k == kCacheEmpty) return false;
+        if (k == key) {
+            const uint32_t v = *(volatile const uint32_t*)(dc.vals + h);
+            if (v == kCacheNone) return false;  // being inserted (background batch): a miss
+            d = v;
+            return true;
+        }
+    }
+    return false;
+}
+
+__device__ void cache_put(const DistCache& dc, uint32_t a, uint32_t b, uint32_t d) {
+    if (a == b || *(volatile unsigned int*)dc.fill >= dc.max_fill) return;
+    const unsigned long long key = cache_key(a, b);
+    uint64_t h = cache_slot(key, dc.mask);
+    for (int p = 0; p < kCacheProbes; ++p, h = (h + 1) & dc.mask) {
+        const unsigned long long prev = atomicCAS(dc.keys + h, kCacheEmpty, key);
+        if (prev == kCacheEmpty || prev == key) {
+            if (prev == kCacheEmpty) atomicAdd(dc.fill, 1u);
+            dc.vals[h] = d;  // the same value whoever writes it
+            return;
+        }
+    }
+}
+
 // Orient each job (shorter string = pattern), pick (G, R) and build the
 // radix key (bucket << 32 | ~n) so one sort groups buckets and balances warps.
 __global__ void plan_kernel(const uint32_t* __restrict__ ia, const uint32_t* __restrict__ ib,
@@ -122,13 +166,13 @@ __global__ void plan_kernel(const uint32_t* __restrict__ ia, const uint32_t* __r
                             const uint32_t* __restrict__ len, int lg_gpar, int wsel, int wmax,
                             LevItem* __restrict__ items, uint64_t* __restrict__ keys,
                             uint32_t* __restrict__ idx, unsigned int* __restrict__ hist,
-                            unsigned long long* __restrict__ cells) {
+                            unsigned long long* __restrict__ cells, const DistCache dc, uint32_t* __restrict__ out) {
     __shared__ unsigned int sh[kBuckets];
-    __shared__ unsigned long long scells[2];
+    __shared__ unsigned long long scells[3];
     for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) sh[i] = 0;
-    if (threadIdx.x < 2) scells[threadIdx.x] = 0;
+    if (threadIdx.x < 3) scells[threadIdx.x] = 0;
     __syncthreads();
-    unsigned long long c0 = 0, c1 = 0;
+    unsigned long long c0 = 0, c1 = 0, c2 = 0;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         uint32_t x, y;
@@ -146,6 +190,18 @@ __global__ void plan_kernel(const uint32_t* __restrict__ ia, const uint32_t* __r
         if (lx > ly) {  // pattern = shorter
             const uint32_t t = x; x = y; y = t;
             const uint32_t tl = lx; lx = ly; ly = tl;
+        }
+        if (dc.keys) {  // answered without a launch: bucket 0 (never launched)
+            uint32_t d = 0;
+            if (x == y || cache_find(dc, x, y, d)) {
+                out[slot] = d;
+                items[i] = LevItem{x, y, slot};
+                keys[i] = 0;
+                idx[i] = (uint32_t)i;
+                atomicAdd(&sh[0], 1u);
+                c2 += (unsigned long long)lx * ly;
+                continue;
+            }
         }
         const uint32_t B = (lx + 31) >> 5;  // 32-row words of the pattern
         int lg = lg_gpar;
@@ -168,12 +224,24 @@ __global__ void plan_kernel(const uint32_t* __restrict__ ia, const uint32_t* __r
     }
     atomicAdd(&scells[0], c0);
     atomicAdd(&scells[1], c1);
+    if (c2) atomicAdd(&scells[2], c2);
     __syncthreads();
     for (int i = threadIdx.x; i < kBuckets; i += blockDim.x)
         if (sh[i]) atomicAdd(&hist[i], sh[i]);
     if (threadIdx.x == 0) {
         atomicAdd(&cells[0], scells[0]);
         atomicAdd(&cells[1], scells[1]);
+        atomicAdd(&cells[2], scells[2]);
+    }
+}
+
+// The computed jobs of a batch (planned items past bucket 0) into the cache.
+__global__ void cache_insert_kernel(const LevItem* __restrict__ items, uint64_t n, const uint32_t* __restrict__ out,
+                                    const DistCache dc) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const LevItem it = items[i];
+        cache_put(dc, it.pat, it.txt, out[it.slot]);
     }
 }
 
@@ -188,7 +256,7 @@ struct LevPlan {
     LevItem* items = nullptr;
     uint32_t* counters = nullptr;
     unsigned int h[kBuckets];
-    unsigned long long hc[2];
+    unsigned long long hc[3];  // cells, cells executed, cells answered by the cache
 };
 
 // plan_kernel's histogram and cell counts for pairs (2i, 2i+1) of host
@@ -221,6 +289,7 @@ void plan_hist_host(const uint64_t* offs, uint64_t n, int lg_gpar, int wsel, int
     for (int k = 0; k < kBuckets; ++k) P.h[k] = h[k] + h[kBuckets + k] + h[2 * kBuckets + k] + h[3 * kBuckets + k];
     P.hc[0] = c0;
     P.hc[1] = c1;
+    P.hc[2] = 0;
 }
 
 // Planner phase on `ctx`'s stream (scratch from ctx): orient, bucket, sort,
@@ -228,7 +297,8 @@ void plan_hist_host(const uint64_t* offs, uint64_t n, int lg_gpar, int wsel, int
 // host offsets of identity pairs (2i, 2i+1), count it on the host and stay
 // asynchronous.
 void plan_batch(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const uint32_t* d_ib,
-                const LevItem* d_in_items, uint64_t n, LevPlan& P, const uint64_t* pair_offs = nullptr) {
+                const LevItem* d_in_items, uint64_t n, LevPlan& P, const uint64_t* pair_offs = nullptr,
+                const DistCache* dc = nullptr, uint32_t* d_out = nullptr) {
     if (n > 0xffffffffull) throw invalid_argument("too many distance jobs in one batch");
     cudaStream_t st = ctx->stream;
     const int np = s->planes;
@@ -254,7 +324,7 @@ void plan_batch(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const uin
     cub::DeviceRadixSort::SortPairs(nullptr, cub_b, (uint64_t*)nullptr, (uint64_t*)nullptr,
                                     (uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 0, 40, st);
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-    const size_t hist_b = al(kBuckets * 4 + 16 + kBuckets * 4);
+    const size_t hist_b = al(kBuckets * 4 + 32 + kBuckets * 4);
     size_t total = al(item_b) * 2 + al(key_b) * 2 + al(idx_b) * 2 + hist_b + al(cub_b);
     char* base = (char*)ctx->items.get(total);
     LevItem* it0 = (LevItem*)base; base += al(item_b);
@@ -265,14 +335,14 @@ void plan_batch(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const uin
     uint32_t* i1 = (uint32_t*)base; base += al(idx_b);
     unsigned int* hist = (unsigned int*)base;
     unsigned long long* cells = (unsigned long long*)(hist + kBuckets);
-    uint32_t* counters = (uint32_t*)(cells + 2);
+    uint32_t* counters = (uint32_t*)(cells + 4);
     base += hist_b;
     void* cub_tmp = base;
 
     DM_CUDA(cudaMemsetAsync(hist, 0, hist_b, st));
     const int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)ctx->sm_count * 8);
     plan_kernel<<<grid, 256, 0, st>>>(d_ia, d_ib, d_in_items, n, s->d_len, lg_gpar, wsel, wmax, it0, k0, i0,
-                                      hist, cells);
+                                      hist, cells, dc ? *dc : DistCache{}, d_out);
     DM_CUDA(cudaGetLastError());
     DM_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_b, k0, k1, i0, i1, (int)n, 0, 40, st));
     gather_items<<<grid, 256, 0, st>>>(it0, i1, n, it1);
@@ -328,7 +398,7 @@ int launch_plan(dm_ctx* ctx, const LevPlan& P, const LevSrc& S, uint32_t* d_out,
     for (int b = 0; b < kBuckets; ++b) {
         starts[b] = start;
         start += P.h[b];
-        if (P.h[b]) order[nb++] = b;
+        if (P.h[b] && b != 0) order[nb++] = b;  // bucket 0: answered by the planner (DistCache)
     }
     // the multi-pass bucket (largest work per job) is first in `order`:
     // it goes to the first side stream and syncs that stream once to size
@@ -393,10 +463,10 @@ int launch_plan(dm_ctx* ctx, const LevPlan& P, const LevSrc& S, uint32_t* d_out,
 
 void run_planned(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const uint32_t* d_ib,
                  const LevItem* d_in_items, uint64_t n, uint32_t* d_out, LevTotals* tot,
-                 bool time_kernels) {
+                 bool time_kernels, const DistCache* dc = nullptr) {
     if (n == 0) return;
     LevPlan P;
-    plan_batch(ctx, s, d_ia, d_ib, d_in_items, n, P);
+    plan_batch(ctx, s, d_ia, d_ib, d_in_items, n, P, nullptr, dc, d_out);
     cudaStream_t st = ctx->stream;
     const bool timed = time_kernels && tot;  // event pairs read later (lev_finish_timing): no sync here
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -407,12 +477,21 @@ void run_planned(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia, const ui
         tot->pend.push_back(e1);
         DM_CUDA(cudaEventRecord(e0, st));
     }
-    const int launches = launch_plan(ctx, P, src_of(s), d_out, st);
+    int launches = launch_plan(ctx, P, src_of(s), d_out, st);
     if (timed) DM_CUDA(cudaEventRecord(e1, st));
+    if (dc && dc->insert && n > P.h[0]) {
+        const uint64_t m = n - P.h[0];
+        const int grid = (int)std::min<uint64_t>((m + 255) / 256, (uint64_t)ctx->sm_count * 8);
+        cache_insert_kernel<<<grid, 256, 0, st>>>(P.items + P.h[0], m, d_out, *dc);
+        DM_CUDA(cudaGetLastError());
+        ++launches;
+    }
     ctx->launches += launches;
     if (tot) {
         tot->cells += P.hc[0];
         tot->cells_exec += P.hc[1];
+        tot->reused += P.h[0];
+        tot->cells_reused += P.hc[2];
         tot->launches += launches + 2;
     }
 }
@@ -508,8 +587,8 @@ void lev_run_host_items(dm_ctx* ctx, const dm_seqset* s, std::vector<LevItem>& i
 }
 
 void lev_run_device_items(dm_ctx* ctx, const dm_seqset* s, const LevItem* d_items, uint64_t n, uint32_t* d_out,
-                          LevTotals* tot, bool time_kernels) {
-    run_planned(ctx, s, nullptr, nullptr, d_items, n, d_out, tot, time_kernels);
+                          LevTotals* tot, bool time_kernels, const DistCache* cache) {
+    run_planned(ctx, s, nullptr, nullptr, d_items, n, d_out, tot, time_kernels, cache);
 }
 
 void lev_run_device_pairs(dm_ctx* ctx, const dm_seqset* s, const uint32_t* d_ia,

@@ -392,11 +392,11 @@ void download(dm_ctx* ctx, std::vector<T>& v, const T* d, size_t n) {
 
 struct TreeScratch {
     DevBuf order, tmp, dc, dl, dr, mat, matoff, kk, cand, candoff, nb, ne, res1, res2, res3, res4, res5, res6, sub_begin,
-        sub_k, sub_mat, sub_matoff, sub_recoff, sub_recs, err, items, itemoff;
+        sub_k, sub_mat, sub_matoff, sub_recoff, sub_recs, err, items, itemoff, ckeys, cvals, cfill;
     explicit TreeScratch(cudaStream_t* s) {
         for (DevBuf* b : {&order, &tmp, &dc, &dl, &dr, &mat, &matoff, &kk, &cand, &candoff, &nb, &ne, &res1, &res2,
                           &res3, &res4, &res5, &res6, &sub_begin, &sub_k, &sub_mat, &sub_matoff, &sub_recoff, &sub_recs, &err,
-                          &items, &itemoff})
+                          &items, &itemoff, &ckeys, &cvals, &cfill})
             b->sp = s;
     }
 };
@@ -526,6 +526,38 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
     uint32_t* d_dr = sc.dr.as<uint32_t>(n);
     std::vector<LevItem> items;
 
+    // Distances already computed in this build (DistCache, dm_internal.h):
+    // the device-item batches (one rank, or subtrees a rank owns) look their
+    // pairs up and add their results; ~30 % of the tree's cells are pairs it
+    // asked for before (a center is a median candidate, a child's sample and
+    // a small subtree's matrix overlap the parent's matrix and pole sweeps).
+    // Sized for ~256 inserts per sequence (cfg4: ~135); inserts stop at a
+    // 5/8 load, lookups never fail.
+    // DM_TREE_CACHE=0 turns it off; =k (10 <= k <= 30) forces 2^k slots (tests:
+    // a full table, long probe chains).
+    DistCache cache, cache_ins;
+    const int cache_env = [] {
+        const char* e = std::getenv("DM_TREE_CACHE");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (n > T && cache_env != 0) {
+        uint64_t cap = 1ull << 12;
+        while (cap < (uint64_t)n * 256 && cap < (1ull << 28)) cap <<= 1;
+        if (cache_env >= 10 && cache_env <= 30) cap = 1ull << cache_env;
+        cache.keys = sc.ckeys.as<unsigned long long>(cap);
+        cache.vals = sc.cvals.as<uint32_t>(cap);
+        cache.fill = sc.cfill.as<unsigned int>(1);
+        cache.mask = cap - 1;
+        cache.max_fill = (unsigned int)(cap / 8 * 5);
+        DM_CUDA(cudaMemsetAsync(cache.keys, 0xff, cap * sizeof(unsigned long long), stream));
+        DM_CUDA(cudaMemsetAsync(cache.vals, 0xff, cap * sizeof(uint32_t), stream));
+        DM_CUDA(cudaMemsetAsync(cache.fill, 0, sizeof(unsigned int), stream));
+        cache_ins = cache;
+        cache_ins.insert = true;
+    }
+    const DistCache* dc_look = cache.on() ? &cache : nullptr;       // lookups only
+    const DistCache* dc_ins = cache.on() ? &cache_ins : nullptr;    // lookups + inserts
+
     const bool trace = std::getenv("DM_TRACE") != nullptr;
     auto tnow = [&] {
         if (trace) DM_CUDA(cudaStreamSynchronize(stream));
@@ -635,7 +667,7 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
                         d_order, upload(bg, b_soff, job.soff), upload(bg, b_sk, job.sk), upload(bg, b_moff, job.moff),
                         upload(bg, b_ioff, job.ioff), d_items);
                     DM_CUDA(cudaGetLastError());
-                    lev_run_device_items(bg, s, d_items, job.itot, d_submat, &bgs.tot, false);
+                    lev_run_device_items(bg, s, d_items, job.itot, d_submat, &bgs.tot, false, dc_look);
                     bgs.tot.launches += 1;
                 }
             } catch (...) {
@@ -739,7 +771,7 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
             pair_items_kernel<<<(unsigned)B, 128, 0, stream>>>(d_cand, d_candoff, d_kk, d_matoff,
                                                                upload(ctx, sc.itemoff, item_off), d_items);
             DM_CUDA(cudaGetLastError());
-            lev_run_device_items(ctx, s, d_items, itot, d_mat, &tot, timing);
+            lev_run_device_items(ctx, s, d_items, itot, d_mat, &tot, timing, dc_ins);
         } else {
             lev_run_host_items(ctx, s, items, d_mat, &tot, timing, owned);
         }
@@ -771,7 +803,7 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
                 sweep_items_kernel<<<(unsigned)B, 256, 0, stream>>>(d_from, d_order, d_nb, d_ne, d_sweepoff, d_items);
                 DM_CUDA(cudaGetLastError());
                 const auto a1 = tnow();
-                lev_run_device_items(ctx, s, d_items, nsweep, d_dist, &tot, timing);
+                lev_run_device_items(ctx, s, d_items, nsweep, d_dist, &tot, timing, dc_ins);
                 sw_build += ms(a0, a1);
                 sw_run += ms(a1, tnow());
                 return;
@@ -891,6 +923,8 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
         }
         tot.cells += bgs.tot.cells;
         tot.cells_exec += bgs.tot.cells_exec;
+        tot.reused += bgs.tot.reused;
+        tot.cells_reused += bgs.tot.cells_reused;
         tot.launches += bgs.tot.launches;
         ctx->launches += bg->launches;
         bg->launches = 0;
@@ -935,7 +969,7 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
             pair_items_kernel<<<(unsigned)S, 128, 0, stream>>>(d_order, upload(ctx, sc.candoff, soff), d_sk, d_smatoff,
                                                                upload(ctx, sc.itemoff, ioff), d_items);
             DM_CUDA(cudaGetLastError());
-            lev_run_device_items(ctx, s, d_items, itot, d_mat, &tot, timing);
+            lev_run_device_items(ctx, s, d_items, itot, d_mat, &tot, timing, dc_look);
             ctx->launches += 1;
             tot.launches += 1;
         } else {
@@ -1031,9 +1065,13 @@ void build_tree(dm_ctx* ctx, const dm_seqset* s, uint64_t seed, uint64_t exact_c
         d.depth = p.depth;
         nodes_out.push_back(d);
     }
+    if (trace)
+        std::fprintf(stderr, "[dm tree] distance cache: %llu jobs / %.3e cells answered without a launch, %.3e computed\n",
+                     (unsigned long long)tot.reused, (double)tot.cells_reused, (double)tot.cells);
     if (st) {
         st->cells += tot.cells;
         st->cells_executed += tot.cells_exec;
+        st->cells_reused += tot.cells_reused;
         st->launches += tot.launches;
         lev_finish_timing(tot);
         st->kernel_ms += tot.kernel_ms;

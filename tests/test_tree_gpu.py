@@ -159,3 +159,28 @@ def test_cfg3_slice_vs_reference(dm, ctx, ref):
     seqs = unique(dm.split(data, offs))
     ss = dm.SeqSet(seqs, ctx)
     _same(dm.build_tree(ss, seed=42), ref.build_tree(seqs, seed=42))
+
+
+@pytest.mark.parametrize("cache", ["1", "0", "10", "12"])
+@pytest.mark.parametrize("bg", ["1", "0"])
+def test_distance_cache_vs_reference(dm, ctx, ref, cache, bg, monkeypatch):
+    """The build's table of pairs already computed (DistCache): on by default
+    (a share of the tree's cells answered without a launch), off
+    (DM_TREE_CACHE=0), and forced to 2^10 / 2^12 slots (inserts stop at a
+    5/8 load, lookups walk long probe chains). The tree is the reference's
+    in every mode, with the small subtrees in the background or not."""
+    monkeypatch.setenv("DM_TREE_CACHE", cache)
+    monkeypatch.setenv("DM_TREE_BG", bg)
+    rng = random.Random(91)
+    seqs = unique(mutation_families(rng, 12, 70, 90, 0.12))
+    ss = dm.SeqSet(seqs, ctx)
+    nodes, order, st = dm.build_tree(ss, seed=42, stats=True)
+    _same((nodes, order), ref.build_tree(seqs, seed=42))
+    if cache == "0":
+        assert st["cells_reused"] == 0
+    else:
+        assert st["cells_reused"] > 0
+    if cache == "1":
+        # the reuse the structure guarantees: every big node's center is one
+        # of its median candidates, so its sweep's distances to them are known
+        assert st["cells_reused"] > 0.05 * (st["cells"] + st["cells_reused"])
