@@ -381,18 +381,22 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
     }
     if (nj == 0) return;
     // tagged units: 4 * score (ring kernel), 256 * score (throughput kernel)
-    const int64_t bound = ((int64_t)nmmax + 2) * (sc.maxabs + std::llabs(sc.open) + std::llabs(sc.extend)) *
-                          (seq ? 256 : 4);
+    // (the throughput kernel's shifted domain, nw_seq.cuh, moves values by up
+    // to (n+m)|extend| and its scores by 2|extend|)
+    const int64_t bound = ((int64_t)nmmax + 2) *
+                          (sc.maxabs + std::llabs(sc.open) + (seq ? 4 : 1) * std::llabs(sc.extend)) * (seq ? 256 : 4);
     const bool wide = bound >= (1ll << 28);
     SeqDev sd;
     const bool prof = seq && sc.KE > 0 && sc.KE <= 8;
     if (seq) {  // 256-scaled table (TAB) or profile table K x KE (PROF), and the column map
         std::vector<int32_t> t256((size_t)sc.K * sc.Kp, 0);
         for (int x = 0; x < sc.K; ++x)
-            for (int y = 0; y < sc.K; ++y) t256[(size_t)x * sc.Kp + y] = 256 * sc.score[(size_t)x * sc.K + y];
+            for (int y = 0; y < sc.K; ++y)
+                t256[(size_t)x * sc.Kp + y] = 256 * (sc.score[(size_t)x * sc.K + y] - 2 * sc.extend);  // shifted domain
         std::vector<int32_t> pt((size_t)sc.K * std::max(sc.KE, 1), 0);
         for (int x = 0; x < sc.K; ++x)
-            for (int c = 0; c < sc.KE; ++c) pt[(size_t)x * sc.KE + c] = 256 * sc.score[(size_t)x * sc.K + sc.pdense[c]];
+            for (int c = 0; c < sc.KE; ++c)
+                pt[(size_t)x * sc.KE + c] = 256 * (sc.score[(size_t)x * sc.K + sc.pdense[c]] - 2 * sc.extend);
         char* buf = (char*)ctx->nw_seqtab.get(t256.size() * 4 + pt.size() * 4 + 128 + 64);
         int32_t* d_t = (int32_t*)buf;
         int32_t* d_p = d_t + t256.size();

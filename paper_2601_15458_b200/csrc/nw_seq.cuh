@@ -24,6 +24,13 @@
 //  * the last band of an alignment uses 12, 8 or 4 rows per lane when it has
 //    at most 384 / 256 / 128 rows, so the padded rows per alignment drop from
 //    up to 511 to at most 127 (cells_executed).
+//  * shifted domain: every state is kept as X''(i,j) = X(i,j) - (i+j)*extend
+//    (one constant per cell, so every max compares the same candidates with
+//    the same ties). Both gap chains then lose their "+ extend" (the row
+//    chain's add is gone, the column's open+extend becomes open), and the
+//    diagonal's -2*extend is folded into the score table / profiles (host,
+//    nw.cu); row 0 / column 0 become constants and the final score adds
+//    (n+m)*extend back. One IMAD per cell fewer.
 // Same recurrence, tie-breaks and trace byte (tagM | tagGB << 2 | tagGA << 4)
 // as nw_fwd.cuh / pairwise.cpp:332-372; the traceback kernel is shared.
 #pragma once
@@ -167,7 +174,7 @@ __device__ __forceinline__ void seq_band(const SeqArgs& a, const NwJob& job, uin
     const uint8_t* A = a.chars + job.a_off;
     uint8_t* T = a.trace + job.t_off;
     const V NEG = neg_inf256<V>();
-    const V O = (V)a.O, E = (V)a.E, NO = -O, EO = E + O;
+    const V O = (V)a.O, NO = -O;
     const uint32_t i0 = band * BAND + (uint32_t)g * RR + 1;
     const uint32_t tag1 = (uint32_t)a.one, tag2 = tag1 + tag1;
 
@@ -180,7 +187,7 @@ __device__ __forceinline__ void seq_band(const SeqArgs& a, const NwJob& job, uin
         if constexpr (!PROF) rowoff[r] = rc * a.Kp * 4;
         LM[r] = (V)(NEG | 2) + O;
         LGA[r] = NEG + O;
-        LGB[r] = (V)((a.O + (int64_t)i * a.E) | 1) + O;  // column 0: GB = open + i*extend
+        LGB[r] = (V)(a.O | 1) + O;  // column 0: GB = open + i*extend, i.e. open in the shifted domain
     }
     if constexpr (PROF) {
         // this lane's rows against every column symbol: [sym][quad][lane][4]
@@ -195,7 +202,7 @@ __device__ __forceinline__ void seq_band(const SeqArgs& a, const NwJob& job, uin
         }
         __syncwarp();
     }
-    V pmax = (i0 == 1 ? (V)2 : (V)((a.O + (int64_t)(i0 - 1) * a.E) | 1)) + O;
+    V pmax = (i0 == 1 ? (V)2 : (V)(a.O | 1)) + O;
     V sM = 0, sGB = 0, sGA = 0;
     // lane 0's input row (the band above, or row 0): columns 1..FIFO in flight
     constexpr int W4 = Cell4<V>::words;
@@ -267,8 +274,8 @@ __device__ __forceinline__ void seq_band(const SeqArgs& a, const NwJob& job, uin
                 }
                 const V mo = add_fma(dmax, (V)sc, a.one);                            // M + O
                 dmax = vmax3(LM[r], LGB[r], LGA[r]);                                 // old row r, + O
-                const V gao = add_fma(vmax3(LM[r], LGB[r], add_fma(LGA[r], NO, a.one)), EO, a.one);
-                const V gbraw = add_fma(vmax3(uM, uGB, uGA), E, a.one);              // the row chain
+                const V gao = add_fma(vmax3(LM[r], LGB[r], add_fma(LGA[r], NO, a.one)), O, a.one);
+                const V gbraw = vmax3(uM, uGB, uGA);  // the row chain (no extend: shifted domain)
                 // trace byte: low bytes are the tags alone (256 scale)
                 tv[r & 3] = (uint32_t)imad_u(lo32(gao), sixteen, imad_u(lo32(gbraw), four, lo32(mo)));
                 if ((r & 3) == 3) tw[r >> 2] = gather_lo(tv[0], tv[1], tv[2], tv[3]);
@@ -319,7 +326,7 @@ __device__ __forceinline__ void seq_band(const SeqArgs& a, const NwJob& job, uin
                 fGA = LGA[r];
             }
         const V fin = vmax3(fM, fGB, fGA) - O;
-        a.res[job.slot].score = (int64_t)(fin >> 8);
+        a.res[job.slot].score = (int64_t)(fin >> 8) + (int64_t)(n + m) * (a.E / 256);  // back from the shifted domain
         a.res[job.slot].final_tag = (uint32_t)(fin & 3);
     }
 }
@@ -355,8 +362,8 @@ __global__ void __launch_bounds__(SEQ_WARPS * 32, sizeof(V) == 4 ? DM_NW_SEQ_MIN
         const uint8_t* B = a.chars + job.b_off;
         for (uint32_t j = g; j <= job.m; j += 32) {
             const uint32_t ch = j ? (uint32_t)B[j - 1] & 127u : 0u;
-            Cell4<V>::store(hin + (uint64_t)j * Cell4<V>::words, (V)(NEG | 2) + O, (V)(NEG | 1),
-                            (V)(a.O + (int64_t)j * a.E) + O, PROF ? s_plut[ch] : s_lut[ch]);
+            Cell4<V>::store(hin + (uint64_t)j * Cell4<V>::words, (V)(NEG | 2) + O, (V)(NEG | 1), (V)a.O + O,
+                            PROF ? s_plut[ch] : s_lut[ch]);
         }
         __syncwarp();
         const uint32_t nb = (job.n + BAND - 1) / BAND;

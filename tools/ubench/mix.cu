@@ -48,6 +48,18 @@ __device__ __forceinline__ uint32_t shl1v(uint32_t (&v)[W], uint32_t cin, uint32
     v[0] = (v[0] << 1) | cin;
     return out;
   }
+  if constexpr (SV == 3) {  // FMA pipe: word w = v[w] * 2 + hi(v[w-1] * 2) (IMAD + IMAD.HI)
+    uint32_t out;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(out) : "r"(v[W - 1]), "r"(two));
+#pragma unroll
+    for (int w = W - 1; w > 0; --w) {
+      uint32_t h;
+      asm("mul.hi.u32 %0, %1, %2;" : "=r"(h) : "r"(v[w - 1]), "r"(two));
+      v[w] = imad(v[w], two, h);
+    }
+    v[0] = imad(v[0], two, cin);
+    return out;
+  }
   if constexpr (SV == 2) {
     uint32_t out;
     uint32_t t[W];
@@ -140,7 +152,7 @@ void run(uint32_t* d, int sms) {
     return;
   }
   const double cells = (double)blocks * 256 * cols * W * 32 * ILP;
-  const char* nm[] = {"IMAD.WIDE", "funnel", "add-chain"};
+  const char* nm[] = {"IMAD.WIDE", "funnel", "add-chain", "IMAD+IMAD.HI"};
   printf("ILP %d, blocks/SM %d, shifts Ph %s / Mh %s, Ph %s: %.1f TCUPS for the bare per-word mix (W=%d)\n", ILP,
          occ, nm[SV], nm[SVM], PH == 0 ? "IMAD" : "LOP3",
          cells / (ms * 1e-3) / 1e12, W);
@@ -159,5 +171,9 @@ int main() {
   run<1, 3, 2, 0, 1>(d, sms);
   run<1, 3, 1, 0, 2>(d, sms);
   run<2, 2, 2>(d, sms);
+  run<1, 3, 3, 0, 2>(d, sms);
+  run<1, 3, 2, 0, 3>(d, sms);
+  run<1, 3, 3, 0, 3>(d, sms);
+  run<1, 3, 3, 0, 1>(d, sms);
   return 0;
 }
