@@ -381,10 +381,10 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
     }
     if (nj == 0) return;
     // tagged units: 4 * score (ring kernel), 256 * score (throughput kernel)
-    // (the throughput kernel's shifted domain, nw_seq.cuh, moves values by up
-    // to (n+m)|extend| and its scores by 2|extend|)
-    const int64_t bound = ((int64_t)nmmax + 2) *
-                          (sc.maxabs + std::llabs(sc.open) + (seq ? 4 : 1) * std::llabs(sc.extend)) * (seq ? 256 : 4);
+    // (the shifted domain of the forward kernels, nw_seq.cuh, moves values by
+    // up to (n+m)|extend| and the scores by 2|extend|)
+    const int64_t bound = ((int64_t)nmmax + 2) * (sc.maxabs + std::llabs(sc.open) + 4 * std::llabs(sc.extend)) *
+                          (seq ? 256 : 4);
     const bool wide = bound >= (1ll << 28);
     SeqDev sd;
     const bool prof = seq && sc.KE > 0 && sc.KE <= 8;
@@ -407,10 +407,13 @@ void nw_run(dm_ctx* ctx, const uint8_t* d_chars, std::vector<NwJob>& jobs, const
         sd = SeqDev{d_t, d_p, d_pl};
     }
     const size_t smem = (size_t)sc.K * sc.Kp * 4;
-    const int32_t* d_table = ctx->nw_table.as<int32_t>(sc.table4.size());
+    // ring / cluster kernels: 4 * (s - 2 * extend), the shifted domain (nw_fwd.cuh)
+    std::vector<int32_t> t4s(sc.table4);
+    for (int x = 0; x < sc.K; ++x)
+        for (int y = 0; y < sc.K; ++y) t4s[(size_t)x * sc.Kp + y] -= (int32_t)(8 * sc.extend);
+    const int32_t* d_table = ctx->nw_table.as<int32_t>(t4s.size());
     uint8_t* d_lut = (uint8_t*)ctx->aux2.get(128);
-    DM_CUDA(cudaMemcpyAsync((void*)d_table, sc.table4.data(), sc.table4.size() * 4, cudaMemcpyHostToDevice,
-                            ctx->stream));
+    DM_CUDA(cudaMemcpyAsync((void*)d_table, t4s.data(), t4s.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
     DM_CUDA(cudaMemcpyAsync(d_lut, sc.lut, 128, cudaMemcpyHostToDevice, ctx->stream));
 
     // Larger alignments first (better tail balance), grouped by warps per

@@ -87,11 +87,11 @@ __global__ void __launch_bounds__(CL_NWW * 32, 1) nw_clu_kernel(const FwdArgs a)
     const int w = threadIdx.x >> 5;
     const uint32_t gw = crank * CL_NWW + (uint32_t)w;  // warp index in the cluster
     const V NEG = neg_inf<V>();
-    const V O4 = (V)a.O4, E4 = (V)a.E4;
+    const V O4 = (V)a.O4;
     const char* tbytes = reinterpret_cast<const char*>(s_table);
     const uint32_t tag1 = (uint32_t)a.one, tag2 = tag1 + tag1, keep = ~(tag2 + tag1);
     const uint32_t four = tag2 + tag2, sixteen = four * four;
-    const V NO4 = -O4, EO4 = E4 + O4;
+    const V NO4 = -O4;
     const int32_t* my_row = s_rows + (size_t)w * (m + 1) * 3;  // the row above this warp's bands
 
     if (jid < a.njobs) {
@@ -113,9 +113,9 @@ __global__ void __launch_bounds__(CL_NWW * 32, 1) nw_clu_kernel(const FwdArgs a)
                 rowoff[r] = (i <= n ? (int)s_lut[A[i - 1] & 127] : 0) * a.Kp * 4;
                 LM[r] = (V)(NEG | 2) + O4;
                 LGA[r] = NEG + O4;
-                LGB[r] = (V)((a.O4 + (int64_t)i * a.E4) | 1) + O4;
+                LGB[r] = (V)(a.O4 | 1) + O4;
             }
-            V pmax = (i0 == 1 ? (V)2 : (V)((a.O4 + (int64_t)(i0 - 1) * a.E4) | 1)) + O4;
+            V pmax = (i0 == 1 ? (V)2 : (V)(a.O4 | 1)) + O4;
             const uint32_t seq_in = (band / W) * (m + 1);
             const bool has_out = band + 1 < nbands;
             const uint32_t seq_out = ((band + 1) / W) * (m + 1);
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(CL_NWW * 32, 1) nw_clu_kernel(const FwdArgs a)
                         if constexpr (FIRST) {
                             iM = (V)(NEG | 2) + O4;
                             iGB = (V)(NEG | 1);
-                            iGA = (V)(a.O4 + (int64_t)(s + 1) * a.E4) + O4;
+                            iGA = (V)a.O4 + O4;  // row 0 in the shifted domain (nw_seq.cuh)
                         } else {
                             const int32_t* e = my_row + (size_t)(s + 1) * 3;
                             iM = e[0];
@@ -159,8 +159,8 @@ __global__ void __launch_bounds__(CL_NWW * 32, 1) nw_clu_kernel(const FwdArgs a)
                                 *reinterpret_cast<const int32_t*>(tbytes + add_fma(rowoff[r], cb4, a.one));
                             const V mo = add_fma(dmax, (V)sc, a.one);
                             dmax = vmax3(LM[r], LGB[r], LGA[r]);
-                            const V gao = add_fma(vmax3(LM[r], LGB[r], add_fma(LGA[r], NO4, a.one)), EO4, a.one);
-                            const V gbraw = add_fma(vmax3(uM, uGB, uGA), E4, a.one);
+                            const V gao = add_fma(vmax3(LM[r], LGB[r], add_fma(LGA[r], NO4, a.one)), O4, a.one);
+                            const V gbraw = vmax3(uM, uGB, uGA);  // shifted domain: no extend
                             tm[r & 3] = (uint32_t)mo;
                             tgb[r & 3] = (uint32_t)gbraw;
                             tga[r & 3] = (uint32_t)gao;
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(CL_NWW * 32, 1) nw_clu_kernel(const FwdArgs a)
                         fGA = LGA[r];
                     }
                 const V fin = vmax3(fM, fGB, fGA) - O4;
-                a.res[job.slot].score = (int64_t)(fin >> 2);
+                a.res[job.slot].score = (int64_t)(fin >> 2) + (int64_t)(n + m) * (a.E4 / 4);
                 a.res[job.slot].final_tag = (uint32_t)(fin & 3);
             }
             __syncwarp();

@@ -23,16 +23,19 @@
 //
 // State convention (fewer ALU ops per cell, the kernel is ALU-bound): a row
 // keeps PM = M + O4, PGB = GapB + O4, PGA = GapA + O4 (tags survive: O4 is a
-// multiple of 4). Then per cell
+// multiple of 4), all in the (i+j)*extend-shifted domain of nw_seq.cuh
+// (X'' = X - (i+j)*E4: the gap chains lose their extend adds, the score table
+// holds s - 2*E4, the final score adds (n+m)*E4 back). Then per cell
 //   diag   = max3(PM, PGB, PGA) of the row above, previous column  (= max + O4)
-//   M + O4 = diag + s                                    -> retag 2 = new PM
-//   GA + O4 = max3(PM, PGB, PGA - O4) (own row, prev col) + E4 + O4 -> & ~3 = new PGA
-//   GB     = max3(PM, GB, PGA) (row above, this column) + E4   -> retag 1; +O4 = new PGB
-// i.e. 6 ALU (3 max3, 3 retags) + 6 FMA (adds incl. the score-table address),
+//   M + O4 = diag + s - 2 E4                             -> retag 2 = new PM
+//   GA + O4 = max3(PM, PGB, PGA - O4) (own row, prev col) + O4 -> & ~3 = new PGA
+//   GB     = max3(PM, GB, PGA) (row above, this column)  -> retag 1; +O4 = new PGB
+// i.e. 6 ALU (3 max3, 3 retags) + 5 FMA (adds incl. the score-table address),
 // where the max3-of-sums form needed 4 ALU VIADDMNMX + 3 retags + 1 max3 +
 // an ALU address add. The vertical-gap chain down the 16 rows of a lane is
-// max3 -> add -> retag (13 cycles a row instead of 30 with two dependent
-// VIADDMNMX). Lanes and the band ring pass (PM, GB, PGA) of their bottom row.
+// max3 -> retag (9 cycles a row; 13 with the extend add of the unshifted
+// form, 30 with two dependent VIADDMNMX). Lanes and the band ring pass (PM,
+// GB, PGA) of their bottom row.
 #pragma once
 
 #include <type_traits>
@@ -145,12 +148,12 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
     const int g = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
     const V NEG = neg_inf<V>();
-    const V O4 = (V)a.O4, E4 = (V)a.E4;
+    const V O4 = (V)a.O4;
     const char* tbytes = reinterpret_cast<const char*>(s_table);
     // opaque ~3 / tag constants (from the runtime 1) for the one-LOP3 retags
     const uint32_t tag1 = (uint32_t)a.one, tag2 = tag1 + tag1, keep = ~(tag2 + tag1);
     const uint32_t four = tag2 + tag2, sixteen = four * four;
-    const V NO4 = -O4, EO4 = E4 + O4;
+    const V NO4 = -O4;
     for (;;) {
         __syncthreads();  // previous job fully done; table/lut loaded
         if (threadIdx.x == 0) sm.jid = atomicAdd(a.counter, 1u);
@@ -179,11 +182,11 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
                 rowoff[r] = (i <= n ? (int)sm.lut[A[i - 1] & 127] : 0) * a.Kp * 4;
                 LM[r] = (V)(NEG | 2) + O4;
                 LGA[r] = NEG + O4;
-                LGB[r] = (V)((a.O4 + (int64_t)i * a.E4) | 1) + O4;  // column 0: GB = open + i*extend
+                LGB[r] = (V)(a.O4 | 1) + O4;  // column 0: GB = open + i*extend
             }
             // row i0-1 at column 0: the first row's diagonal at column 1
             // (as the max over its three states: all the M recurrence needs), + O4
-            V pmax = (i0 == 1 ? (V)2 /* M[0][0] = 0 */ : (V)((a.O4 + (int64_t)(i0 - 1) * a.E4) | 1)) + O4;
+            V pmax = (i0 == 1 ? (V)2 /* M[0][0] = 0 */ : (V)(a.O4 | 1)) + O4;
             // ring in (from band-1) and out (to band+1); sequence = gen*(m+1)+j
             const int rin = (int)(band % NWW), rout = (int)((band + 1) % NWW);
             const uint32_t seq_in = (band / NWW) * (m + 1), seq_out = ((band + 1) / NWW) * (m + 1);
@@ -234,7 +237,7 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
                     if (band == 0) {
                         iM = (V)(NEG | 2) + O4;
                         iGB = (V)(NEG | 1);
-                        iGA = (V)(a.O4 + (int64_t)(s + 1) * a.E4) + O4;
+                        iGA = (V)a.O4 + O4;  // row 0 in the shifted domain (nw_seq.cuh)
                     } else if (NWW > 1 && rin == 0) {
                         const V* e = wrapbuf + (uint64_t)(s + 1) * 3;
                         iM = ldcg(e);
@@ -262,8 +265,8 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
                         const int32_t sc = *reinterpret_cast<const int32_t*>(tbytes + add_fma(rowoff[r], cb4, a.one));
                         const V mo = add_fma(dmax, (V)sc, a.one);                  // M + O4
                         dmax = vmax3(LM[r], LGB[r], LGA[r]);                       // old row r, + O4
-                        const V gao = add_fma(vmax3(LM[r], LGB[r], add_fma(LGA[r], NO4, a.one)), EO4, a.one);
-                        const V gbraw = add_fma(vmax3(uM, uGB, uGA), E4, a.one);   // the row chain
+                        const V gao = add_fma(vmax3(LM[r], LGB[r], add_fma(LGA[r], NO4, a.one)), O4, a.one);
+                        const V gbraw = vmax3(uM, uGB, uGA);   // the row chain (shifted domain: no extend)
                         tm[r & 3] = (uint32_t)mo;
                         tgb[r & 3] = (uint32_t)gbraw;
                         tga[r & 3] = (uint32_t)gao;
@@ -370,7 +373,7 @@ __global__ void __launch_bounds__(NWW * 32) nw_fwd_kernel(const FwdArgs a) {
                         fGA = LGA[r];
                     }
                 const V fin = vmax3(fM, fGB, fGA) - O4;
-                a.res[job.slot].score = (int64_t)(fin >> 2);
+                a.res[job.slot].score = (int64_t)(fin >> 2) + (int64_t)(n + m) * (a.E4 / 4);
                 a.res[job.slot].final_tag = (uint32_t)(fin & 3);
             }
             __syncwarp();
