@@ -312,7 +312,7 @@ def nw_micro(dm, ctx, data, offs, p_int32, npairs=65536, reps=3, cpu=True):
            "e2e_gcups": cells / (wall / reps) / 1e9,
            "roofline": {"bound": "int32", "achieved": fwd_gcups, "peak": p_int32 / C_NW / 1e9, "unit": "GCUPS",
                         "frac": fwd_gcups / (p_int32 / C_NW / 1e9),
-                        "kernel": "nw_fwd_kernel<int32,NWW> (score + trace)",
+                        "kernel": "nw_seq_kernel<int32,PROF> (throughput form: score + trace; nw_seq.cuh)",
                         "peak_source": f"measured INT32 lane-op/s {p_int32:.3e} / c_nw=13 ops per cell"}}
     if cpu:
         import oracle as _o

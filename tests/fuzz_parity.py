@@ -15,6 +15,8 @@ under `-m gpu`. What is compared, bit for bit:
   tree     dm_build_tree                         vs build_tree (cluster_tree.cpp:168-235)
   msa      dm_msa                                vs build_tree + align_all (msa_merge.cpp:107-158)
   align    dm_align_sequences (duplicates)       vs align_sequences (pipeline.cpp:78-159)
+  fasta    dm_run_align: FASTA in, aligned FASTA + tree / dedup dumps out vs run_align (pipeline.cpp:160-187)
+  metrics  dm_evaluate                           vs evaluate (metrics.cpp:84-169)
 """
 import argparse
 import os
@@ -319,7 +321,76 @@ class Campaign:
         return f"{kind} n {len(seqs)} alphabet {abet} knobs {kn.set}", \
             None if got == want else f"{got[0]} vs {want[0]}: {str(got[1])[:80]} / {str(want[1])[:80]}"
 
-    CASES = ("lev", "packed", "scan", "nw", "tree", "msa", "align")
+    # -- FASTA pipeline and metrics (the path's callers) ------------------------
+    def case_fasta(self, rng):
+        import tempfile
+        kind = rng.choice(("nt", "aa"))
+        alpha = ALPHABETS["dna" if kind == "nt" else "aa"]
+        seqs = self._family_set(rng, alpha, rng.choice((4, 30, 120)), rng.choice((20, 150, 400)))
+        seqs += [rng.choice(seqs) for _ in range(rng.randint(0, len(seqs) // 2))]  # duplicates: re-expanded
+        rng.shuffle(seqs)
+        lines = []
+        for k, sq in enumerate(seqs):
+            desc = rng.choice(("", " sample", " a  b\tc", " len=%d" % len(sq)))
+            lines.append(f">s{k}{desc}")
+            if rng.random() < 0.3:
+                sq = "".join(c.lower() if rng.random() < 0.5 else c for c in sq)  # normalised by the parser
+            w = rng.choice((1, 7, 60, 80, 10 ** 6))
+            for x in range(0, len(sq), w):
+                lines.append(sq[x:x + w] + rng.choice(("", "", " ", "\r")))
+            if rng.random() < 0.2:
+                lines.append("")
+        text = "\n".join(lines) + rng.choice(("\n", "", "\n\n"))
+        abet, order = rng.choice(("auto", kind)), rng.choice(("tree", "input"))
+        go = -rng.randint(1, 12)
+        ge = -rng.randint(0, min(3, -go))
+        mode = rng.choice(("affine", "flat"))
+        with tempfile.TemporaryDirectory() as d, Knobs(rng, ("DM_TREE_BG", "DM_NW_SEQ", "DM_NW_CLU")) as kn:
+            inp = os.path.join(d, "in.fa")
+            with open(inp, "w", newline="") as f:
+                f.write(text)
+
+            def side(tag, fn):
+                paths = [os.path.join(d, f"{tag}.{x}") for x in ("fa", "tree", "dedup")]
+                try:
+                    fn(*paths)
+                except Exception as e:
+                    return ("error", str(e))
+                return ("files", [open(q, "rb").read() if os.path.exists(q) else None for q in paths])
+
+            got = side("g", lambda o, t, u: self.dm.run_align(inp, o, alphabet=abet, gap_open=go, gap_extend=ge,
+                                                              gap_mode=mode, order=order, dump_tree=t, dump_dedup=u,
+                                                              ctx=self.ctx))
+            want = side("r", lambda o, t, u: self.ref.run_align(inp, o, alphabet=abet, gap_open=go, gap_extend=ge,
+                                                                flat=mode == "flat", order=order, dump_tree=t,
+                                                                dump_dedup=u))
+        desc = f"{kind} records {len(seqs)} alphabet {abet} order {order} go {go} ge {ge} {mode} knobs {kn.set}"
+        if got == want:
+            return desc, None
+        if got[0] != want[0]:
+            return desc, f"{got[0]} vs {want[0]}: {str(got[1])[:80]} / {str(want[1])[:80]}"
+        if got[0] == "error":
+            return desc, f"error text differs: {got[1][:80]} / {want[1][:80]}"
+        which = [n for n, x, y in zip(("fasta", "tree dump", "dedup dump"), got[1], want[1]) if x != y]
+        return desc, "differs: " + ", ".join(which)
+
+    def case_metrics(self, rng):
+        kind = rng.choice(("nt", "aa"))
+        alpha = ALPHABETS["dna" if kind == "nt" else "aa"]
+        seqs = self._family_set(rng, alpha, rng.choice((4, 40, 200)), rng.choice((20, 150, 500)))
+        sc = (self.dm.ScoringScheme.nucleotide if kind == "nt" else self.dm.ScoringScheme.protein)()
+        m = self.dm.msa(self.dm.SeqSet(seqs, self.ctx), sc)
+        ss, pb, seed = rng.choice((3, 50, 10000)), rng.choice((1, 20, 100000)), rng.choice((42, 5))
+        got = self.dm.evaluate(m, seqs, sample_size=ss, pair_budget=pb, seed=seed, ctx=self.ctx)
+        want = self.ref.evaluate(list(m.rows), m.row_to_sequence, seqs, sample_size=ss, pair_budget=pb, seed=seed)
+        fields = ("width", "stretch", "gap_percent", "distortion", "p_min", "p_avg", "p_max", "sample_size",
+                  "pair_count", "seed", "zero_distance_pairs")
+        bad = [k for k in fields if got[k] != want[k]]
+        return f"{kind} n {len(seqs)} sample {ss} budget {pb} seed {seed}", \
+            None if not bad else f"fields differ: {[(k, got[k], want[k]) for k in bad][:3]}"
+
+
+    CASES = ("lev", "packed", "scan", "nw", "tree", "msa", "align", "fasta", "metrics")
 
     def run(self, seconds, kinds=None, log=print, max_cases=None):
         kinds = list(kinds or self.CASES)
