@@ -83,8 +83,44 @@ __device__ __forceinline__ uint4 trace_chunk16(const uint8_t* T, uint32_t n, uin
 constexpr int TC = 32;  // tile columns (one per lane)
 constexpr int TR = 64;  // tile rows (bytes per column)
 
+// trace_chunk16 into shared memory with cp.async (the prefetched tile)
+__device__ __forceinline__ void cp_async_n(void* smem, const void* gmem, int bytes) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    if (bytes == 16) asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void trace_chunk16_async(uint8_t* dst, const uint8_t* T, uint32_t n, uint32_t m, uint32_t pa,
+                                                    int diag, uint32_t R, uint32_t j) {
+    if (!diag) {
+        cp_async_n(dst, T + (uint64_t)(j - 1) * pa + R, 16);
+        return;
+    }
+    const uint32_t b = R / nwk::BAND, nb = (n + nwk::BAND - 1) / nwk::BAND;
+    const uint32_t rr = b + 1 < nb ? 16u : nwk::seq_tail_rr(n - b * nwk::BAND);
+    const uint8_t* base = T + (uint64_t)b * (m + 31) * nwk::BAND;
+    const uint32_t l = R - b * nwk::BAND;
+    if (rr == 16) {
+        const uint32_t g = l / 16;
+        cp_async_n(dst, base + (uint64_t)(j + g - 1) * 512 + g * 16, 16);
+        return;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t row = l + 4 * q, g = row / rr, r = row - g * rr;
+        cp_async_n(dst + 4 * q, base + (uint64_t)(j + g - 1) * 32 * rr + g * rr + r, 4);
+    }
+}
+
+// Warp per alignment. The path is walked by lane 0 inside a 32-column x
+// 64-row tile of trace bytes staged in shared memory (lane g loads column
+// jtop - g); while it walks, the tile the path most likely enters next (32
+// columns to the left, rows following the diagonal) is prefetched with
+// cp.async into the other buffer and used if the walk really ended there
+// (else the tile is staged again at the walk's position, as for the first).
+// The walk itself is branch-free: the state selects its 2-bit field of the
+// trace byte by a shift, the gap lists are written under predicates.
 __global__ void __launch_bounds__(128) nw_traceback_kernel(const TbArgs a) {
-    __shared__ __align__(16) uint8_t tile[4][TC][TR];
+    __shared__ __align__(16) uint8_t tile[4][2][TC][TR];
     const int g = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
     for (;;) {
@@ -101,42 +137,62 @@ __global__ void __launch_bounds__(128) nw_traceback_kernel(const TbArgs a) {
         NwRes& res = a.res[job.slot];
         uint32_t state = 2u - res.final_tag;  // 0 M, 1 GapB, 2 GapA
         uint32_t i = n, j = job.m, len = 0, nga = 0, ngb = 0;
+        int buf = 0;
+        bool have = false;   // tile[w][buf] already holds the tile (jtop = j, rows from r0)
+        int r0 = 0;
         while (i > 0 && j > 0) {
             const uint32_t jtop = j;
-            const int r0 = max(0, (int)((i - 1) & ~15u) - (TR - 16));
-            const int jc = (int)jtop - g;
-            if (jc >= 1) {
-                uint4* dst = reinterpret_cast<uint4*>(&tile[w][g][0]);
+            if (!have) {
+                r0 = max(0, (int)((i - 1) & ~15u) - (TR - 16));
+                const int jc = (int)jtop - g;
+                if (jc >= 1) {
+                    uint4* dst = reinterpret_cast<uint4*>(&tile[w][buf][g][0]);
 #pragma unroll
-                for (int q = 0; q < TR / 16; ++q)
-                    if ((uint32_t)(r0 + q * 16) < pa)
-                        dst[q] = trace_chunk16(T, n, job.m, pa, a.diag, (uint32_t)(r0 + q * 16), (uint32_t)jc);
+                    for (int q = 0; q < TR / 16; ++q)
+                        if ((uint32_t)(r0 + q * 16) < pa)
+                            dst[q] = trace_chunk16(T, n, job.m, pa, a.diag, (uint32_t)(r0 + q * 16), (uint32_t)jc);
+                }
             }
+            // the likely next tile: columns jtop-32 .. jtop-63, rows for a path near the diagonal
+            const bool pf = jtop > (uint32_t)TC && i > 24;
+            const uint32_t jtop_n = jtop - TC;
+            const int r0n = pf ? max(0, (int)((i - 25) & ~15u) - (TR - 16)) : 0;
+            if (pf) {
+                const int jc = (int)jtop_n - g;
+                if (jc >= 1) {
+#pragma unroll
+                    for (int q = 0; q < TR / 16; ++q)
+                        if ((uint32_t)(r0n + q * 16) < pa)
+                            trace_chunk16_async(&tile[w][buf ^ 1][g][q * 16], T, n, job.m, pa, a.diag,
+                                                (uint32_t)(r0n + q * 16), (uint32_t)jc);
+                }
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
             __syncwarp();
             if (g == 0) {
                 // pairwise.cpp:384-409, inside the staged tile
+                const uint8_t* tb = &tile[w][buf][0][0];
                 while (i > 0 && j > 0 && jtop - j < (uint32_t)TC && (int)(i - 1) >= r0) {
-                    const uint32_t code = tile[w][jtop - j][(i - 1) - r0];
+                    const uint32_t code = tb[(jtop - j) * TR + ((i - 1) - r0)];
                     ++len;
-                    if (state == 0) {
-                        state = 2u - (code & 3u);
-                        --i;
-                        --j;
-                    } else if (state == 1) {
-                        gb[ngb++] = j;
-                        state = 2u - ((code >> 2) & 3u);
-                        --i;
-                    } else {
-                        ga[nga++] = i;
-                        state = 2u - ((code >> 4) & 3u);
-                        --j;
-                    }
+                    const uint32_t nxt = 2u - ((code >> (2u * state)) & 3u);
+                    if (state == 1) gb[ngb++] = j;
+                    if (state == 2) ga[nga++] = i;
+                    i -= state != 2u;
+                    j -= state != 1u;
+                    state = nxt;
                 }
             }
             i = __shfl_sync(FULL, i, 0);
             j = __shfl_sync(FULL, j, 0);
             state = __shfl_sync(FULL, state, 0);
+            asm volatile("cp.async.wait_all;" ::: "memory");
             __syncwarp();
+            have = pf && j == jtop_n && i > 0 && (int)(i - 1) >= r0n && (int)(i - 1) < r0n + TR;
+            if (have) {
+                buf ^= 1;
+                r0 = r0n;
+            }
         }
         if (g == 0) {
             // row 0 is all GapA, column 0 all GapB (pairwise.cpp:322-339)
