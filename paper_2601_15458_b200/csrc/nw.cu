@@ -170,18 +170,36 @@ __global__ void __launch_bounds__(128) nw_traceback_kernel(const TbArgs a) {
             asm volatile("cp.async.commit_group;" ::: "memory");
             __syncwarp();
             if (g == 0) {
-                // pairwise.cpp:384-409, inside the staged tile
+                // pairwise.cpp:384-409 inside the staged tile, in tile coordinates:
+                // column c = jtop - j (j > 0 <=> c < jtop), row r = (i - 1) - r0
+                // (r >= 0 implies i > 0). One dependent chain per step: trace byte ->
+                // the state's 2-bit field -> next state -> r / c; the gap lists
+                // (GapB records j, GapA records i) are written under predicates.
                 const uint8_t* tb = &tile[w][buf][0][0];
-                while (i > 0 && j > 0 && jtop - j < (uint32_t)TC && (int)(i - 1) >= r0) {
-                    const uint32_t code = tb[(jtop - j) * TR + ((i - 1) - r0)];
+                int c = 0, r = (int)(i - 1) - r0;
+                const int cmax = (int)min((uint32_t)TC, jtop);
+                uint32_t st = state;
+                while (r >= 0 && c < cmax) {
+                    const uint32_t code = tb[c * TR + r];
+                    const uint32_t nxt = 2u - ((code >> (st + st)) & 3u);
+                    asm volatile(
+                        "{ .reg .pred p, q;\n"
+                        "  setp.eq.u32 p, %4, 1;\n"
+                        "  setp.eq.u32 q, %4, 2;\n"
+                        "  @p st.global.u32 [%0], %1;\n"
+                        "  @q st.global.u32 [%2], %3; }" ::"l"(gb + ngb),
+                        "r"(jtop - (uint32_t)c), "l"(ga + nga), "r"((uint32_t)(r + r0 + 1)), "r"(st)
+                        : "memory");
+                    ngb += st == 1u;
+                    nga += st == 2u;
+                    r -= st != 2u;
+                    c += st != 1u;
+                    st = nxt;
                     ++len;
-                    const uint32_t nxt = 2u - ((code >> (2u * state)) & 3u);
-                    if (state == 1) gb[ngb++] = j;
-                    if (state == 2) ga[nga++] = i;
-                    i -= state != 2u;
-                    j -= state != 1u;
-                    state = nxt;
                 }
+                i = (uint32_t)(r + r0 + 1);
+                j = jtop - (uint32_t)c;
+                state = st;
             }
             i = __shfl_sync(FULL, i, 0);
             j = __shfl_sync(FULL, j, 0);
