@@ -44,7 +44,9 @@ Multi-GPU (torchrun): every rank runs the same cfg1 batch independently
 (weak scaling, no data-path collective; barrier + max-over-ranks timing).
 The msa key is then strong-scaled: cfg4 (and cfg2) sharded across the ranks
 inside libdmb200 (NCCL all-gather of distance shards and merge results),
-every rank's rows checked against the reference's SHA.
+every rank's rows checked against the reference's SHA. The sharded leg runs
+under a timer (--msa-timeout-s): if a collective never completes, rank 0
+still prints the finished cfg1 line, with the msa key saying so.
 """
 from __future__ import annotations
 
@@ -400,6 +402,8 @@ def main():
     ap.add_argument("--no-nw", action="store_true", help="skip the NW micro-benchmark")
     ap.add_argument("--msa", default="2,4", help="MSA configs for the msa key (comma list; '' to skip)")
     ap.add_argument("--msa-reps", type=int, default=3)
+    ap.add_argument("--msa-timeout-s", type=float, default=420.0,
+                    help="several ranks: give the sharded msa key this long, then print the line without it")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -594,16 +598,35 @@ def main():
         line["cpu_baseline"] = cpu_baseline(data, offs, n_pairs, args.cpu_budget_s)
     if args.msa:
         del data, offs, pinned
-        if world > 1:  # the MSA job is sharded across the ranks inside libdmb200 (strong scaling)
-            from paper_2601_15458_b200 import dist as dmdist
-            dmdist.attach_from_torch(ctx)
+        watchdog = None
+        if world > 1:
+            # The MSA job is sharded across the ranks inside libdmb200 (strong
+            # scaling). Its collectives block in native code, so a rank that
+            # never arrives would hang every other one: each rank arms a
+            # timer that prints the (complete) cfg1 line without the msa key
+            # and ends the process.
+            def _give_up():
+                if rank == 0:
+                    line["msa"] = {"error": f"no result within {args.msa_timeout_s:.0f} s (sharded msa key abandoned)"}
+                    line["msa_scaling"] = "strong (one MSA job sharded across the ranks)"
+                    print(json.dumps(line), flush=True)
+                os._exit(0)
+
+            watchdog = threading.Timer(args.msa_timeout_s, _give_up)
+            watchdog.daemon = True
+            watchdog.start()
         cfgs = [(int(c), 1.0) for c in args.msa.split(",") if c]
         try:
+            if world > 1:
+                from paper_2601_15458_b200 import dist as dmdist
+                dmdist.attach_from_torch(ctx)
             line["msa"] = msa_bench(dm, ctx, cfgs, args.msa_reps, world, rank)
         except SystemExit:
             raise
         except Exception as e:  # noqa: BLE001 -- the distance metric above stands; record why msa failed
             line["msa"] = {"error": f"{type(e).__name__}: {e}"}
+        if watchdog is not None:
+            watchdog.cancel()
         line["msa_scaling"] = "strong (one MSA job sharded across the ranks)" if world > 1 else "1 GPU"
     if rank == 0:
         print(json.dumps(line), flush=True)
